@@ -1,0 +1,185 @@
+/*
+ * ficco.h — C-ABI of the B200-native FiCCO executor (libficco_b200.so).
+ *
+ * The reference (overlap_sim 0.1.0, /root/reference/pkg) is a pure-Python
+ * simulator: its only "executor" is engine.simulate(plan, machine, topo,
+ * model) (/root/reference/pkg/src/overlap_sim/engine.py:117), which prices the
+ * Transfer/Gather/Gemm/Scatter DAG produced by planner.build_plan
+ * (/root/reference/pkg/src/overlap_sim/planner.py:409). This library is the
+ * real executor that takes that slot: the Python layer lowers an
+ * ExecutionPlan (per rank) into
+ *   - a COPY PROGRAM run on a dedicated copy stream: copy-engine peer copies
+ *     (cudaMemcpyBatchAsync / cudaMemcpy2DAsync, no SMs) interleaved with
+ *     stream memory operations that publish per-chunk readiness flags, and
+ *   - a TILE PROGRAM run by one persistent tcgen05/TMEM/TMA kernel on the
+ *     compute stream whose producer warp gates each tile's TMA loads on those
+ *     flags (no host round trip).
+ * Each reference TaskSpec maps as follows:
+ *   TransferSpec (planner.py:58-64)  -> FICCO_OP_COPY + FICCO_OP_SIGNAL
+ *   GatherSpec   (planner.py:67-69)  -> folded: copies land in place
+ *   GemmSpec     (planner.py:77-89)  -> ficco_tile entries (rows/col_block)
+ *   ScatterSpec  (planner.py:72-74)  -> folded: epilogue writes C in place
+ *   Task.deps    (planner.py:95-100) -> flag waits (copy stream or kernel)
+ *
+ * All device buffers are caller-owned except the symmetric workspace, which
+ * the library allocates (ficco_ws_alloc) so it can be shared across ranks by
+ * CUDA IPC. No C++ exception crosses this boundary: every entry point returns
+ * 0 on success or a negative FICCO_E* code; ficco_last_error() gives the
+ * thread-local message. Streams are cudaStream_t passed as void*.
+ */
+#ifndef FICCO_H_
+#define FICCO_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define FICCO_ABI_VERSION 1
+
+/* status codes */
+#define FICCO_OK 0
+#define FICCO_EINVAL (-1)   /* bad argument (maps to ValueError / PlanError) */
+#define FICCO_ECUDA (-2)    /* CUDA runtime/driver failure (RuntimeError) */
+#define FICCO_ETIMEOUT (-3) /* a readiness flag never arrived (DeadlockError) */
+#define FICCO_ENODEV (-4)   /* no sm_100 device */
+
+/* symmetric workspace layout: flag words first, data after FICCO_WS_DATA_OFFSET */
+#define FICCO_WS_FLAG_WORDS 16384
+#define FICCO_WS_DATA_OFFSET (FICCO_WS_FLAG_WORDS * 4)
+#define FICCO_FLAG_ABORT (FICCO_WS_FLAG_WORDS - 1) /* kernel-side timeout indicator */
+#define FICCO_FLAG_COUNTERS 12288                  /* per-chunk tile counters (reset per run) */
+
+/* copy-program opcodes (executed in order on the copy stream) */
+#define FICCO_OP_COPY 0        /* copy width x height bytes src(peer buf) -> dst(local buf) */
+#define FICCO_OP_SIGNAL 1      /* local flag[flag] = epoch (after everything before it) */
+#define FICCO_OP_NOTIFY 2      /* flag[flag] of rank `peer` = epoch (remote write over NVLink) */
+#define FICCO_OP_WAIT 3        /* copy stream waits until local flag[flag] >= epoch - value */
+#define FICCO_OP_WAIT_COUNTER 4 /* copy stream waits until local counter[flag] >= value */
+
+/* buffer ids */
+#define FICCO_BUF_NONE 0
+#define FICCO_BUF_A 1   /* call argument a */
+#define FICCO_BUF_B 2   /* call argument b */
+#define FICCO_BUF_C 3   /* call argument c */
+#define FICCO_BUF_WS 4  /* symmetric workspace of rank `peer` (local rank for dst) */
+
+/* epilogue modes of a tile */
+#define FICCO_EPI_STORE 0        /* out[c] = bf16(alpha * acc) */
+#define FICCO_EPI_STORE_SIGNAL 1 /* partial[c] = bf16(acc); counter[chunk] += 1 when the tile is stored */
+#define FICCO_EPI_REDUCE 2       /* out[c] = bf16(acc + sum_j recv_j[...]) after rs flags of `chunk` */
+
+typedef struct ficco_comm ficco_comm_t;
+typedef struct ficco_plan ficco_plan_t;
+
+typedef struct {
+  int32_t op;       /* FICCO_OP_* */
+  int32_t peer;     /* source rank of a COPY (pull) / target rank of a NOTIFY */
+  int32_t flag;     /* flag / counter word index */
+  int32_t src_buf;  /* FICCO_BUF_* */
+  int32_t dst_buf;  /* FICCO_BUF_* (WS means the local workspace, or `dst_peer`'s when push) */
+  int32_t dst_peer; /* -1: local; else rank whose workspace receives the bytes (push) */
+  int64_t src_off, dst_off;     /* bytes from buffer base */
+  int64_t src_par, dst_par;     /* added once per odd epoch (double-buffered workspaces) */
+  int64_t width, height;        /* bytes per row, rows (height 1 = 1D copy) */
+  int64_t src_pitch, dst_pitch; /* bytes between rows (2D) */
+  uint32_t value;               /* WAIT_COUNTER threshold */
+  uint32_t reserved;
+} ficco_copy_op;
+
+typedef struct {
+  int32_t a_row;  /* row coordinate of the 128-row A box (TMA) */
+  int32_t b_row;  /* row coordinate of the 256-row B box (TMA) */
+  int32_t c_row;  /* first output row */
+  int32_t c_col;  /* first output column */
+  int16_t rows;   /* valid output rows (<= 128) */
+  int16_t cols;   /* valid output columns (<= 256, multiple of 32) */
+  int16_t flag;   /* first readiness flag gating the A/B loads (-1: none) */
+  int16_t kseg;   /* k-blocks (64 elements) per flag segment (0: one flag for the tile) */
+  int16_t mode;   /* FICCO_EPI_* */
+  int16_t chunk;  /* counter index (STORE_SIGNAL) or rs-flag group (REDUCE) */
+  int32_t recv_row; /* REDUCE: row offset into every receive slot */
+} ficco_tile;
+
+typedef struct {
+  int32_t buf;      /* FICCO_BUF_* (WS = local workspace) */
+  int32_t pad;
+  int64_t off;      /* bytes */
+  int64_t par;      /* extra bytes on odd epochs */
+  int64_t rows;     /* rows of the row-major bf16 matrix */
+  int64_t ld;       /* elements between rows */
+} ficco_operand;
+
+typedef struct {
+  int32_t n_ops;
+  int32_t n_tiles;
+  const ficco_copy_op* ops;
+  const ficco_tile* tiles;
+  ficco_operand a;    /* M x K, K contiguous (TMA box 128 x 64) */
+  ficco_operand b;    /* N x K, K contiguous (TMA box 256 x 64) */
+  ficco_operand c;    /* output, bf16 */
+  ficco_operand part; /* STORE_SIGNAL destination (RS partials) */
+  ficco_operand recv; /* REDUCE sources: slot j at off + j*recv_slot (+par on odd epochs) */
+  int64_t recv_slot;  /* bytes between receive slots */
+  int64_t k;          /* reduction length in elements (multiple of 8) */
+  int32_t n_recv;     /* receive slots summed by REDUCE tiles */
+  int32_t rs_flag0;   /* first rs flag word; REDUCE waits flag[rs_flag0 + chunk*n_recv + j] */
+  int32_t n_counters; /* counters [0, n_counters) reset to 0 before each run */
+  int32_t grid;       /* persistent CTAs (0: one per SM) */
+  float alpha;        /* epilogue scale (STORE) */
+  int32_t reserved;
+} ficco_plan_desc;
+
+int ficco_abi_version(void);
+const char* ficco_last_error(void);
+
+/* device / workspace / IPC */
+int ficco_device_info(int device, int* sm_count, int* cc_major, int* cc_minor);
+int ficco_ws_alloc(size_t bytes, void** out);
+int ficco_ws_free(void* ptr);
+int ficco_ipc_handle_size(void);
+int ficco_ipc_get_handle(void* ptr, void* out_handle);
+int ficco_ipc_open(const void* handle, void** out);
+int ficco_ipc_close(void* ptr);
+
+/* communicator: ws[r] = rank r's workspace as mapped in this process.
+ * virtual_peers=1: a single process plays rank `rank` of `world`; peers'
+ * workspaces are local allocations and cross-rank waits/notifies are
+ * satisfied locally (decomposition-only mode). */
+int ficco_comm_create(int rank, int world, void* const* ws, size_t ws_bytes, int virtual_peers,
+                      ficco_comm_t** out);
+int ficco_comm_destroy(ficco_comm_t* comm);
+int ficco_comm_epoch(ficco_comm_t* comm, uint32_t* epoch);
+/* blocks until all work of the communicator finished; FICCO_ETIMEOUT if a kernel hit its flag timeout */
+int ficco_comm_check(ficco_comm_t* comm, void* stream);
+/* set local flag words [first, first+count) to value (stream-ordered on `stream`) */
+int ficco_comm_set_flags(ficco_comm_t* comm, int first, int count, uint32_t value, void* stream);
+
+/* plans */
+int ficco_plan_create(ficco_comm_t* comm, const ficco_plan_desc* desc, ficco_plan_t** out);
+int ficco_plan_destroy(ficco_plan_t* plan);
+/* one execution: copy program on the comm's copy stream, tile kernel on `stream`,
+ * joined back into `stream`; advances the comm epoch. Non-blocking. */
+int ficco_plan_run(ficco_plan_t* plan, const void* a, const void* b, void* c, void* stream);
+/* only the copy program / only the tile kernel (for calibration of DIL/CIL) */
+int ficco_plan_run_parts(ficco_plan_t* plan, const void* a, const void* b, void* c, void* stream,
+                         int run_copies, int run_tiles);
+
+/* stand-alone primitives (calibration, benchmarks) */
+int ficco_gemm_bf16(const void* a, const void* b, void* c, int64_t m, int64_t n, int64_t k, float alpha,
+                    int grid, void* stream);
+int ficco_copy_batch(void* const* dsts, const void* const* srcs, const size_t* sizes, size_t count,
+                     void* stream);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* FICCO_H_ */

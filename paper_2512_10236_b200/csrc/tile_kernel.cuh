@@ -1,0 +1,262 @@
+// Persistent, flag-gated tcgen05 tile kernel: the compute half of every FiCCO schedule.
+//
+// One CTA per SM walks a host-lowered tile list (ficco_tile) in order; tile t
+// goes to CTA t mod gridDim.x. Warp roles (192 threads):
+//   warp 0      TMA producer: waits the tile's readiness flag(s) (written by
+//               copy-engine stream memops or by peers), then streams 128x64 A
+//               and 256x64 B boxes (128B swizzle) into a STAGES-deep ring.
+//   warp 1      MMA issuer: one elected thread issues tcgen05.mma
+//               (kind::f16, M=128 N=256 K=16) into one of two TMEM accumulators
+//               (2 x 256 fp32 columns) so the epilogue of tile i overlaps the
+//               MMAs of tile i+1.
+//   warps 2-5   epilogue: tcgen05.ld 32x32b (one accumulator row per thread),
+//               scale / reduce, bf16 pack, masked 16-byte stores at
+//               (c_row, c_col) — the reference's ScatterSpec folded into the
+//               store addressing (planner.py:262-271).
+//
+// A schedule kind is nothing but a tile ORDER plus a DEPENDENCY SET:
+//   uniform_fused_1d  step-major tiles, each gated on its round's flag
+//   hetero_*_1d       local-shard tiles first (no wait), then rounds
+//   uniform_fused_2d  output-stationary tiles, k-block kb gated on round kb/kseg
+//                     (TMEM-resident accumulation replaces the chained additive
+//                     GEMMs of planner.py:368-383)
+//   shard_overlap     shard-major tiles gated on the ring step's flag
+#pragma once
+
+#include "../../include/ficco.h"
+#include "sm100_primitives.cuh"
+
+namespace ficco {
+
+constexpr int BM = 128;
+constexpr int BN = 256;
+constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle row
+constexpr int UMMA_K = 16;
+constexpr int STAGES = 4;
+constexpr int A_STAGE = BM * BK * 2;  // 16 KiB
+constexpr int B_STAGE = BN * BK * 2;  // 32 KiB
+constexpr int NUM_THREADS = 192;
+constexpr int EPI_THREADS = 128;
+constexpr uint32_t TMEM_COLS = 512;  // two 128x256 fp32 accumulators
+constexpr int MAX_RECV = 15;
+constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * (A_STAGE + B_STAGE) + 256;
+constexpr uint32_t SPIN_LIMIT = 1u << 25;  // ~4-10 s of polling before declaring a timeout
+
+struct alignas(64) TileParams {
+  CUtensorMap tmap_a;
+  CUtensorMap tmap_b;
+  const ficco_tile* tiles;
+  int num_tiles;
+  int num_kb;
+  __nv_bfloat16* out;      // STORE / REDUCE destination
+  __nv_bfloat16* part;     // STORE_SIGNAL destination
+  int64_t ld_out;
+  int64_t ld_part;
+  const __nv_bfloat16* recv[MAX_RECV];
+  int64_t ld_recv;
+  int n_recv;
+  int rs_flag0;
+  uint32_t* flags;         // local flag words
+  uint32_t* counters;      // local tile counters
+  uint32_t* abort_word;
+  uint32_t epoch;
+  float alpha;
+};
+
+// Poll a flag written by another agent (copy engine memop, peer GPU) until it
+// reaches `epoch` (wrap-safe). On timeout raise the abort word and give up so
+// the kernel drains instead of hanging the device.
+__device__ __forceinline__ void wait_flag(const uint32_t* f, uint32_t epoch, uint32_t* abort_word) {
+  uint32_t spins = 0;
+  while (static_cast<int32_t>(ld_acquire_sys(f) - epoch) < 0) {
+    if (++spins >= SPIN_LIMIT) {
+      atomicExch(abort_word, 1u);
+      break;
+    }
+    if ((spins & 1023u) == 0 && *reinterpret_cast<volatile uint32_t*>(abort_word)) break;
+    __nanosleep(64);
+  }
+  // make the copy-engine-written bytes visible to the async (TMA) proxy
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+__device__ __forceinline__ void producer_loop(const TileParams& p, uint8_t* sA, uint8_t* sB, uint64_t* full,
+                                              uint64_t* empty) {
+  const uint64_t hint_a = policy_evict_first();
+  const uint64_t hint_b = policy_evict_last();
+  uint32_t stage = 0, phase = 0;
+  for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+    const ficco_tile td = p.tiles[t];
+    for (int kb = 0; kb < p.num_kb; ++kb) {
+      if (td.flag >= 0) {
+        if (td.kseg == 0) {
+          if (kb == 0) wait_flag(p.flags + td.flag, p.epoch, p.abort_word);
+        } else if (kb % td.kseg == 0) {
+          wait_flag(p.flags + td.flag + kb / td.kseg, p.epoch, p.abort_word);
+        }
+      }
+      mbar_wait(&empty[stage], phase ^ 1u);
+      mbar_arrive_expect_tx(&full[stage], A_STAGE + B_STAGE);
+      tma_load_2d(sA + stage * A_STAGE, &p.tmap_a, &full[stage], kb * BK, td.a_row, hint_a);
+      tma_load_2d(sB + stage * B_STAGE, &p.tmap_b, &full[stage], kb * BK, td.b_row, hint_b);
+      if (++stage == STAGES) {
+        stage = 0;
+        phase ^= 1u;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void mma_loop(const TileParams& p, uint8_t* sA, uint8_t* sB, uint64_t* full,
+                                         uint64_t* empty, uint64_t* tfull, uint64_t* tempty, uint32_t tmem) {
+  constexpr uint32_t idesc = make_idesc_bf16(BM, BN);
+  uint32_t stage = 0, phase = 0, it = 0;
+  for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
+    const uint32_t acc = it & 1u;
+    mbar_wait(&tempty[acc], ((it >> 1) & 1u) ^ 1u);
+    tc_fence_after();
+    const uint32_t d = tmem + acc * BN;
+    for (int kb = 0; kb < p.num_kb; ++kb) {
+      mbar_wait(&full[stage], phase);
+      tc_fence_after();
+      const uint64_t ad = make_sdesc_sw128(smem_addr(sA + stage * A_STAGE));
+      const uint64_t bd = make_sdesc_sw128(smem_addr(sB + stage * B_STAGE));
+#pragma unroll
+      for (int k = 0; k < BK / UMMA_K; ++k) {
+        // +32 bytes per K step inside the 128B swizzle row (>>4 in the descriptor)
+        umma_bf16(d, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc, (kb | k) != 0);
+      }
+      umma_commit(&empty[stage]);  // smem slot free once these MMAs retire
+      if (++stage == STAGES) {
+        stage = 0;
+        phase ^= 1u;
+      }
+    }
+    umma_commit(&tfull[acc]);  // accumulator complete
+  }
+}
+
+__device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfull, uint64_t* tempty,
+                                              uint32_t tmem) {
+  const int warp = threadIdx.x / 32;
+  const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+  const int row = quarter * 32 + (threadIdx.x & 31);
+  uint32_t it = 0;
+  for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
+    const ficco_tile td = p.tiles[t];
+    const uint32_t acc = it & 1u;
+    if (td.mode == FICCO_EPI_REDUCE) {
+      // peers' partial chunks must have landed in our receive slots
+      if (threadIdx.x == 64) {
+        for (int j = 0; j < p.n_recv; ++j)
+          wait_flag(p.flags + p.rs_flag0 + td.chunk * p.n_recv + j, p.epoch, p.abort_word);
+      }
+      named_bar_sync(1, EPI_THREADS);
+    }
+    mbar_wait(&tfull[acc], (it >> 1) & 1u);
+    tc_fence_after();
+    const uint32_t taddr = tmem + (uint32_t(quarter * 32) << 16) + acc * BN;
+    const bool row_ok = row < td.rows;
+    __nv_bfloat16* dst;
+    if (td.mode == FICCO_EPI_STORE_SIGNAL)
+      dst = p.part + int64_t(td.c_row + row) * p.ld_part + td.c_col;
+    else
+      dst = p.out + int64_t(td.c_row + row) * p.ld_out + td.c_col;
+    const float scale = td.mode == FICCO_EPI_STORE ? p.alpha : 1.0f;
+#pragma unroll 1
+    for (int cc = 0; cc < BN / 32; ++cc) {
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(taddr + cc * 32, v);
+      tmem_ld_wait();
+      if (row_ok && cc * 32 < td.cols) {
+        float f[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]) * scale;
+        if (td.mode == FICCO_EPI_REDUCE) {
+          for (int j = 0; j < p.n_recv; ++j) {
+            const uint4* src = reinterpret_cast<const uint4*>(p.recv[j] + int64_t(td.recv_row + row) * p.ld_recv +
+                                                              td.c_col + cc * 32);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint4 w = __ldcs(src + q);
+              const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                float2 x = __bfloat1622float2(h[e]);
+                f[q * 8 + 2 * e] += x.x;
+                f[q * 8 + 2 * e + 1] += x.y;
+              }
+            }
+          }
+        }
+        uint4* o = reinterpret_cast<uint4*>(dst + cc * 32);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 w;
+          w.x = pack_bf16x2(f[q * 8 + 0], f[q * 8 + 1]);
+          w.y = pack_bf16x2(f[q * 8 + 2], f[q * 8 + 3]);
+          w.z = pack_bf16x2(f[q * 8 + 4], f[q * 8 + 5]);
+          w.w = pack_bf16x2(f[q * 8 + 6], f[q * 8 + 7]);
+          o[q] = w;
+        }
+      }
+    }
+    tc_fence_before();
+    mbar_arrive(&tempty[acc]);
+    if (td.mode == FICCO_EPI_STORE_SIGNAL) {
+      named_bar_sync(1, EPI_THREADS);  // every row of the tile is stored
+      if (threadIdx.x == 64) {
+        __threadfence_system();
+        red_release_add(p.counters + td.chunk, 1u);
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(NUM_THREADS, 1) tile_gemm_kernel(const __grid_constant__ TileParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = base;
+  uint8_t* sB = base + STAGES * A_STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&p.tmap_a);
+    tma_prefetch_desc(&p.tmap_b);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], EPI_THREADS);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) producer_loop(p, sA, sB, full, empty);
+  } else if (warp == 1) {
+    if (lane == 0) mma_loop(p, sA, sB, full, empty, tfull, tempty, tmem);
+  } else {
+    epilogue_loop(p, tfull, tempty, tmem);
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc(tmem, TMEM_COLS);
+}
+
+}  // namespace ficco

@@ -1,0 +1,233 @@
+"""Overlapped-op entry points (the north star's additions to the reference API).
+
+* ``all_gather_matmul(a_shard, weight)``        AG -> GEMM      (TP/SP up-projection, configs C1/C2/C3')
+* ``matmul_reduce_scatter(a, weight)``          GEMM -> RS      (TP/SP down-projection, config C3)
+* ``cp_kv_all_gather_qk(q, k_shard)``           CP KV-AG -> QK^T (config C4)
+
+Each builds the reference's ExecutionPlan for the equivalent scenario
+(``routing.build_plan``), picks the schedule with ``select_schedule`` when
+``kind`` is None, lowers it for this rank (``lowering``) and runs it through
+the C-ABI executor. Weights use the ``nn.Linear`` layout ``[N, K]`` (K
+contiguous), so C = A @ W^T.
+
+A ``FiccoGroup`` owns the communicator (symmetric workspaces, copy stream,
+epoch) and caches lowered plans per (op, shape, kind). Two flavours:
+
+* ``FiccoGroup.distributed(group)`` — one process per GPU (or several ranks
+  sharing a GPU), CUDA-IPC handles exchanged through ``torch.distributed``.
+* ``FiccoGroup.virtual_group(world, rank)`` — decomposition-only single-process
+  mode: this process plays ``rank`` of a ``world``-rank job whose peers'
+  shards are pre-loaded into local stand-in workspaces (``load_peer_shards``)
+  so the copy engines, flags and tile kernel do exactly one rank's work.
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+from .domain import Collective, GemmShape, Parallelism, Scenario
+from .lowering import F_RS, Lowered, lower_ag, lower_rs
+from .machines import b200_machine
+from .routing import PlanError, ScheduleKind, build_plan
+from .runtime import FICCO_WS_DATA_OFFSET, Communicator, Plan
+from .selector import select_schedule
+
+
+def _scenario(name: str, m: int, n: int, k: int, world: int, collective=Collective.ALL_GATHER) -> Scenario:
+    return Scenario(name=name, parallelism=Parallelism.SP_TP, model="ficco-op", gemm=GemmShape(m, n, k, 2),
+                    collective=collective, n_gpus=world)
+
+
+def choose_kind(scenario: Scenario, kind: ScheduleKind | str | None, machine=None, t_ref: float | None = None):
+    if kind is None:
+        spec = machine or b200_machine()
+        return select_schedule(scenario, spec.machine, spec.t_ref if t_ref is None else t_ref)
+    return ScheduleKind(kind) if isinstance(kind, str) else kind
+
+
+class FiccoGroup:
+    def __init__(self, world: int, rank: int, virtual: bool, pg=None):
+        self.world, self.rank, self.virtual, self.pg = world, rank, virtual, pg
+        self.comm: Communicator | None = None
+        self._plans: dict = {}
+        self._ws_bytes = 0
+
+    @classmethod
+    def virtual_group(cls, world: int, rank: int = 0) -> "FiccoGroup":
+        return cls(world, rank, True)
+
+    @classmethod
+    def distributed(cls, group=None) -> "FiccoGroup":
+        import torch.distributed as dist
+        return cls(dist.get_world_size(group), dist.get_rank(group), False, group)
+
+    # ---------------------------------------------------------------- workspace
+    def ensure_workspace(self, nbytes: int) -> None:
+        nbytes = max(nbytes, FICCO_WS_DATA_OFFSET)
+        if self.comm is not None and nbytes <= self._ws_bytes:
+            return
+        nbytes = 1 << max(20, math.ceil(math.log2(nbytes)))
+        if self.comm is not None:
+            torch.cuda.synchronize()
+            self._plans.clear()
+            self.comm.close()
+        if self.virtual:
+            self.comm = Communicator.virtual(self.world, self.rank, nbytes)
+            # peers never notify in virtual mode: pre-satisfy every receive flag
+            self.comm.set_flags(F_RS, 2048, 0x7FFFFFFF)
+            torch.cuda.synchronize()
+        else:
+            self.comm = Communicator.from_process_group(nbytes, self.pg)
+        self._ws_bytes = nbytes
+
+    def plan(self, key, make) -> tuple[Plan, Lowered]:
+        hit = self._plans.get(key)
+        if hit is None:
+            low = make()
+            self.ensure_workspace(low.ws_bytes)
+            hit = (Plan(self.comm, low.desc, low.ops, low.tiles), low)
+            self._plans[key] = hit
+        return hit
+
+    def ws_tensor(self, rank: int, offset: int, shape, dtype=torch.bfloat16) -> torch.Tensor:
+        """A torch view of (part of) a workspace (local, or a virtual peer's)."""
+        numel = math.prod(shape)
+        nbytes = numel * torch.tensor([], dtype=dtype).element_size()
+        if offset + nbytes > self._ws_bytes:
+            raise ValueError("view exceeds workspace")
+        ptr = self.comm.ws_ptrs[rank] + offset
+        return _wrap_device_ptr(ptr, shape, dtype)
+
+    def close(self) -> None:
+        self._plans.clear()
+        if self.comm is not None:
+            self.comm.close()
+            self.comm = None
+
+    # ---------------------------------------------------------------- virtual-mode data
+    def load_peer_shards(self, low: Lowered, shards: list[torch.Tensor]) -> None:
+        """Virtual mode: give every stand-in peer the shards it would hold (all slots, both parities).
+
+        Pull copies read chunk (p, c) from peer p's own slot (fine-grain kinds)
+        or a forwarded shard from the left neighbour's slot (ring), so each
+        peer workspace gets every shard at its gathered-row offset.
+        """
+        assert self.virtual
+        rows = shards[0].shape[0]
+        cols = shards[0].shape[1]
+        for peer in range(self.world):
+            if peer == self.rank:
+                continue
+            for p, sh in enumerate(shards):
+                for par in (0, 1):
+                    off = low.gather_off + par * low.gather_par + p * rows * cols * 2
+                    self.ws_tensor(peer, off, (rows, cols)).copy_(sh)
+
+    def load_peer_partials(self, low: Lowered, partials: list[torch.Tensor]) -> None:
+        """Virtual mode (RS): ``partials[j]`` = peer slot j's [R, N] contribution to this rank's shard."""
+        assert self.virtual
+        rows, cols = partials[0].shape
+        for j, part in enumerate(partials):
+            for par in (0, 1):
+                off = low.recv_off + par * low.recv_par + j * low.recv_slot
+                self.ws_tensor(self.rank, off, (rows, cols)).copy_(part)
+
+
+def _wrap_device_ptr(ptr: int, shape, dtype) -> torch.Tensor:
+    class _Holder:
+        pass
+
+    h = _Holder()
+    nbytes = math.prod(shape) * torch.tensor([], dtype=dtype).element_size()
+    h.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3,
+                                  "strides": None}
+    raw = torch.as_tensor(h, device=torch.device("cuda", torch.cuda.current_device()))
+    return raw.view(dtype).view(*shape)
+
+
+def _default_group(group, world):
+    if group is not None:
+        return group
+    raise ValueError("pass a FiccoGroup (FiccoGroup.distributed(pg) or FiccoGroup.virtual_group(world, rank))")
+
+
+def prepare_ag(grp: FiccoGroup, R: int, K: int, N: int, kind=None):
+    """Build (or fetch) the lowered AG->GEMM plan for this rank: (plan, lowered, kind)."""
+    M = R * grp.world
+    sc = _scenario("ag_gemm", M, N, K, grp.world)
+    kd = choose_kind(sc, kind)
+    plan, low = grp.plan(("ag", M, N, K, kd), lambda: lower_ag(build_plan(sc, kd), grp.rank, "A"))
+    return plan, low, kd
+
+
+def prepare_rs(grp: FiccoGroup, M: int, K: int, N: int, kind=None):
+    sc = _scenario("gemm_rs", M, N, K, grp.world)
+    kd = choose_kind(sc, kind)
+    if kd not in (ScheduleKind.UNIFORM_FUSED_1D, ScheduleKind.HETERO_FUSED_1D, ScheduleKind.HETERO_UNFUSED_1D):
+        kd = ScheduleKind.HETERO_FUSED_1D  # the 2D/serial choices have no RS adjoint on this executor
+    plan, low = grp.plan(("rs", M, N, K, kd), lambda: lower_rs(sc, kd, grp.rank))
+    return plan, low, kd
+
+
+def prepare_cp(grp: FiccoGroup, Tq: int, d: int, Tkv: int, kind=None, scale: float | None = None):
+    sc = _scenario("cp_qk", Tkv, Tq, d, grp.world)
+    kd = choose_kind(sc, kind)
+    if kd is ScheduleKind.UNIFORM_FUSED_2D:
+        kd = ScheduleKind.UNIFORM_FUSED_1D  # K=d is a single k-segment; the 2D split does not apply
+    alpha = (1.0 / math.sqrt(d)) if scale is None else scale
+    plan, low = grp.plan(("cp", Tkv, Tq, d, kd, alpha),
+                         lambda: lower_ag(build_plan(sc, kd), grp.rank, "B", alpha=alpha, other_rows=Tq))
+    return plan, low, kd
+
+
+def all_gather_matmul(a_shard: torch.Tensor, weight: torch.Tensor, kind=None, group: FiccoGroup | None = None,
+                      out: torch.Tensor | None = None, stream=None, return_gathered: bool = False):
+    """C = all_gather(A_shard) @ W^T with FiCCO overlap. A_shard [R, K], W [N, K] -> C [G*R, N].
+
+    ``return_gathered`` also returns the gathered A (a view into the group's
+    double-buffered workspace, valid until the call after next).
+    """
+    grp = _default_group(group, None)
+    R, K = a_shard.shape
+    N = weight.shape[0]
+    M = R * grp.world
+    plan, low, _ = prepare_ag(grp, R, K, N, kind)
+    if out is None:
+        out = torch.empty(M, N, dtype=torch.bfloat16, device=a_shard.device)
+    plan.run(a_shard, weight, out, stream)
+    if return_gathered:
+        par = grp.comm.epoch() & 1
+        gathered = grp.ws_tensor(grp.rank, low.gather_off + par * low.gather_par, (M, K))
+        return out, gathered
+    return out
+
+
+def matmul_reduce_scatter(a: torch.Tensor, weight: torch.Tensor, kind=None, group: FiccoGroup | None = None,
+                          out: torch.Tensor | None = None, stream=None):
+    """C_shard = reduce_scatter_rows(A @ W^T). A [M, Kg], W [N, Kg] -> [M/G, N] (this rank's rows)."""
+    grp = _default_group(group, None)
+    M, K = a.shape
+    N = weight.shape[0]
+    plan, _, _ = prepare_rs(grp, M, K, N, kind)
+    if out is None:
+        out = torch.empty(M // grp.world, N, dtype=torch.bfloat16, device=a.device)
+    plan.run(a, weight, out, stream)
+    return out
+
+
+def cp_kv_all_gather_qk(q: torch.Tensor, k_shard: torch.Tensor, kind=None, scale: float | None = None,
+                        group: FiccoGroup | None = None, out: torch.Tensor | None = None, stream=None):
+    """S = scale * Q @ all_gather(K_shard)^T. Q [Tq, d], K_shard [Tkv/G, d] -> S [Tq, Tkv] (bf16).
+
+    Scenario view: M = Tkv (gathered kv tokens), N = Tq, K = d.
+    """
+    grp = _default_group(group, None)
+    Tq, d = q.shape
+    Tkv = k_shard.shape[0] * grp.world
+    plan, _, _ = prepare_cp(grp, Tq, d, Tkv, kind, scale)
+    if out is None:
+        out = torch.empty(Tq, Tkv, dtype=torch.bfloat16, device=q.device)
+    plan.run(q, k_shard, out, stream)
+    return out

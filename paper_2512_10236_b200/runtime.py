@@ -1,0 +1,286 @@
+"""ctypes binding of the C-ABI executor (include/ficco.h -> libficco_b200.so).
+
+PyTorch is plumbing here: it owns caller buffers and streams, and
+``torch.distributed`` exchanges CUDA-IPC handles of the symmetric workspaces.
+Every compute call goes through the C library; there is no fallback — if the
+library cannot be loaded or the device is not sm_100, calls raise.
+
+Error mapping: FICCO_EINVAL -> ValueError, FICCO_ECUDA ->
+RuntimeError, FICCO_ETIMEOUT -> DeadlockError (the reference's
+engine.DeadlockError, engine.py:35), FICCO_ENODEV -> RuntimeError.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import pathlib
+import threading
+
+from .simulator import DeadlockError
+
+LIB_PATH = pathlib.Path(__file__).resolve().parent / "libficco_b200.so"
+
+FICCO_WS_FLAG_WORDS = 16384
+FICCO_WS_DATA_OFFSET = FICCO_WS_FLAG_WORDS * 4
+FICCO_FLAG_ABORT = FICCO_WS_FLAG_WORDS - 1
+FICCO_FLAG_COUNTERS = 12288
+
+OP_COPY, OP_SIGNAL, OP_NOTIFY, OP_WAIT, OP_WAIT_COUNTER = 0, 1, 2, 3, 4
+BUF_NONE, BUF_A, BUF_B, BUF_C, BUF_WS = 0, 1, 2, 3, 4
+EPI_STORE, EPI_STORE_SIGNAL, EPI_REDUCE = 0, 1, 2
+TILE_M, TILE_N, TILE_K = 128, 256, 64
+MAX_RECV = 15
+
+EXPORTED = (
+    "ficco_abi_version", "ficco_last_error", "ficco_device_info", "ficco_ws_alloc", "ficco_ws_free",
+    "ficco_ipc_handle_size", "ficco_ipc_get_handle", "ficco_ipc_open", "ficco_ipc_close",
+    "ficco_comm_create", "ficco_comm_destroy", "ficco_comm_epoch", "ficco_comm_check", "ficco_comm_set_flags",
+    "ficco_plan_create", "ficco_plan_destroy", "ficco_plan_run", "ficco_plan_run_parts",
+    "ficco_gemm_bf16", "ficco_copy_batch",
+)
+
+
+class CopyOp(C.Structure):
+    _fields_ = [("op", C.c_int32), ("peer", C.c_int32), ("flag", C.c_int32), ("src_buf", C.c_int32),
+                ("dst_buf", C.c_int32), ("dst_peer", C.c_int32), ("src_off", C.c_int64), ("dst_off", C.c_int64),
+                ("src_par", C.c_int64), ("dst_par", C.c_int64), ("width", C.c_int64), ("height", C.c_int64),
+                ("src_pitch", C.c_int64), ("dst_pitch", C.c_int64), ("value", C.c_uint32),
+                ("reserved", C.c_uint32)]
+
+
+class Tile(C.Structure):
+    _fields_ = [("a_row", C.c_int32), ("b_row", C.c_int32), ("c_row", C.c_int32), ("c_col", C.c_int32),
+                ("rows", C.c_int16), ("cols", C.c_int16), ("flag", C.c_int16), ("kseg", C.c_int16),
+                ("mode", C.c_int16), ("chunk", C.c_int16), ("recv_row", C.c_int32)]
+
+
+class Operand(C.Structure):
+    _fields_ = [("buf", C.c_int32), ("pad", C.c_int32), ("off", C.c_int64), ("par", C.c_int64),
+                ("rows", C.c_int64), ("ld", C.c_int64)]
+
+
+class PlanDesc(C.Structure):
+    _fields_ = [("n_ops", C.c_int32), ("n_tiles", C.c_int32), ("ops", C.POINTER(CopyOp)),
+                ("tiles", C.POINTER(Tile)), ("a", Operand), ("b", Operand), ("c", Operand), ("part", Operand),
+                ("recv", Operand), ("recv_slot", C.c_int64), ("k", C.c_int64), ("n_recv", C.c_int32),
+                ("rs_flag0", C.c_int32), ("n_counters", C.c_int32), ("grid", C.c_int32), ("alpha", C.c_float),
+                ("reserved", C.c_int32)]
+
+
+assert C.sizeof(CopyOp) == 96 and C.sizeof(Tile) == 32 and C.sizeof(Operand) == 40
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load_library(path: os.PathLike | str | None = None) -> C.CDLL:
+    """Load (once) and type the C-ABI. Raises if the shared object is missing."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        p = pathlib.Path(path) if path else LIB_PATH
+        if not p.exists():
+            raise RuntimeError(f"{p} not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+        lib = C.CDLL(str(p))
+        vp, i32, i64, sz = C.c_void_p, C.c_int, C.c_int64, C.c_size_t
+        sig = {
+            "ficco_abi_version": ([], i32),
+            "ficco_last_error": ([], C.c_char_p),
+            "ficco_device_info": ([i32, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)], i32),
+            "ficco_ws_alloc": ([sz, C.POINTER(vp)], i32),
+            "ficco_ws_free": ([vp], i32),
+            "ficco_ipc_handle_size": ([], i32),
+            "ficco_ipc_get_handle": ([vp, vp], i32),
+            "ficco_ipc_open": ([vp, C.POINTER(vp)], i32),
+            "ficco_ipc_close": ([vp], i32),
+            "ficco_comm_create": ([i32, i32, C.POINTER(vp), sz, i32, C.POINTER(vp)], i32),
+            "ficco_comm_destroy": ([vp], i32),
+            "ficco_comm_epoch": ([vp, C.POINTER(C.c_uint32)], i32),
+            "ficco_comm_check": ([vp, vp], i32),
+            "ficco_comm_set_flags": ([vp, i32, i32, C.c_uint32, vp], i32),
+            "ficco_plan_create": ([vp, C.POINTER(PlanDesc), C.POINTER(vp)], i32),
+            "ficco_plan_destroy": ([vp], i32),
+            "ficco_plan_run": ([vp, vp, vp, vp, vp], i32),
+            "ficco_plan_run_parts": ([vp, vp, vp, vp, vp, i32, i32], i32),
+            "ficco_gemm_bf16": ([vp, vp, vp, i64, i64, i64, C.c_float, i32, vp], i32),
+            "ficco_copy_batch": ([C.POINTER(vp), C.POINTER(vp), C.POINTER(sz), sz, vp], i32),
+        }
+        for name, (args, res) in sig.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = res
+        if lib.ficco_abi_version() != 1:
+            raise RuntimeError("libficco_b200 ABI mismatch")
+        _lib = lib
+        return lib
+
+
+def check(rc: int) -> None:
+    if rc == 0:
+        return
+    msg = (load_library().ficco_last_error() or b"").decode()
+    if rc == -1:
+        raise ValueError(msg)
+    if rc == -3:
+        raise DeadlockError(msg)
+    raise RuntimeError(f"libficco_b200 error {rc}: {msg}")
+
+
+def _stream_ptr(stream) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+class Workspace:
+    """A symmetric workspace buffer (flags + data) allocated by the library."""
+
+    def __init__(self, nbytes: int):
+        lib = load_library()
+        ptr = C.c_void_p()
+        check(lib.ficco_ws_alloc(nbytes, C.byref(ptr)))
+        self.ptr = ptr.value
+        self.nbytes = nbytes
+
+    def ipc_handle(self) -> bytes:
+        lib = load_library()
+        buf = C.create_string_buffer(lib.ficco_ipc_handle_size())
+        check(lib.ficco_ipc_get_handle(C.c_void_p(self.ptr), buf))
+        return buf.raw
+
+    def free(self) -> None:
+        if self.ptr:
+            check(load_library().ficco_ws_free(C.c_void_p(self.ptr)))
+            self.ptr = None
+
+
+def ipc_open(handle: bytes) -> int:
+    out = C.c_void_p()
+    check(load_library().ficco_ipc_open(C.create_string_buffer(handle, len(handle)), C.byref(out)))
+    return out.value
+
+
+def ipc_close(ptr: int) -> None:
+    check(load_library().ficco_ipc_close(C.c_void_p(ptr)))
+
+
+class Communicator:
+    """One rank's view of G symmetric workspaces (+ its copy stream and epoch).
+
+    ``Communicator.virtual(G, rank, nbytes)`` builds the single-process
+    decomposition-only mode: the G-1 peers' workspaces are
+    local allocations and cross-rank waits/notifies are satisfied locally.
+    ``Communicator.from_process_group(nbytes, group)`` exchanges CUDA-IPC
+    handles through ``torch.distributed`` (works for ranks on different GPUs
+    of one node, and for several ranks sharing one GPU).
+    """
+
+    def __init__(self, rank: int, world: int, ws_ptrs: list[int], nbytes: int, virtual: bool,
+                 owned: list[Workspace], opened: list[int]):
+        lib = load_library()
+        arr = (C.c_void_p * world)(*ws_ptrs)
+        h = C.c_void_p()
+        check(lib.ficco_comm_create(rank, world, arr, nbytes, int(virtual), C.byref(h)))
+        self.handle = h.value
+        self.rank, self.world, self.nbytes, self.virtual = rank, world, nbytes, virtual
+        self.ws_ptrs = list(ws_ptrs)
+        self._owned, self._opened = owned, opened
+
+    @classmethod
+    def virtual(cls, world: int, rank: int, nbytes: int) -> "Communicator":
+        owned = [Workspace(nbytes) for _ in range(world)]
+        return cls(rank, world, [w.ptr for w in owned], nbytes, True, owned, [])
+
+    @classmethod
+    def from_process_group(cls, nbytes: int, group=None) -> "Communicator":
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        mine = Workspace(nbytes)
+        handles: list = [None] * world
+        dist.all_gather_object(handles, mine.ipc_handle(), group=group)
+        ptrs, opened = [], []
+        for r, h in enumerate(handles):
+            if r == rank:
+                ptrs.append(mine.ptr)
+            else:
+                p = ipc_open(h)
+                ptrs.append(p)
+                opened.append(p)
+        dist.barrier(group=group)
+        return cls(rank, world, ptrs, nbytes, False, [mine], opened)
+
+    @property
+    def local_ws(self) -> int:
+        return self.ws_ptrs[self.rank]
+
+    def epoch(self) -> int:
+        e = C.c_uint32()
+        check(load_library().ficco_comm_epoch(C.c_void_p(self.handle), C.byref(e)))
+        return e.value
+
+    def check(self, stream=None) -> None:
+        """Synchronise and raise DeadlockError if a kernel timed out on a flag."""
+        check(load_library().ficco_comm_check(C.c_void_p(self.handle), C.c_void_p(_stream_ptr(stream))))
+
+    def set_flags(self, first: int, count: int, value: int, stream=None) -> None:
+        check(load_library().ficco_comm_set_flags(C.c_void_p(self.handle), first, count, value,
+                                                  C.c_void_p(_stream_ptr(stream))))
+
+    def close(self) -> None:
+        if self.handle:
+            load_library().ficco_comm_destroy(C.c_void_p(self.handle))
+            self.handle = None
+            for p in self._opened:
+                ipc_close(p)
+            for w in self._owned:
+                w.free()
+            self._owned, self._opened = [], []
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Plan:
+    """A lowered per-rank program bound to a communicator (ficco_plan_t)."""
+
+    def __init__(self, comm: Communicator, desc: PlanDesc, ops: list[CopyOp], tiles: list[Tile]):
+        lib = load_library()
+        self._ops = (CopyOp * max(1, len(ops)))(*ops)
+        self._tiles = (Tile * max(1, len(tiles)))(*tiles)
+        desc.n_ops, desc.n_tiles = len(ops), len(tiles)
+        desc.ops = C.cast(self._ops, C.POINTER(CopyOp))
+        desc.tiles = C.cast(self._tiles, C.POINTER(Tile))
+        h = C.c_void_p()
+        check(lib.ficco_plan_create(C.c_void_p(comm.handle), C.byref(desc), C.byref(h)))
+        self.handle, self.comm, self.desc = h.value, comm, desc
+        self.n_ops, self.n_tiles = len(ops), len(tiles)
+
+    def run(self, a, b, c, stream=None, copies: bool = True, tiles: bool = True) -> None:
+        ptr = lambda t: C.c_void_p(0 if t is None else t.data_ptr())  # noqa: E731
+        check(load_library().ficco_plan_run_parts(C.c_void_p(self.handle), ptr(a), ptr(b), ptr(c),
+                                                  C.c_void_p(_stream_ptr(stream)), int(copies), int(tiles)))
+
+    def close(self) -> None:
+        if self.handle:
+            load_library().ficco_plan_destroy(C.c_void_p(self.handle))
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def gemm_bf16(a, b, out, alpha: float = 1.0, grid: int = 0, stream=None) -> None:
+    """out[M,N] = alpha * a[M,K] @ b[N,K]^T with the tcgen05 tile kernel (no flags)."""
+    m, k = a.shape
+    n = b.shape[0]
+    check(load_library().ficco_gemm_bf16(C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()),
+                                         C.c_void_p(out.data_ptr()), m, n, k, alpha, grid,
+                                         C.c_void_p(_stream_ptr(stream))))

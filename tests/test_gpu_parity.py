@@ -1,0 +1,139 @@
+"""GPU parity: the CUDA path (C-ABI -> copy engines + tcgen05 tile kernel) vs the CPU oracle.
+
+Bars: gathered buffers bit-exact; GEMM outputs (bf16 in, fp32
+accumulate, bf16 out) within rtol=1.6e-2 / atol=1e-2 of the oracle's fp32
+result (atol x sqrt(G) for RS).
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import ficco_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+RTOL, ATOL = 1.6e-2, 1e-2
+
+
+def _t(x: np.ndarray) -> torch.Tensor:
+    return torch.from_numpy(x).to(torch.bfloat16).cuda()
+
+
+def _np(t: torch.Tensor) -> np.ndarray:
+    return t.float().cpu().numpy()
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2512_10236_b200 import runtime
+    runtime.load_library()
+    return runtime
+
+
+@pytest.mark.parametrize("m,n,k", [(128, 256, 64), (256, 512, 1024), (384, 544, 520), (1000, 96, 200),
+                                   (2048, 3584, 4096)])
+def test_tile_gemm_matches_fp32(lib, m, n, k):
+    a = orc.seeded_inputs(0, 0, (m, k))
+    w = orc.seeded_inputs(0, 1, (n, k), "normal")
+    out = torch.empty(m, n, dtype=torch.bfloat16, device="cuda")
+    lib.gemm_bf16(_t(a), _t(w), out)
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(_np(out), a @ w.T, rtol=RTOL, atol=ATOL)
+
+
+def test_tile_gemm_alpha_and_grid(lib):
+    a = orc.seeded_inputs(3, 0, (512, 256))
+    w = orc.seeded_inputs(3, 1, (768, 256), "normal")
+    out = torch.empty(512, 768, dtype=torch.bfloat16, device="cuda")
+    lib.gemm_bf16(_t(a), _t(w), out, alpha=0.125, grid=7)
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(_np(out), 0.125 * (a @ w.T), rtol=RTOL, atol=ATOL)
+
+
+AG_KINDS = ["serial", "shard_overlap_p2p", "uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d",
+            "uniform_fused_2d"]
+
+
+@pytest.mark.parametrize("kind", AG_KINDS)
+@pytest.mark.parametrize("G,rank,R,K,N", [(4, 0, 512, 1024, 768), (4, 3, 512, 1024, 768), (2, 1, 256, 512, 256),
+                                          (8, 5, 128, 512, 512)])
+def test_ag_virtual_matches_oracle(lib, kind, G, rank, R, K, N):
+    from paper_2512_10236_b200 import ops
+    shards = [orc.seeded_inputs(0, p, (R, K)) for p in range(G)]
+    w = orc.seeded_inputs(0, 99, (N, K), "normal")
+    gathered_ref, outs = orc.execute_ag(kind, shards, w)
+    grp = ops.FiccoGroup.virtual_group(G, rank)
+    try:
+        _, low, _ = ops.prepare_ag(grp, R, K, N, kind)
+        grp.load_peer_shards(low, [_t(s) for s in shards])
+        a, wt = _t(shards[rank]), _t(w)
+        for it in range(3):  # both workspace parities
+            out, gathered = ops.all_gather_matmul(a, wt, kind=kind, group=grp, return_gathered=True)
+            grp.comm.check()
+            assert np.array_equal(_np(gathered), gathered_ref[rank]), (kind, it)
+            np.testing.assert_allclose(_np(out), outs[rank], rtol=RTOL, atol=ATOL)
+    finally:
+        grp.close()
+
+
+@pytest.mark.parametrize("kind", ["uniform_fused_1d", "hetero_fused_1d"])
+def test_ag_ragged_chunks(lib, kind):
+    """Chunks of 96 rows (tiles straddle nothing, partial 128-row boxes), N tail of 32, K tail of 8."""
+    from paper_2512_10236_b200 import ops
+    G, R, K, N = 4, 384, 520, 544
+    shards = [orc.seeded_inputs(5, p, (R, K)) for p in range(G)]
+    w = orc.seeded_inputs(5, 99, (N, K), "normal")
+    gathered_ref, outs = orc.execute_ag(kind, shards, w)
+    grp = ops.FiccoGroup.virtual_group(G, 1)
+    try:
+        _, low, _ = ops.prepare_ag(grp, R, K, N, kind)
+        grp.load_peer_shards(low, [_t(s) for s in shards])
+        out, gathered = ops.all_gather_matmul(_t(shards[1]), _t(w), kind=kind, group=grp, return_gathered=True)
+        grp.comm.check()
+        assert np.array_equal(_np(gathered), gathered_ref[1])
+        np.testing.assert_allclose(_np(out), outs[1], rtol=RTOL, atol=ATOL)
+    finally:
+        grp.close()
+
+
+@pytest.mark.parametrize("kind", ["uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d"])
+@pytest.mark.parametrize("G,rank", [(2, 0), (4, 2), (8, 7)])
+def test_rs_virtual_matches_oracle(lib, kind, G, rank):
+    from paper_2512_10236_b200 import ops
+    M, Kg, N = 128 * G * G, 256, 512
+    a = [orc.seeded_inputs(7, p, (M, Kg)) for p in range(G)]
+    w = [orc.seeded_inputs(7, 100 + p, (N, Kg), "normal") for p in range(G)]
+    want = orc.execute_rs(a, w)[rank]
+    R = M // G
+    peers = [orc.bf16_round(a[p] @ w[p].T)[rank * R:(rank + 1) * R] for p in range(G) if p != rank]
+    grp = ops.FiccoGroup.virtual_group(G, rank)
+    try:
+        _, low, _ = ops.prepare_rs(grp, M, Kg, N, kind)
+        grp.load_peer_partials(low, [_t(x) for x in peers])
+        for _ in range(2):
+            out = ops.matmul_reduce_scatter(_t(a[rank]), _t(w[rank]), kind=kind, group=grp)
+            grp.comm.check()
+            np.testing.assert_allclose(_np(out), want, rtol=RTOL, atol=ATOL * math.sqrt(G))
+    finally:
+        grp.close()
+
+
+@pytest.mark.parametrize("kind", ["uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d", "serial"])
+def test_cp_qk_virtual_matches_oracle(lib, kind):
+    from paper_2512_10236_b200 import ops
+    G, rank, d, Tq, Tkv = 4, 1, 128, 384, 4096
+    q = orc.seeded_inputs(9, 50, (Tq, d), "normal")
+    ks = [orc.seeded_inputs(9, p, (Tkv // G, d), "normal") for p in range(G)]
+    want, _ = orc.execute_cp_qk(q, ks, 1.0 / math.sqrt(d))
+    grp = ops.FiccoGroup.virtual_group(G, rank)
+    try:
+        _, low, _ = ops.prepare_cp(grp, Tq, d, Tkv, kind)
+        grp.load_peer_shards(low, [_t(x) for x in ks])
+        for _ in range(2):
+            out = ops.cp_kv_all_gather_qk(_t(q), _t(ks[rank]), kind=kind, group=grp)
+            grp.comm.check()
+            np.testing.assert_allclose(_np(out), want, rtol=RTOL, atol=ATOL)
+    finally:
+        grp.close()

@@ -1,0 +1,82 @@
+"""Pin the CPU oracle (oracle/ficco_oracle.py) to the reference's own outputs.
+
+The oracle's routing restatement must reproduce, for every kind and every
+golden scenario, the exact TransferSpec sequence and GemmSpec fragments the
+reference planner emitted (tests/golden/plans_small.json); its selector must
+reproduce every golden select_schedule case. Numerics (unpinned by the
+reference) are checked for internal consistency: every schedule yields the
+same gathered buffer (bit-exact) and the same product as one full matmul.
+"""
+import numpy as np
+import pytest
+
+from oracle import ficco_oracle as orc
+
+from _golden import load
+
+SMALL = load("plans_small.json")
+
+
+@pytest.mark.parametrize("name", sorted(SMALL))
+def test_oracle_routing_matches_reference(name):
+    m, n, k, elt, g = SMALL[name]["scenario"]
+    for kind in orc.KINDS:
+        want = SMALL[name]["plans"][kind]
+        if "error" in want:
+            with pytest.raises(ValueError):
+                orc.transfers(kind, m, k, g, elt)
+            continue
+        # task record: [id, gpu, deps, "T", src, dst, bytes, fine, round]
+        ref_x = [(t[5], t[4], t[6], bool(t[7]), t[8]) for t in want["tasks"] if t[3] == "T"]
+        assert orc.transfers(kind, m, k, g, elt) == ref_x, (name, kind)
+        for gpu in range(g):
+            # [id, gpu, deps, "M", m, n, k, elt, additive, dil, rows, col_block]
+            ref_m = [(tuple(tuple(f) for f in t[10]), None if t[11] is None else tuple(t[11]))
+                     for t in want["tasks"] if t[3] == "M" and t[1] == gpu]
+            assert orc.gemm_fragments(kind, m, k, g, gpu) == ref_m, (name, kind, gpu)
+
+
+def test_oracle_selector_matches_reference():
+    peak = {"mesh": 1.3e15, "example": 1e15, "b200": 1.6081e15}
+    for m, n, k, elt, g, mname, t_ref, want in load("selector.json")["cases"]:
+        assert orc.select_schedule(m, n, k, peak[mname], t_ref) == want
+
+
+def test_bf16_round_known_answers():
+    x = np.array([1.0, 1.00390625, 1.005859375, -2.5, 3.140625, 1e-40, np.inf], dtype=np.float32)
+    y = orc.bf16_round(x)
+    # 1+2^-8 is a tie between 1 and 1+2^-7 -> even (1.0); 1.005859375 rounds up
+    assert y[0] == 1.0 and y[1] == 1.0 and y[2] == np.float32(1.0078125)
+    assert y[3] == -2.5 and y[4] == np.float32(3.140625) and y[6] == np.inf
+    import torch
+    r = np.random.default_rng(0).standard_normal(4096).astype(np.float32)
+    ref = torch.from_numpy(r).to(torch.bfloat16).float().numpy()
+    assert np.array_equal(orc.bf16_round(r), ref)
+
+
+@pytest.mark.parametrize("g", [2, 4])
+def test_oracle_schedules_agree(g):
+    R, K, N = 32, 64, 48
+    shards = [orc.seeded_inputs(0, p, (R, K)) for p in range(g)]
+    w = orc.seeded_inputs(0, 99, (N, K), "normal")
+    full = np.concatenate(shards)
+    want = full @ w.T
+    for kind in ("serial", "shard_overlap_p2p") + orc.FINE:
+        gathered, outs = orc.execute_ag(kind, shards, w)
+        for gpu in range(g):
+            assert np.array_equal(gathered[gpu], full), (kind, gpu)
+            np.testing.assert_allclose(outs[gpu], want, rtol=1e-5, atol=1e-5)
+
+
+def test_oracle_rs_and_cp():
+    g, M, Kg, N = 4, 64, 32, 40
+    a = [orc.seeded_inputs(1, p, (M, Kg)) for p in range(g)]
+    w = [orc.seeded_inputs(1, 100 + p, (N, Kg), "normal") for p in range(g)]
+    outs = orc.execute_rs(a, w)
+    full = sum(x @ y.T for x, y in zip(a, w))
+    for q in range(g):
+        np.testing.assert_allclose(outs[q], full[q * 16:(q + 1) * 16], rtol=2e-2, atol=2e-2)
+    qm = orc.seeded_inputs(2, 0, (16, 32), "normal")
+    ks = [orc.seeded_inputs(2, 1 + p, (8, 32), "normal") for p in range(g)]
+    s, kall = orc.execute_cp_qk(qm, ks, 0.5)
+    np.testing.assert_allclose(s, 0.5 * qm @ kall.T, rtol=1e-6)
