@@ -110,25 +110,29 @@ class ClockSampler:
 
 
 def time_steps(fn, steps: int, warmup: int, flush, stream, barrier=None) -> list[float]:
-    """Per-step device times (ms) with CUDA events on `stream`, L2 flushed between steps."""
+    """Per-step device times (ms): CUDA events on `stream` around each step, L2 flushed
+    (256 MiB write) between steps outside the events. Everything is enqueued
+    asynchronously (the host runs ahead, so launch latency hides behind the
+    flush as it would in a pipelined job); the K timed steps are bracketed by a
+    barrier + synchronize on both sides."""
     import torch
     for _ in range(warmup):
+        flush()
         fn()
     torch.cuda.synchronize()
-    times = []
-    for _ in range(steps):
+    if barrier:
+        barrier()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for a, b in evs:
         flush()
-        if barrier:
-            barrier()
-        torch.cuda.synchronize()
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
         fn()
         b.record(stream)
-        b.synchronize()
-        times.append(a.elapsed_time(b))
-    return times
+    torch.cuda.synchronize()
+    if barrier:
+        barrier()
+    return [a.elapsed_time(b) for a, b in evs]
 
 
 def our_arm(args) -> None:

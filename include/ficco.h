@@ -49,18 +49,38 @@ extern "C" {
 #define FICCO_ETIMEOUT (-3) /* a readiness flag never arrived (DeadlockError) */
 #define FICCO_ENODEV (-4)   /* no sm_100 device */
 
-/* symmetric workspace layout: flag words first, data after FICCO_WS_DATA_OFFSET */
+/* Symmetric workspace layout: flag words first, data after FICCO_WS_DATA_OFFSET.
+ * Flags are one-shot 0/1 words (constant values, so a lowered plan can be
+ * replayed as a CUDA graph). Run r uses flag block (r & 1) — FICCO_FLAG_BLOCK
+ * words each. Inside a block, words [0, FICCO_FLAG_RUN_LOCAL) are cross-rank
+ * flags written by peers and reset by their consumer (FICCO_OP_WAIT); words
+ * [FICCO_FLAG_RUN_LOCAL, FICCO_FLAG_BLOCK) are reset to 0 at the start of the
+ * run that uses the block. */
 #define FICCO_WS_FLAG_WORDS 16384
 #define FICCO_WS_DATA_OFFSET (FICCO_WS_FLAG_WORDS * 4)
+#define FICCO_FLAG_BLOCK 4096
+#define FICCO_FLAG_RUN_LOCAL 256
+#define FICCO_FLAG_COUNTERS 2048                   /* block-relative: per-unit tile counters (run-local) */
+#define FICCO_FLAG_CONST_ONE 16320                 /* constant 0x01010101: source of flag-setting copies */
+#define FICCO_FLAG_CONST_ZERO 16322                /* constant 8 zero bytes: source of flag resets */
 #define FICCO_FLAG_ABORT (FICCO_WS_FLAG_WORDS - 1) /* kernel-side timeout indicator */
-#define FICCO_FLAG_COUNTERS 12288                  /* per-chunk tile counters (reset per run) */
+#define FICCO_MAX_STREAMS 16                       /* copy streams (parallel copy-engine chains) */
 
 /* copy-program opcodes (executed in order on the copy stream) */
-#define FICCO_OP_COPY 0        /* copy width x height bytes src(peer buf) -> dst(local buf) */
-#define FICCO_OP_SIGNAL 1      /* local flag[flag] = epoch (after everything before it) */
-#define FICCO_OP_NOTIFY 2      /* flag[flag] of rank `peer` = epoch (remote write over NVLink) */
-#define FICCO_OP_WAIT 3        /* copy stream waits until local flag[flag] >= epoch - value */
-#define FICCO_OP_WAIT_COUNTER 4 /* copy stream waits until local counter[flag] >= value */
+/* copy-program opcodes; ops with the same `stream` run in order on that copy
+ * stream (one copy-engine chain); different streams run concurrently. Flags
+ * are set by tiny copy-engine copies of a constant word (not by stream
+ * write-value memops, which serialise across chains), so a flag lands right
+ * behind the data it covers on the same engine. */
+#define FICCO_OP_COPY 0         /* copy width x height bytes src -> dst (copy engine) */
+#define FICCO_OP_SIGNAL 1       /* local flag[flag] := 1 (after everything before it on the stream) */
+#define FICCO_OP_NOTIFY 2       /* flag[flag] of rank `peer` := 1 (remote write over NVLink) */
+#define FICCO_OP_WAIT 3         /* wait until local flag[flag] != 0, then reset it (cross-rank flags) */
+#define FICCO_OP_WAIT_COUNTER 4 /* wait until local counter[flag] >= value */
+#define FICCO_OP_BARRIER 5      /* set byte `rank` of every rank's 8-byte barrier words at flag, wait for all, reset */
+#define FICCO_OP_RECORD 6       /* record event slot `value` on the stream */
+#define FICCO_OP_STREAM_WAIT 7  /* the stream waits for event slot `value` */
+#define FICCO_MAX_EVENTS 64
 
 /* buffer ids */
 #define FICCO_BUF_NONE 0
@@ -85,32 +105,35 @@ typedef struct {
   int32_t dst_buf;  /* FICCO_BUF_* (WS means the local workspace, or `dst_peer`'s when push) */
   int32_t dst_peer; /* -1: local; else rank whose workspace receives the bytes (push) */
   int64_t src_off, dst_off;     /* bytes from buffer base */
-  int64_t src_par, dst_par;     /* added once per odd epoch (double-buffered workspaces) */
+  int64_t src_par, dst_par;     /* added once per odd run (double-buffered workspaces) */
   int64_t width, height;        /* bytes per row, rows (height 1 = 1D copy) */
   int64_t src_pitch, dst_pitch; /* bytes between rows (2D) */
-  uint32_t value;               /* WAIT_COUNTER threshold */
-  uint32_t reserved;
+  uint32_t value;               /* WAIT_COUNTER threshold / event slot */
+  int32_t stream;               /* copy stream index in [0, FICCO_MAX_STREAMS) */
 } ficco_copy_op;
 
 typedef struct {
-  int32_t a_row;  /* row coordinate of the 128-row A box (TMA) */
-  int32_t b_row;  /* row coordinate of the 256-row B box (TMA) */
-  int32_t c_row;  /* first output row */
-  int32_t c_col;  /* first output column */
-  int16_t rows;   /* valid output rows (<= 128) */
-  int16_t cols;   /* valid output columns (<= 256, multiple of 32) */
-  int16_t flag;   /* first readiness flag gating the A/B loads (-1: none) */
-  int16_t kseg;   /* k-blocks (64 elements) per flag segment (0: one flag for the tile) */
-  int16_t mode;   /* FICCO_EPI_* */
-  int16_t chunk;  /* counter index (STORE_SIGNAL) or rs-flag group (REDUCE) */
+  int32_t a_row;    /* row coordinate of the 128-row A box (TMA) */
+  int32_t b_row;    /* row coordinate of the tile_n-row B box (TMA) */
+  int32_t c_row;    /* first output row */
+  int32_t c_col;    /* first output column */
   int32_t recv_row; /* REDUCE: row offset into every receive slot */
+  int16_t rows;     /* valid output rows (<= 128) */
+  int16_t cols;     /* valid output columns (<= tile_n, multiple of 32) */
+  int16_t flag;     /* first readiness flag gating the A/B loads (-1: none) */
+  int16_t nflag;    /* consecutive flags [flag, flag+nflag) that must all be set (>= 1) */
+  int16_t kseg;     /* k-blocks (64 elements) per segment; segment s waits flag + s*kstride (0: off) */
+  int16_t kstride;  /* flag stride between k segments */
+  int16_t mode;     /* FICCO_EPI_* */
+  int16_t chunk;    /* counter index (STORE_SIGNAL) or rs-flag group (REDUCE) */
+  int32_t reserved;
 } ficco_tile;
 
 typedef struct {
   int32_t buf;      /* FICCO_BUF_* (WS = local workspace) */
   int32_t pad;
   int64_t off;      /* bytes */
-  int64_t par;      /* extra bytes on odd epochs */
+  int64_t par;      /* extra bytes on odd runs */
   int64_t rows;     /* rows of the row-major bf16 matrix */
   int64_t ld;       /* elements between rows */
 } ficco_operand;
@@ -121,18 +144,18 @@ typedef struct {
   const ficco_copy_op* ops;
   const ficco_tile* tiles;
   ficco_operand a;    /* M x K, K contiguous (TMA box 128 x 64) */
-  ficco_operand b;    /* N x K, K contiguous (TMA box 256 x 64) */
+  ficco_operand b;    /* N x K, K contiguous (TMA box tile_n x 64) */
   ficco_operand c;    /* output, bf16 */
   ficco_operand part; /* STORE_SIGNAL destination (RS partials) */
-  ficco_operand recv; /* REDUCE sources: slot j at off + j*recv_slot (+par on odd epochs) */
+  ficco_operand recv; /* REDUCE sources: slot j at off + j*recv_slot (+par on odd runs) */
   int64_t recv_slot;  /* bytes between receive slots */
   int64_t k;          /* reduction length in elements (multiple of 8) */
   int32_t n_recv;     /* receive slots summed by REDUCE tiles */
-  int32_t rs_flag0;   /* first rs flag word; REDUCE waits flag[rs_flag0 + chunk*n_recv + j] */
+  int32_t rs_flag0;   /* first rs flag word (run-local); REDUCE waits flag[rs_flag0 + chunk*n_recv + j] */
   int32_t n_counters; /* counters [0, n_counters) reset to 0 before each run */
   int32_t grid;       /* persistent CTAs (0: one per SM) */
   float alpha;        /* epilogue scale (STORE) */
-  int32_t reserved;
+  int32_t tile_n;     /* tile width = B box rows: 128, 160, 192, 224 or 256 (0: 256) */
 } ficco_plan_desc;
 
 int ficco_abi_version(void);
@@ -154,21 +177,31 @@ int ficco_ipc_close(void* ptr);
 int ficco_comm_create(int rank, int world, void* const* ws, size_t ws_bytes, int virtual_peers,
                       ficco_comm_t** out);
 int ficco_comm_destroy(ficco_comm_t* comm);
-int ficco_comm_epoch(ficco_comm_t* comm, uint32_t* epoch);
+int ficco_comm_epoch(ficco_comm_t* comm, uint32_t* runs); /* runs started so far */
 /* blocks until all work of the communicator finished; FICCO_ETIMEOUT if a kernel hit its flag timeout */
 int ficco_comm_check(ficco_comm_t* comm, void* stream);
-/* set local flag words [first, first+count) to value (stream-ordered on `stream`) */
+/* set local flag words [first, first+count) (absolute word index) to value, stream-ordered on `stream` */
 int ficco_comm_set_flags(ficco_comm_t* comm, int first, int count, uint32_t value, void* stream);
 
 /* plans */
 int ficco_plan_create(ficco_comm_t* comm, const ficco_plan_desc* desc, ficco_plan_t** out);
 int ficco_plan_destroy(ficco_plan_t* plan);
-/* one execution: copy program on the comm's copy stream, tile kernel on `stream`,
- * joined back into `stream`; advances the comm epoch. Non-blocking. */
+/* One execution, replayed from a CUDA graph (one per flag/workspace parity,
+ * instantiated on first use, kernel/copy nodes re-pointed when a/b/c change):
+ * run-local flag reset, copy program on the copy streams and the tile kernel,
+ * all joined into `stream`. Advances the comm's run counter. Non-blocking. */
 int ficco_plan_run(ficco_plan_t* plan, const void* a, const void* b, void* c, void* stream);
-/* only the copy program / only the tile kernel (for calibration of DIL/CIL) */
+/* Same semantics enqueued directly on streams (no graph); run_copies / run_tiles
+ * select the halves (calibration of DIL/CIL; a tile half alone only terminates if
+ * its flags are satisfied). */
 int ficco_plan_run_parts(ficco_plan_t* plan, const void* a, const void* b, void* c, void* stream,
                          int run_copies, int run_tiles);
+
+/* Optional measured timeline: buf (device, u64) receives %globaltimer ns stamps —
+ * [0, grid) CTA start, then per tile t {2t: flags satisfied / loads start,
+ * 2t+1: tile stored} at offset grid. NULL disables. Rebuilds the plan's graphs. */
+int ficco_plan_set_trace(ficco_plan_t* plan, void* buf);
+int ficco_plan_info(ficco_plan_t* plan, int* n_tiles, int* grid, int* n_streams);
 
 /* stand-alone primitives (calibration, benchmarks) */
 int ficco_gemm_bf16(const void* a, const void* b, void* c, int64_t m, int64_t n, int64_t k, float alpha,

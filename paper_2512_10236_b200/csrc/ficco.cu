@@ -52,11 +52,13 @@ typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_
                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 typedef CUresult (*PFN_writeValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 typedef CUresult (*PFN_waitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*PFN_waitValue64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
 
 struct Driver {
   PFN_encodeTiled encode = nullptr;
   PFN_writeValue32 write32 = nullptr;
   PFN_waitValue32 wait32 = nullptr;
+  PFN_waitValue64 wait64 = nullptr;
   bool ok = false;
 };
 
@@ -73,7 +75,8 @@ int get_driver(Driver** out) {
     };
     bool ok = get("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&d.encode)) &&
               get("cuStreamWriteValue32", reinterpret_cast<void**>(&d.write32)) &&
-              get("cuStreamWaitValue32", reinterpret_cast<void**>(&d.wait32));
+              get("cuStreamWaitValue32", reinterpret_cast<void**>(&d.wait32)) &&
+              get("cuStreamWaitValue64", reinterpret_cast<void**>(&d.wait64));
     d.ok = ok;
     if (!ok) {
       status = FICCO_ECUDA;
@@ -99,13 +102,29 @@ int encode_bf16_2d(Driver* drv, CUtensorMap* map, const void* base, int64_t rows
   return 0;
 }
 
-int g_kernel_configured = -1;  // device id the kernel attributes were set for
+// Resolve the tile-width instantiation: kernel entry point and dynamic smem size.
+int kernel_for(int tn, const void** fn, int* smem) {
+  switch (tn) {
+#define FICCO_CASE(T)                                                  \
+  case T:                                                              \
+    *fn = reinterpret_cast<const void*>(ficco::tile_gemm_kernel<T>);   \
+    *smem = ficco::TileCfg<T>::SMEM_BYTES;                             \
+    return 0;
+    FICCO_FOR_EACH_TN(FICCO_CASE)
+#undef FICCO_CASE
+    default: return fail(FICCO_EINVAL, "unsupported tile width " + std::to_string(tn));
+  }
+}
 
-int configure_kernel(int dev) {
-  if (g_kernel_configured == dev) return 0;
-  CK(cudaFuncSetAttribute(ficco::tile_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          ficco::SMEM_BYTES));
-  g_kernel_configured = dev;
+int configure_kernels(int dev) {
+  static int configured = -1;
+  if (configured == dev) return 0;
+#define FICCO_CFG(T)                                                                              \
+  CK(cudaFuncSetAttribute(ficco::tile_gemm_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                          ficco::TileCfg<T>::SMEM_BYTES));
+  FICCO_FOR_EACH_TN(FICCO_CFG)
+#undef FICCO_CFG
+  configured = dev;
   return 0;
 }
 
@@ -116,12 +135,24 @@ struct ficco_comm {
   bool virt = false;
   size_t ws_bytes = 0;
   std::vector<uint8_t*> ws;  // per rank, mapped into this process
-  std::vector<void*> owned;  // virtual-mode peer workspaces we allocated
-  uint32_t epoch = 0;
-  cudaStream_t copy = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_counters = nullptr;
+  uint32_t runs = 0;         // runs started; run r uses flag block / workspace parity r & 1
+  cudaStream_t copy[FICCO_MAX_STREAMS] = {};
+  cudaEvent_t ev_fork = nullptr;
+  cudaEvent_t ev_join[FICCO_MAX_STREAMS] = {};
+  cudaEvent_t ev_pool[FICCO_MAX_EVENTS] = {};
   Driver* drv = nullptr;
   uint32_t* flags(int r) { return reinterpret_cast<uint32_t*>(ws[r]); }
+  uint32_t* block(int r, uint32_t parity) { return flags(r) + parity * FICCO_FLAG_BLOCK; }
+};
+
+struct GraphInst {
+  cudaGraph_t graph = nullptr;  // kept alive: node handles index into it for exec updates
+  cudaGraphExec_t exec = nullptr;
+  cudaGraphNode_t kernel = nullptr;
+  std::vector<std::pair<cudaGraphNode_t, int>> user_copies;
+  const void* a = nullptr;
+  const void* b = nullptr;
+  void* c = nullptr;
 };
 
 struct ficco_plan {
@@ -129,13 +160,20 @@ struct ficco_plan {
   std::vector<ficco_copy_op> ops;
   ficco_tile* d_tiles = nullptr;
   int n_tiles = 0;
+  int n_streams = 0;
+  bool user_copies = false;  // some copy touches a call argument (kept out of the graph)
+  cudaGraphNode_t captured_kernel = nullptr;
+  std::vector<std::pair<cudaGraphNode_t, int>> captured_copies;  // (node, op index) touching call arguments
+  unsigned long long* trace = nullptr;  // optional device timeline buffer
+  int tile_n = 256;                     // B box rows = tile width (kernel instantiation)
   ficco_plan_desc desc{};
+  GraphInst graph[2];
 };
 
 namespace {
 
-int resolve(ficco_comm* c, int buf, int peer, int64_t off, int64_t par, const void* a, const void* b, void* cc,
-            uint8_t** out) {
+int resolve(ficco_comm* c, uint32_t parity, int buf, int peer, int64_t off, int64_t par, const void* a,
+            const void* b, void* cc, uint8_t** out) {
   uint8_t* base = nullptr;
   switch (buf) {
     case FICCO_BUF_A: base = (uint8_t*)a; break;
@@ -149,137 +187,258 @@ int resolve(ficco_comm* c, int buf, int peer, int64_t off, int64_t par, const vo
     default: return fail(FICCO_EINVAL, "bad buffer id " + std::to_string(buf));
   }
   if (!base) return fail(FICCO_EINVAL, "null buffer for id " + std::to_string(buf));
-  *out = base + off + ((c->epoch & 1u) ? par : 0);
+  *out = base + off + (parity ? par : 0);
   return 0;
 }
 
-struct Batch {
-  std::vector<void*> dst;
-  std::vector<void*> src;
-  std::vector<size_t> size;
-};
+bool is_user(int buf) { return buf == FICCO_BUF_A || buf == FICCO_BUF_B || buf == FICCO_BUF_C; }
 
-int flush(Batch& b, cudaStream_t s) {
-  if (b.dst.empty()) return 0;
-  cudaMemcpyAttributes attr{};
-  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-  attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-  size_t idx = 0, fail_idx = 0;
-  cudaError_t e = cudaMemcpyBatchAsync(b.dst.data(), b.src.data(), b.size.data(), b.dst.size(), &attr, &idx, 1,
-                                       &fail_idx, s);
-  if (e != cudaSuccess) {
-    // Older drivers: fall back to one cudaMemcpyAsync per copy (still copy engines).
-    cudaGetLastError();
-    for (size_t i = 0; i < b.dst.size(); ++i)
-      CK(cudaMemcpyAsync(b.dst[i], b.src[i], b.size[i], cudaMemcpyDefault, s));
+int enqueue_copy(ficco_comm* cm, uint32_t parity, const ficco_copy_op& op, const void* a, const void* b, void* c,
+                 cudaStream_t s) {
+  uint8_t *src, *dst;
+  int r = resolve(cm, parity, op.src_buf, op.peer, op.src_off, op.src_par, a, b, c, &src);
+  if (r) return r;
+  r = resolve(cm, parity, op.dst_buf, op.dst_peer, op.dst_off, op.dst_par, a, b, c, &dst);
+  if (r) return r;
+  if (op.height <= 1) {
+    CK(cudaMemcpyAsync(dst, src, size_t(op.width), cudaMemcpyDefault, s));
+  } else {
+    CK(cudaMemcpy2DAsync(dst, size_t(op.dst_pitch), src, size_t(op.src_pitch), size_t(op.width),
+                         size_t(op.height), cudaMemcpyDefault, s));
   }
-  b.dst.clear();
-  b.src.clear();
-  b.size.clear();
   return 0;
 }
 
-int run_copy_program(ficco_plan* p, const void* a, const void* b, void* c) {
+// One run enqueued on `s` + the copy streams (also used under stream capture to build the graph).
+int enqueue_run(ficco_plan* p, uint32_t parity, const void* a, const void* b, void* c, cudaStream_t s,
+                bool copies, bool tiles, int (*launch)(ficco_plan*, uint32_t, const void*, const void*, void*,
+                                                      cudaStream_t)) {
   ficco_comm* cm = p->comm;
-  Batch batch;
-  const uint32_t epoch = cm->epoch;
-  for (const ficco_copy_op& op : p->ops) {
-    switch (op.op) {
-      case FICCO_OP_COPY: {
-        uint8_t *src, *dst;
-        int r = resolve(cm, op.src_buf, op.peer, op.src_off, op.src_par, a, b, c, &src);
-        if (r) return r;
-        r = resolve(cm, op.dst_buf, op.dst_peer, op.dst_off, op.dst_par, a, b, c, &dst);
-        if (r) return r;
-        if (op.height <= 1) {
-          batch.dst.push_back(dst);
-          batch.src.push_back(src);
-          batch.size.push_back(size_t(op.width));
-        } else {
-          if ((r = flush(batch, cm->copy))) return r;
-          CK(cudaMemcpy2DAsync(dst, size_t(op.dst_pitch), src, size_t(op.src_pitch), size_t(op.width),
-                               size_t(op.height), cudaMemcpyDefault, cm->copy));
+  const uint32_t* blk = cm->block(cm->rank, parity);
+  // run-local flags and tile counters start at 0
+  CK(cudaMemsetAsync(const_cast<uint32_t*>(blk) + FICCO_FLAG_RUN_LOCAL, 0,
+                     4 * size_t(FICCO_FLAG_BLOCK - FICCO_FLAG_RUN_LOCAL), s));
+  const bool fork = copies && p->n_streams > 0;
+  if (fork) {
+    CK(cudaEventRecord(cm->ev_fork, s));
+    for (int i = 0; i < p->n_streams; ++i) CK(cudaStreamWaitEvent(cm->copy[i], cm->ev_fork, 0));
+  }
+  if (tiles) {
+    int r = launch(p, parity, a, b, c, s);
+    if (r) return r;
+  }
+  if (fork) {
+    for (const ficco_copy_op& op : p->ops) {
+      cudaStream_t cs = cm->copy[op.stream];
+      switch (op.op) {
+        case FICCO_OP_COPY: {
+          int r = enqueue_copy(cm, parity, op, a, b, c, cs);
+          if (r) return r;
+          if (is_user(op.src_buf) || is_user(op.dst_buf)) {  // remember it for graph re-pointing
+            cudaStreamCaptureStatus st;
+            CK(cudaStreamIsCapturing(cs, &st));
+            if (st == cudaStreamCaptureStatusActive) {
+              if (op.height > 1) return fail(FICCO_EINVAL, "2D copies of call arguments are not supported");
+              const cudaGraphNode_t* deps = nullptr;
+              size_t nd = 0;
+              CK(cudaStreamGetCaptureInfo(cs, &st, nullptr, nullptr, &deps, &nd));
+              if (nd != 1) return fail(FICCO_ECUDA, "graph capture: copy node not found");
+              p->captured_copies.push_back({deps[0], int(&op - p->ops.data())});
+            }
+          }
+          break;
         }
-        break;
+        case FICCO_OP_SIGNAL:
+          CK(cudaMemcpyAsync(cm->block(cm->rank, parity) + op.flag, cm->flags(cm->rank) + FICCO_FLAG_CONST_ONE, 4,
+                             cudaMemcpyDeviceToDevice, cs));
+          break;
+        case FICCO_OP_NOTIFY:
+          if (op.peer < 0 || op.peer >= cm->world) return fail(FICCO_EINVAL, "notify peer out of range");
+          if (!cm->virt)
+            CK(cudaMemcpyAsync(cm->block(op.peer, parity) + op.flag, cm->flags(cm->rank) + FICCO_FLAG_CONST_ONE, 4,
+                               cudaMemcpyDefault, cs));
+          break;
+        case FICCO_OP_WAIT:
+          if (!cm->virt) {
+            uint32_t* f = cm->block(cm->rank, parity) + op.flag;
+            CKD(cm->drv->wait32(cs, CUdeviceptr(f), 1u, CU_STREAM_WAIT_VALUE_GEQ));
+            CK(cudaMemcpyAsync(f, cm->flags(cm->rank) + FICCO_FLAG_CONST_ZERO, 4, cudaMemcpyDeviceToDevice, cs));
+          }
+          break;
+        case FICCO_OP_WAIT_COUNTER:
+          CKD(cm->drv->wait32(cs, CUdeviceptr(cm->block(cm->rank, parity) + FICCO_FLAG_COUNTERS + op.flag),
+                              op.value, CU_STREAM_WAIT_VALUE_GEQ));
+          break;
+        case FICCO_OP_BARRIER: {
+          if (cm->virt) break;
+          if (op.flag % 2) return fail(FICCO_EINVAL, "barrier word must be 8-byte aligned");
+          const int nwords = (cm->world + 7) / 8;
+          const uint8_t* one = reinterpret_cast<const uint8_t*>(cm->flags(cm->rank) + FICCO_FLAG_CONST_ONE);
+          for (int q = 0; q < cm->world; ++q) {  // byte `rank` of everyone's barrier (own included)
+            uint8_t* dst = reinterpret_cast<uint8_t*>(cm->block(q, parity) + op.flag) + cm->rank;
+            CK(cudaMemcpyAsync(dst, one, 1, cudaMemcpyDefault, cs));
+          }
+          uint64_t* mine = reinterpret_cast<uint64_t*>(cm->block(cm->rank, parity) + op.flag);
+          for (int w = 0; w < nwords; ++w) {
+            uint64_t want = 0;
+            for (int q = 8 * w; q < cm->world && q < 8 * w + 8; ++q) want |= uint64_t(1) << (8 * (q - 8 * w));
+            CKD(cm->drv->wait64(cs, CUdeviceptr(mine + w), want, CU_STREAM_WAIT_VALUE_GEQ));
+          }
+          CK(cudaMemcpyAsync(mine, cm->flags(cm->rank) + FICCO_FLAG_CONST_ZERO, 8 * size_t(nwords),
+                             cudaMemcpyDeviceToDevice, cs));
+          break;
+        }
+        case FICCO_OP_RECORD:
+          if (op.value >= FICCO_MAX_EVENTS) return fail(FICCO_EINVAL, "event slot out of range");
+          CK(cudaEventRecord(cm->ev_pool[op.value], cs));
+          break;
+        case FICCO_OP_STREAM_WAIT:
+          if (op.value >= FICCO_MAX_EVENTS) return fail(FICCO_EINVAL, "event slot out of range");
+          CK(cudaStreamWaitEvent(cs, cm->ev_pool[op.value], 0));
+          break;
+        default: return fail(FICCO_EINVAL, "bad copy opcode " + std::to_string(op.op));
       }
-      case FICCO_OP_SIGNAL: {
-        int r = flush(batch, cm->copy);
-        if (r) return r;
-        CKD(cm->drv->write32(cm->copy, CUdeviceptr(cm->flags(cm->rank) + op.flag), epoch, 0));
-        break;
-      }
-      case FICCO_OP_NOTIFY: {
-        int r = flush(batch, cm->copy);
-        if (r) return r;
-        if (op.peer < 0 || op.peer >= cm->world) return fail(FICCO_EINVAL, "notify peer out of range");
-        if (!cm->virt) CKD(cm->drv->write32(cm->copy, CUdeviceptr(cm->flags(op.peer) + op.flag), epoch, 0));
-        break;
-      }
-      case FICCO_OP_WAIT: {
-        int r = flush(batch, cm->copy);
-        if (r) return r;
-        // wait until flag >= epoch - value (value = epoch lag, e.g. 1 for "peer finished the previous run")
-        if (!cm->virt)
-          CKD(cm->drv->wait32(cm->copy, CUdeviceptr(cm->flags(cm->rank) + op.flag), epoch - op.value,
-                              CU_STREAM_WAIT_VALUE_GEQ));
-        break;
-      }
-      case FICCO_OP_WAIT_COUNTER: {
-        int r = flush(batch, cm->copy);
-        if (r) return r;
-        CKD(cm->drv->wait32(cm->copy, CUdeviceptr(cm->flags(cm->rank) + FICCO_FLAG_COUNTERS + op.flag), op.value,
-                            CU_STREAM_WAIT_VALUE_GEQ));
-        break;
-      }
-      default: return fail(FICCO_EINVAL, "bad copy opcode " + std::to_string(op.op));
+    }
+    for (int i = 0; i < p->n_streams; ++i) {
+      CK(cudaEventRecord(cm->ev_join[i], cm->copy[i]));
+      CK(cudaStreamWaitEvent(s, cm->ev_join[i], 0));
     }
   }
-  return flush(batch, cm->copy);
+  return 0;
 }
 
-int launch_tiles(ficco_plan* p, const void* a, const void* b, void* c, cudaStream_t s) {
+int make_params(ficco_plan* p, uint32_t parity, const void* a, const void* b, void* c, ficco::TileParams* prm,
+                int* grid) {
   ficco_comm* cm = p->comm;
   const ficco_plan_desc& d = p->desc;
-  if (p->n_tiles == 0) return 0;
-  int r = configure_kernel(cm->device);
-  if (r) return r;
-  ficco::TileParams prm;
-  memset(&prm, 0, sizeof(prm));
-  uint8_t* pa;
-  uint8_t* pb;
-  if ((r = resolve(cm, d.a.buf, -1, d.a.off, d.a.par, a, b, c, &pa))) return r;
-  if ((r = resolve(cm, d.b.buf, -1, d.b.off, d.b.par, a, b, c, &pb))) return r;
-  if ((r = encode_bf16_2d(cm->drv, &prm.tmap_a, pa, d.a.rows, d.k, d.a.ld, ficco::BM))) return r;
-  if ((r = encode_bf16_2d(cm->drv, &prm.tmap_b, pb, d.b.rows, d.k, d.b.ld, ficco::BN))) return r;
+  int r;
+  memset(prm, 0, sizeof(*prm));
+  uint8_t *pa, *pb;
+  if ((r = resolve(cm, parity, d.a.buf, -1, d.a.off, d.a.par, a, b, c, &pa))) return r;
+  if ((r = resolve(cm, parity, d.b.buf, -1, d.b.off, d.b.par, a, b, c, &pb))) return r;
+  if ((r = encode_bf16_2d(cm->drv, &prm->tmap_a, pa, d.a.rows, d.k, d.a.ld, ficco::BM))) return r;
+  if ((r = encode_bf16_2d(cm->drv, &prm->tmap_b, pb, d.b.rows, d.k, d.b.ld, p->tile_n))) return r;
   uint8_t* po = nullptr;
-  if (d.c.buf != FICCO_BUF_NONE && (r = resolve(cm, d.c.buf, -1, d.c.off, d.c.par, a, b, c, &po))) return r;
+  if (d.c.buf != FICCO_BUF_NONE && (r = resolve(cm, parity, d.c.buf, -1, d.c.off, d.c.par, a, b, c, &po))) return r;
   uint8_t* pp = nullptr;
-  if (d.part.buf != FICCO_BUF_NONE && (r = resolve(cm, d.part.buf, -1, d.part.off, d.part.par, a, b, c, &pp)))
+  if (d.part.buf != FICCO_BUF_NONE &&
+      (r = resolve(cm, parity, d.part.buf, -1, d.part.off, d.part.par, a, b, c, &pp)))
     return r;
-  prm.tiles = p->d_tiles;
-  prm.num_tiles = p->n_tiles;
-  prm.num_kb = int((d.k + ficco::BK - 1) / ficco::BK);
-  prm.out = reinterpret_cast<__nv_bfloat16*>(po);
-  prm.part = reinterpret_cast<__nv_bfloat16*>(pp);
-  prm.ld_out = d.c.ld;
-  prm.ld_part = d.part.ld;
-  prm.n_recv = d.n_recv;
+  prm->tiles = p->d_tiles;
+  prm->num_tiles = p->n_tiles;
+  prm->num_kb = int((d.k + ficco::BK - 1) / ficco::BK);
+  prm->out = reinterpret_cast<__nv_bfloat16*>(po);
+  prm->part = reinterpret_cast<__nv_bfloat16*>(pp);
+  prm->ld_out = d.c.ld;
+  prm->ld_part = d.part.ld;
+  prm->n_recv = d.n_recv;
   for (int j = 0; j < d.n_recv; ++j) {
     uint8_t* pr;
-    if ((r = resolve(cm, d.recv.buf, -1, d.recv.off + j * d.recv_slot, d.recv.par, a, b, c, &pr))) return r;
-    prm.recv[j] = reinterpret_cast<const __nv_bfloat16*>(pr);
+    if ((r = resolve(cm, parity, d.recv.buf, -1, d.recv.off + j * d.recv_slot, d.recv.par, a, b, c, &pr))) return r;
+    prm->recv[j] = reinterpret_cast<const __nv_bfloat16*>(pr);
   }
-  prm.ld_recv = d.recv.ld;
-  prm.rs_flag0 = d.rs_flag0;
-  prm.flags = cm->flags(cm->rank);
-  prm.counters = prm.flags + FICCO_FLAG_COUNTERS;
-  prm.abort_word = prm.flags + FICCO_FLAG_ABORT;
-  prm.epoch = cm->epoch;
-  prm.alpha = d.alpha;
-  int grid = d.grid > 0 ? d.grid : cm->sms;
-  if (grid > p->n_tiles) grid = p->n_tiles;
-  ficco::tile_gemm_kernel<<<grid, ficco::NUM_THREADS, ficco::SMEM_BYTES, s>>>(prm);
-  CK(cudaGetLastError());
+  prm->ld_recv = d.recv.ld;
+  prm->rs_flag0 = d.rs_flag0;
+  prm->flags = cm->block(cm->rank, parity);
+  prm->counters = cm->block(cm->rank, parity) + FICCO_FLAG_COUNTERS;
+  prm->abort_word = cm->flags(cm->rank) + FICCO_FLAG_ABORT;
+  prm->epoch = 1u;  // one-shot flags: wait for != 0
+  prm->alpha = d.alpha;
+  prm->trace = p->trace;
+  int g = d.grid > 0 ? d.grid : cm->sms;
+  if (g > p->n_tiles) g = p->n_tiles;
+  *grid = g;
+  return 0;
+}
+
+int launch_tiles(ficco_plan* p, uint32_t parity, const void* a, const void* b, void* c, cudaStream_t s) {
+  if (p->n_tiles == 0) return 0;
+  int r = configure_kernels(p->comm->device);
+  if (r) return r;
+  ficco::TileParams prm;
+  int grid, smem;
+  const void* fn;
+  if ((r = kernel_for(p->tile_n, &fn, &smem))) return r;
+  if ((r = make_params(p, parity, a, b, c, &prm, &grid))) return r;
+  void* args[] = {&prm};
+  CK(cudaLaunchKernel(fn, dim3(grid), dim3(ficco::NUM_THREADS), args, size_t(smem), s));
+  cudaStreamCaptureStatus st;
+  CK(cudaStreamIsCapturing(s, &st));
+  if (st == cudaStreamCaptureStatusActive) {  // remember the kernel node so later runs can re-point it
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    CK(cudaStreamGetCaptureInfo(s, &st, nullptr, nullptr, &deps, &nd));
+    p->captured_kernel = nd == 1 ? deps[0] : nullptr;
+  }
+  return 0;
+}
+
+int build_graph(ficco_plan* p, uint32_t parity, const void* a, const void* b, void* c, cudaStream_t s) {
+  GraphInst& gi = p->graph[parity];
+  cudaStream_t cap;
+  CK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+  CK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+  p->captured_kernel = nullptr;
+  p->captured_copies.clear();
+  int r = enqueue_run(p, parity, a, b, c, cap, true, true, launch_tiles);
+  cudaGraph_t graph = nullptr;
+  cudaError_t e = cudaStreamEndCapture(cap, &graph);
+  cudaStreamDestroy(cap);
+  if (r) {
+    if (graph) cudaGraphDestroy(graph);
+    return r;
+  }
+  if (e != cudaSuccess) return fail(FICCO_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+  gi.kernel = p->captured_kernel;
+  gi.user_copies = p->captured_copies;
+  p->captured_kernel = nullptr;
+  p->captured_copies.clear();
+  if (p->n_tiles > 0 && !gi.kernel) {
+    cudaGraphDestroy(graph);
+    return fail(FICCO_ECUDA, "graph capture: kernel node not found");
+  }
+  if (gi.exec) cudaGraphExecDestroy(gi.exec);
+  if (gi.graph) cudaGraphDestroy(gi.graph);
+  gi.exec = nullptr;
+  gi.graph = graph;
+  e = cudaGraphInstantiate(&gi.exec, graph, 0);
+  if (e != cudaSuccess) return fail(FICCO_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+  gi.a = a;
+  gi.b = b;
+  gi.c = c;
+  return 0;
+}
+
+int repoint_graph(ficco_plan* p, uint32_t parity, const void* a, const void* b, void* c) {
+  GraphInst& gi = p->graph[parity];
+  if (gi.kernel) {
+    ficco::TileParams prm;
+    int grid;
+    int r = make_params(p, parity, a, b, c, &prm, &grid);
+    if (r) return r;
+    void* args[] = {&prm};
+    const void* fn;
+    int smem;
+    if ((r = kernel_for(p->tile_n, &fn, &smem))) return r;
+    cudaKernelNodeParams kp{};
+    kp.func = const_cast<void*>(fn);
+    kp.gridDim = dim3(grid);
+    kp.blockDim = dim3(ficco::NUM_THREADS);
+    kp.sharedMemBytes = size_t(smem);
+    kp.kernelParams = args;
+    CK(cudaGraphExecKernelNodeSetParams(gi.exec, gi.kernel, &kp));
+  }
+  for (auto& nc : gi.user_copies) {
+    const ficco_copy_op& op = p->ops[nc.second];
+    uint8_t *src, *dst;
+    int r = resolve(p->comm, parity, op.src_buf, op.peer, op.src_off, op.src_par, a, b, c, &src);
+    if (r) return r;
+    if ((r = resolve(p->comm, parity, op.dst_buf, op.dst_peer, op.dst_off, op.dst_par, a, b, c, &dst))) return r;
+    CK(cudaGraphExecMemcpyNodeSetParams1D(gi.exec, nc.first, dst, src, size_t(op.width), cudaMemcpyDefault));
+  }
+  gi.a = a;
+  gi.b = b;
+  gi.c = c;
   return 0;
 }
 
@@ -304,6 +463,8 @@ int ficco_ws_alloc(size_t bytes, void** out) {
   void* p = nullptr;
   CK(cudaMalloc(&p, bytes));
   CK(cudaMemset(p, 0, FICCO_WS_DATA_OFFSET));
+  const uint32_t one = 0x01010101u;
+  CK(cudaMemcpy(reinterpret_cast<uint32_t*>(p) + FICCO_FLAG_CONST_ONE, &one, 4, cudaMemcpyHostToDevice));
   CK(cudaDeviceSynchronize());
   *out = p;
   return 0;
@@ -356,12 +517,15 @@ int ficco_comm_create(int rank, int world, void* const* ws, size_t ws_bytes, int
   c->ws_bytes = ws_bytes;
   c->drv = drv;
   for (int i = 0; i < world; ++i) c->ws.push_back(reinterpret_cast<uint8_t*>(ws[i]));
-  cudaError_t e = cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_counters, cudaEventDisableTiming);
+  cudaError_t e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
+  for (int i = 0; i < FICCO_MAX_STREAMS && e == cudaSuccess; ++i) {
+    e = cudaStreamCreateWithFlags(&c->copy[i], cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_join[i], cudaEventDisableTiming);
+  }
+  for (int i = 0; i < FICCO_MAX_EVENTS && e == cudaSuccess; ++i)
+    e = cudaEventCreateWithFlags(&c->ev_pool[i], cudaEventDisableTiming);
   if (e != cudaSuccess) {
-    delete c;
+    ficco_comm_destroy(c);
     return fail(FICCO_ECUDA, std::string("comm stream/event creation: ") + cudaGetErrorString(e));
   }
   *out = c;
@@ -370,25 +534,30 @@ int ficco_comm_create(int rank, int world, void* const* ws, size_t ws_bytes, int
 
 int ficco_comm_destroy(ficco_comm_t* c) {
   if (!c) return 0;
-  cudaStreamSynchronize(c->copy);
-  cudaStreamDestroy(c->copy);
-  cudaEventDestroy(c->ev_fork);
-  cudaEventDestroy(c->ev_join);
-  cudaEventDestroy(c->ev_counters);
+  for (int i = 0; i < FICCO_MAX_STREAMS; ++i) {
+    if (c->copy[i]) {
+      cudaStreamSynchronize(c->copy[i]);
+      cudaStreamDestroy(c->copy[i]);
+    }
+    if (c->ev_join[i]) cudaEventDestroy(c->ev_join[i]);
+  }
+  for (int i = 0; i < FICCO_MAX_EVENTS; ++i)
+    if (c->ev_pool[i]) cudaEventDestroy(c->ev_pool[i]);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   delete c;
   return 0;
 }
 
-int ficco_comm_epoch(ficco_comm_t* c, uint32_t* epoch) {
-  if (!c || !epoch) return fail(FICCO_EINVAL, "null argument");
-  *epoch = c->epoch;
+int ficco_comm_epoch(ficco_comm_t* c, uint32_t* runs) {
+  if (!c || !runs) return fail(FICCO_EINVAL, "null argument");
+  *runs = c->runs;
   return 0;
 }
 
 int ficco_comm_check(ficco_comm_t* c, void* stream) {
   if (!c) return fail(FICCO_EINVAL, "null comm");
   CK(cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream)));
-  CK(cudaStreamSynchronize(c->copy));
+  for (int i = 0; i < FICCO_MAX_STREAMS; ++i) CK(cudaStreamSynchronize(c->copy[i]));
   uint32_t abort_word = 0;
   CK(cudaMemcpy(&abort_word, c->flags(c->rank) + FICCO_FLAG_ABORT, 4, cudaMemcpyDeviceToHost));
   if (abort_word) return fail(FICCO_ETIMEOUT, "tile kernel timed out waiting for a readiness flag");
@@ -398,8 +567,7 @@ int ficco_comm_check(ficco_comm_t* c, void* stream) {
 int ficco_comm_set_flags(ficco_comm_t* c, int first, int count, uint32_t value, void* stream) {
   if (!c || first < 0 || count < 0 || first + count > FICCO_WS_FLAG_WORDS) return fail(FICCO_EINVAL, "bad flag range");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  for (int i = 0; i < count; ++i)
-    CKD(c->drv->write32(s, CUdeviceptr(c->flags(c->rank) + first + i), value, 0));
+  for (int i = 0; i < count; ++i) CKD(c->drv->write32(s, CUdeviceptr(c->flags(c->rank) + first + i), value, 0));
   return 0;
 }
 
@@ -408,15 +576,38 @@ int ficco_plan_create(ficco_comm_t* c, const ficco_plan_desc* d, ficco_plan_t** 
   if (d->n_tiles < 0 || d->n_ops < 0) return fail(FICCO_EINVAL, "negative program length");
   if (d->n_tiles > 0 && (d->k <= 0 || d->k % 8 != 0)) return fail(FICCO_EINVAL, "K must be a positive multiple of 8");
   if (d->n_recv < 0 || d->n_recv > ficco::MAX_RECV) return fail(FICCO_EINVAL, "too many receive slots");
-  if (d->n_counters < 0 || FICCO_FLAG_COUNTERS + d->n_counters >= FICCO_FLAG_ABORT)
+  if (d->n_counters < 0 || FICCO_FLAG_COUNTERS + d->n_counters > FICCO_FLAG_BLOCK)
     return fail(FICCO_EINVAL, "too many counters");
+  const int tile_n = d->tile_n > 0 ? d->tile_n : 256;
+  {
+    const void* fn;
+    int smem;
+    int r = kernel_for(tile_n, &fn, &smem);
+    if (r) return r;
+  }
   for (int i = 0; i < d->n_tiles; ++i) {
     const ficco_tile& t = d->tiles[i];
-    if (t.rows < 1 || t.rows > ficco::BM || t.cols < 32 || t.cols > ficco::BN || t.cols % 32)
+    if (t.rows < 1 || t.rows > ficco::BM || t.cols < 32 || t.cols > tile_n || t.cols % 32)
       return fail(FICCO_EINVAL, "tile " + std::to_string(i) + ": rows/cols out of range");
     if (t.mode < FICCO_EPI_STORE || t.mode > FICCO_EPI_REDUCE)
       return fail(FICCO_EINVAL, "tile " + std::to_string(i) + ": bad epilogue mode");
-    if (t.flag >= FICCO_FLAG_COUNTERS) return fail(FICCO_EINVAL, "tile flag index out of range");
+    if (t.flag >= 0) {
+      const int last = t.flag + (t.nflag - 1) + (t.kseg ? (int((d->k + 63) / 64) / t.kseg) * t.kstride : 0);
+      if (t.nflag < 1 || last >= FICCO_FLAG_BLOCK || t.kseg < 0)
+        return fail(FICCO_EINVAL, "tile " + std::to_string(i) + ": flag range out of the flag block");
+    }
+  }
+  int n_streams = 0;
+  bool user = false;
+  for (int i = 0; i < d->n_ops; ++i) {
+    const ficco_copy_op& op = d->ops[i];
+    if (op.stream < 0 || op.stream >= FICCO_MAX_STREAMS) return fail(FICCO_EINVAL, "op stream out of range");
+    if (op.op < FICCO_OP_COPY || op.op > FICCO_OP_STREAM_WAIT) return fail(FICCO_EINVAL, "bad copy opcode");
+    if ((op.op == FICCO_OP_SIGNAL || op.op == FICCO_OP_NOTIFY || op.op == FICCO_OP_WAIT ||
+         op.op == FICCO_OP_BARRIER) && (op.flag < 0 || op.flag + 4 > FICCO_FLAG_BLOCK))
+      return fail(FICCO_EINVAL, "op flag index out of range");
+    if (op.op == FICCO_OP_COPY && (is_user(op.src_buf) || is_user(op.dst_buf))) user = true;
+    if (op.stream + 1 > n_streams) n_streams = op.stream + 1;
   }
   auto* p = new ficco_plan();
   p->comm = c;
@@ -425,6 +616,9 @@ int ficco_plan_create(ficco_comm_t* c, const ficco_plan_desc* d, ficco_plan_t** 
   p->desc.ops = nullptr;
   p->desc.tiles = nullptr;
   p->n_tiles = d->n_tiles;
+  p->tile_n = tile_n;
+  p->n_streams = n_streams;
+  p->user_copies = user;
   if (d->n_tiles > 0) {
     size_t bytes = sizeof(ficco_tile) * size_t(d->n_tiles);
     cudaError_t e = cudaMalloc(&p->d_tiles, bytes);
@@ -441,48 +635,70 @@ int ficco_plan_create(ficco_comm_t* c, const ficco_plan_desc* d, ficco_plan_t** 
 
 int ficco_plan_destroy(ficco_plan_t* p) {
   if (!p) return 0;
+  for (auto& g : p->graph) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (g.graph) cudaGraphDestroy(g.graph);
+  }
   if (p->d_tiles) cudaFree(p->d_tiles);
   delete p;
+  return 0;
+}
+
+int ficco_plan_set_trace(ficco_plan_t* p, void* buf) {
+  if (!p) return fail(FICCO_EINVAL, "null plan");
+  p->trace = reinterpret_cast<unsigned long long*>(buf);
+  for (auto& g : p->graph) {  // rebuild on next run with the new kernel parameters
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (g.graph) cudaGraphDestroy(g.graph);
+    g = GraphInst{};
+  }
+  return 0;
+}
+
+int ficco_plan_info(ficco_plan_t* p, int* n_tiles, int* grid, int* n_streams) {
+  if (!p) return fail(FICCO_EINVAL, "null plan");
+  int g = p->desc.grid > 0 ? p->desc.grid : p->comm->sms;
+  if (g > p->n_tiles) g = p->n_tiles;
+  if (n_tiles) *n_tiles = p->n_tiles;
+  if (grid) *grid = g;
+  if (n_streams) *n_streams = p->n_streams;
   return 0;
 }
 
 int ficco_plan_run_parts(ficco_plan_t* p, const void* a, const void* b, void* c, void* stream, int run_copies,
                          int run_tiles) {
   if (!p) return fail(FICCO_EINVAL, "null plan");
-  ficco_comm* cm = p->comm;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  cm->epoch += 1;
-  int r;
-  // counters are per-run: reset them on the compute stream before anything waits on them
-  if (p->desc.n_counters > 0) {
-    CK(cudaMemsetAsync(cm->flags(cm->rank) + FICCO_FLAG_COUNTERS, 0, 4 * size_t(p->desc.n_counters), s));
-  }
-  const bool copies = run_copies && !p->ops.empty();
-  if (copies) {
-    CK(cudaEventRecord(cm->ev_fork, s));
-    CK(cudaStreamWaitEvent(cm->copy, cm->ev_fork, 0));
-  }
-  if (run_tiles && (r = launch_tiles(p, a, b, c, s))) return r;
-  if (copies) {
-    if ((r = run_copy_program(p, a, b, c))) return r;
-    CK(cudaEventRecord(cm->ev_join, cm->copy));
-    CK(cudaStreamWaitEvent(s, cm->ev_join, 0));
-  }
-  return 0;
+  const uint32_t parity = p->comm->runs & 1u;
+  p->comm->runs += 1;
+  return enqueue_run(p, parity, a, b, c, s, run_copies != 0, run_tiles != 0, launch_tiles);
 }
 
 int ficco_plan_run(ficco_plan_t* p, const void* a, const void* b, void* c, void* stream) {
-  return ficco_plan_run_parts(p, a, b, c, stream, 1, 1);
+  if (!p) return fail(FICCO_EINVAL, "null plan");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const uint32_t parity = p->comm->runs & 1u;
+  GraphInst& gi = p->graph[parity];
+  int r;
+  if (!gi.exec) {
+    if ((r = build_graph(p, parity, a, b, c, s))) return r;
+  } else if (gi.a != a || gi.b != b || gi.c != c) {
+    if ((r = repoint_graph(p, parity, a, b, c))) return r;
+  }
+  p->comm->runs += 1;
+  CK(cudaGraphLaunch(gi.exec, s));
+  return 0;
 }
 
 int ficco_copy_batch(void* const* dsts, const void* const* srcs, const size_t* sizes, size_t count, void* stream) {
-  Batch b;
-  for (size_t i = 0; i < count; ++i) {
-    b.dst.push_back(dsts[i]);
-    b.src.push_back(const_cast<void*>(srcs[i]));
-    b.size.push_back(sizes[i]);
-  }
-  return flush(b, reinterpret_cast<cudaStream_t>(stream));
+  if (count == 0) return 0;
+  cudaMemcpyAttributes attr{};
+  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+  attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+  size_t idx = 0, fail_idx = 0;
+  CK(cudaMemcpyBatchAsync(const_cast<void**>(dsts), const_cast<void**>(srcs), const_cast<size_t*>(sizes), count,
+                          &attr, &idx, 1, &fail_idx, reinterpret_cast<cudaStream_t>(stream)));
+  return 0;
 }
 
 int ficco_gemm_bf16(const void* a, const void* b, void* c, int64_t m, int64_t n, int64_t k, float alpha, int grid,
@@ -508,17 +724,31 @@ int ficco_gemm_bf16(const void* a, const void* b, void* c, int64_t m, int64_t n,
     void* w = ws_by_dev[dev];
     int r = ficco_comm_create(0, 1, &w, FICCO_WS_DATA_OFFSET, 1, &cm);
     if (r) return r;
+    // tile width minimising (waves x width) over the instantiated widths
+    int tn = 256;
+    double best = 1e30;
+    const int widths[] = {256, 224, 192, 160, 128};
+    for (int w : widths) {
+      const int64_t tiles_n = (n + w - 1) / w, tiles_m = (m + ficco::BM - 1) / ficco::BM;
+      const int64_t waves = (tiles_n * tiles_m + cm->sms - 1) / cm->sms;
+      const double cost = double(waves) * w * (1.0 + 0.02 * (256.0 / w));  // small per-tile overhead term
+      if (cost < best - 1e-9) {
+        best = cost;
+        tn = w;
+      }
+    }
     std::vector<ficco_tile> tiles;
     for (int64_t i = 0; i < m; i += ficco::BM)
-      for (int64_t j = 0; j < n; j += ficco::BN) {
+      for (int64_t j = 0; j < n; j += tn) {
         ficco_tile t{};
         t.a_row = int32_t(i);
         t.b_row = int32_t(j);
         t.c_row = int32_t(i);
         t.c_col = int32_t(j);
         t.rows = int16_t(m - i < ficco::BM ? m - i : ficco::BM);
-        t.cols = int16_t(n - j < ficco::BN ? n - j : ficco::BN);
+        t.cols = int16_t(n - j < tn ? n - j : tn);
         t.flag = -1;
+        t.nflag = 0;
         t.mode = FICCO_EPI_STORE;
         tiles.push_back(t);
       }
@@ -528,6 +758,7 @@ int ficco_gemm_bf16(const void* a, const void* b, void* c, int64_t m, int64_t n,
     d.grid = grid;
     d.alpha = 1.0f;
     d.k = k;
+    d.tile_n = tn;
     ficco_plan* p;
     if ((r = ficco_plan_create(cm, &d, &p))) return r;
     it = cache.emplace(key, std::make_pair(cm, p)).first;
@@ -538,7 +769,7 @@ int ficco_gemm_bf16(const void* a, const void* b, void* c, int64_t m, int64_t n,
   p->desc.c = ficco_operand{FICCO_BUF_C, 0, 0, 0, m, n};
   p->desc.k = k;
   p->desc.alpha = alpha;
-  return ficco_plan_run_parts(p, a, b, c, stream, 0, 1);
+  return ficco_plan_run_parts(p, a, b, c, stream, 0, 1);  // no flags: direct launch
 }
 
 }  // extern "C"

@@ -29,18 +29,26 @@
 namespace ficco {
 
 constexpr int BM = 128;
-constexpr int BN = 256;
-constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle row
+constexpr int BN_MAX = 256;  // widest tile (UMMA N <= 256); per-plan tile width TN in {128,...,256}
+constexpr int BK = 64;       // 64 bf16 = 128 B = one swizzle row
 constexpr int UMMA_K = 16;
-constexpr int STAGES = 4;
 constexpr int A_STAGE = BM * BK * 2;  // 16 KiB
-constexpr int B_STAGE = BN * BK * 2;  // 32 KiB
 constexpr int NUM_THREADS = 192;
 constexpr int EPI_THREADS = 128;
-constexpr uint32_t TMEM_COLS = 512;  // two 128x256 fp32 accumulators
+constexpr uint32_t TMEM_COLS = 512;  // two accumulators of up to 256 fp32 columns
 constexpr int MAX_RECV = 15;
-constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * (A_STAGE + B_STAGE) + 256;
 constexpr uint32_t SPIN_LIMIT = 1u << 25;  // ~4-10 s of polling before declaring a timeout
+constexpr int SMEM_LIMIT = 227 * 1024;
+
+// Per tile-width configuration: as many pipeline stages as fit in shared memory.
+template <int TN>
+struct TileCfg {
+  static_assert(TN % 32 == 0 && TN >= 64 && TN <= 256, "tile width");
+  static constexpr int B_STAGE = TN * BK * 2;
+  static constexpr int STAGE = A_STAGE + B_STAGE;
+  static constexpr int STAGES = (SMEM_LIMIT - 1024 - 256) / STAGE > 6 ? 6 : (SMEM_LIMIT - 1024 - 256) / STAGE;
+  static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE + 256;
+};
 
 struct alignas(64) TileParams {
   CUtensorMap tmap_a;
@@ -56,12 +64,21 @@ struct alignas(64) TileParams {
   int64_t ld_recv;
   int n_recv;
   int rs_flag0;
-  uint32_t* flags;         // local flag words
+  uint32_t* flags;         // local flag block of this run's parity
   uint32_t* counters;      // local tile counters
   uint32_t* abort_word;
-  uint32_t epoch;
+  uint32_t epoch;          // value a flag must reach (1: one-shot flags)
   float alpha;
+  // optional timeline (ns, %globaltimer): [0, gridDim) CTA start; then per tile
+  // {loads may start (flags satisfied), accumulator stored}
+  unsigned long long* trace;
 };
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Poll a flag written by another agent (copy engine memop, peer GPU) until it
 // reaches `epoch` (wrap-safe). On timeout raise the abort word and give up so
@@ -80,8 +97,10 @@ __device__ __forceinline__ void wait_flag(const uint32_t* f, uint32_t epoch, uin
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
+template <int TN>
 __device__ __forceinline__ void producer_loop(const TileParams& p, uint8_t* sA, uint8_t* sB, uint64_t* full,
                                               uint64_t* empty) {
+  using Cfg = TileCfg<TN>;
   const uint64_t hint_a = policy_evict_first();
   const uint64_t hint_b = policy_evict_last();
   uint32_t stage = 0, phase = 0;
@@ -90,16 +109,19 @@ __device__ __forceinline__ void producer_loop(const TileParams& p, uint8_t* sA, 
     for (int kb = 0; kb < p.num_kb; ++kb) {
       if (td.flag >= 0) {
         if (td.kseg == 0) {
-          if (kb == 0) wait_flag(p.flags + td.flag, p.epoch, p.abort_word);
+          if (kb == 0)
+            for (int f = 0; f < td.nflag; ++f) wait_flag(p.flags + td.flag + f, p.epoch, p.abort_word);
         } else if (kb % td.kseg == 0) {
-          wait_flag(p.flags + td.flag + kb / td.kseg, p.epoch, p.abort_word);
+          const int base = td.flag + (kb / td.kseg) * td.kstride;
+          for (int f = 0; f < td.nflag; ++f) wait_flag(p.flags + base + f, p.epoch, p.abort_word);
         }
       }
+      if (kb == 0 && p.trace) p.trace[gridDim.x + 2 * t] = globaltimer();
       mbar_wait(&empty[stage], phase ^ 1u);
-      mbar_arrive_expect_tx(&full[stage], A_STAGE + B_STAGE);
+      mbar_arrive_expect_tx(&full[stage], Cfg::STAGE);
       tma_load_2d(sA + stage * A_STAGE, &p.tmap_a, &full[stage], kb * BK, td.a_row, hint_a);
-      tma_load_2d(sB + stage * B_STAGE, &p.tmap_b, &full[stage], kb * BK, td.b_row, hint_b);
-      if (++stage == STAGES) {
+      tma_load_2d(sB + stage * Cfg::B_STAGE, &p.tmap_b, &full[stage], kb * BK, td.b_row, hint_b);
+      if (++stage == Cfg::STAGES) {
         stage = 0;
         phase ^= 1u;
       }
@@ -107,27 +129,29 @@ __device__ __forceinline__ void producer_loop(const TileParams& p, uint8_t* sA, 
   }
 }
 
+template <int TN>
 __device__ __forceinline__ void mma_loop(const TileParams& p, uint8_t* sA, uint8_t* sB, uint64_t* full,
                                          uint64_t* empty, uint64_t* tfull, uint64_t* tempty, uint32_t tmem) {
-  constexpr uint32_t idesc = make_idesc_bf16(BM, BN);
+  using Cfg = TileCfg<TN>;
+  constexpr uint32_t idesc = make_idesc_bf16(BM, TN);
   uint32_t stage = 0, phase = 0, it = 0;
   for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
     const uint32_t acc = it & 1u;
     mbar_wait(&tempty[acc], ((it >> 1) & 1u) ^ 1u);
     tc_fence_after();
-    const uint32_t d = tmem + acc * BN;
+    const uint32_t d = tmem + acc * BN_MAX;
     for (int kb = 0; kb < p.num_kb; ++kb) {
       mbar_wait(&full[stage], phase);
       tc_fence_after();
       const uint64_t ad = make_sdesc_sw128(smem_addr(sA + stage * A_STAGE));
-      const uint64_t bd = make_sdesc_sw128(smem_addr(sB + stage * B_STAGE));
+      const uint64_t bd = make_sdesc_sw128(smem_addr(sB + stage * Cfg::B_STAGE));
 #pragma unroll
       for (int k = 0; k < BK / UMMA_K; ++k) {
         // +32 bytes per K step inside the 128B swizzle row (>>4 in the descriptor)
         umma_bf16(d, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc, (kb | k) != 0);
       }
       umma_commit(&empty[stage]);  // smem slot free once these MMAs retire
-      if (++stage == STAGES) {
+      if (++stage == Cfg::STAGES) {
         stage = 0;
         phase ^= 1u;
       }
@@ -136,6 +160,7 @@ __device__ __forceinline__ void mma_loop(const TileParams& p, uint8_t* sA, uint8
   }
 }
 
+template <int TN>
 __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfull, uint64_t* tempty,
                                               uint32_t tmem) {
   const int warp = threadIdx.x / 32;
@@ -155,7 +180,7 @@ __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfu
     }
     mbar_wait(&tfull[acc], (it >> 1) & 1u);
     tc_fence_after();
-    const uint32_t taddr = tmem + (uint32_t(quarter * 32) << 16) + acc * BN;
+    const uint32_t taddr = tmem + (uint32_t(quarter * 32) << 16) + acc * BN_MAX;
     const bool row_ok = row < td.rows;
     __nv_bfloat16* dst;
     if (td.mode == FICCO_EPI_STORE_SIGNAL)
@@ -164,7 +189,7 @@ __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfu
       dst = p.out + int64_t(td.c_row + row) * p.ld_out + td.c_col;
     const float scale = td.mode == FICCO_EPI_STORE ? p.alpha : 1.0f;
 #pragma unroll 1
-    for (int cc = 0; cc < BN / 32; ++cc) {
+    for (int cc = 0; cc < TN / 32; ++cc) {
       uint32_t v[32];
       tmem_ld_32x32b_x32(taddr + cc * 32, v);
       tmem_ld_wait();
@@ -203,6 +228,7 @@ __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfu
     }
     tc_fence_before();
     mbar_arrive(&tempty[acc]);
+    if (p.trace && threadIdx.x == 64) p.trace[gridDim.x + 2 * t + 1] = globaltimer();
     if (td.mode == FICCO_EPI_STORE_SIGNAL) {
       named_bar_sync(1, EPI_THREADS);  // every row of the tile is stored
       if (threadIdx.x == 64) {
@@ -213,23 +239,26 @@ __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfu
   }
 }
 
+template <int TN>
 __global__ void __launch_bounds__(NUM_THREADS, 1) tile_gemm_kernel(const __grid_constant__ TileParams p) {
+  using Cfg = TileCfg<TN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = base;
-  uint8_t* sB = base + STAGES * A_STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
+  uint8_t* sB = base + Cfg::STAGES * A_STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + Cfg::STAGES * Cfg::B_STAGE);
+  uint64_t* empty = full + Cfg::STAGES;
+  uint64_t* tfull = empty + Cfg::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
+  if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x] = globaltimer();
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&p.tmap_a);
     tma_prefetch_desc(&p.tmap_b);
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < Cfg::STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -246,11 +275,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tile_gemm_kernel(const __grid_
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) producer_loop(p, sA, sB, full, empty);
+    if (lane == 0) producer_loop<TN>(p, sA, sB, full, empty);
   } else if (warp == 1) {
-    if (lane == 0) mma_loop(p, sA, sB, full, empty, tfull, tempty, tmem);
+    if (lane == 0) mma_loop<TN>(p, sA, sB, full, empty, tfull, tempty, tmem);
   } else {
-    epilogue_loop(p, tfull, tempty, tmem);
+    epilogue_loop<TN>(p, tfull, tempty, tmem);
   }
 
   tc_fence_before();
@@ -258,5 +287,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tile_gemm_kernel(const __grid_
   tc_fence_after();
   if (warp == 1) tmem_dealloc(tmem, TMEM_COLS);
 }
+
+// Tile widths instantiated for the per-plan choice (see lowering.choose_tile_n).
+#define FICCO_FOR_EACH_TN(X) X(128) X(160) X(192) X(224) X(256)
 
 }  // namespace ficco

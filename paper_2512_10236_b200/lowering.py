@@ -48,19 +48,22 @@ from .domain import Scenario
 from .routing import (ExecutionPlan, GatherSpec, GemmSpec, PlanError, ScatterSpec, ScheduleKind, TransferSpec,
                       build_plan)
 from .runtime import (BUF_A, BUF_B, BUF_C, BUF_NONE, BUF_WS, EPI_REDUCE, EPI_STORE, EPI_STORE_SIGNAL,
-                      FICCO_FLAG_COUNTERS, FICCO_WS_DATA_OFFSET, MAX_RECV, OP_COPY, OP_NOTIFY, OP_SIGNAL,
-                      OP_WAIT, OP_WAIT_COUNTER, TILE_K, TILE_M, TILE_N, CopyOp, Operand, PlanDesc, Tile)
+                      FICCO_WS_DATA_OFFSET, MAX_RECV, OP_BARRIER, OP_COPY, OP_NOTIFY, OP_RECORD, OP_SIGNAL,
+                      OP_STREAM_WAIT, OP_WAIT, OP_WAIT_COUNTER, TILE_K, TILE_M, TILE_WIDTHS, CopyOp, Operand, PlanDesc,
+                      Tile)
 
-# flag word map (local flag area of each rank's workspace)
-F_PUB = 0        # + src rank: "src has published this epoch's shard"
-F_LOCAL = 64     # local shard copied into its own slot
-F_ROUND = 65     # + round c: all chunks of round c landed
-F_XFER = 256     # + c*G + p: chunk (p, c) landed (unfused)
-F_RING = 512     # + step i: ring step i landed
-F_RINGN = 576    # + step i: left neighbour holds the shard we pull at step i+1
-F_ALL = 640      # serial: every shard landed
-F_DONE = 704     # + src rank: "src finished its previous run" (RS receive-buffer reuse)
-F_RS = 1024      # + chunk*(G-1) + slot: partial chunk from a peer landed (RS)
+# Flag words, relative to the run's parity block (one-shot words, include/ficco.h).
+# [0, 256): cross-rank words, written by peers and reset by their consumer
+F_PUB = 0        # 8-byte barrier words (byte r = rank r published this run's shard)   [0, 4)
+F_DONE = 4       # 8-byte barrier words (byte r = rank r started this run; RS receive) [4, 8)
+F_RINGN = 64     # + step i: the left neighbour holds the shard we pull at ring step i+1
+# [256, 4096): run-local flags, reset when the run starts
+F_LOCAL = 256    # the local shard sits in its own slot
+F_XFER = 320     # + c*G + p: chunk c of rank p landed (p = own rank is set with LOCAL)
+F_RING = 704     # + step i: ring step i landed
+F_RS = 1024      # + chunk*(G-1) + slot: a peer's partial chunk landed (RS)
+EV_START = 0     # event slot: the cross-rank barrier passed
+MAX_WORLD = 16
 
 ELT = 2  # bf16
 
@@ -99,11 +102,33 @@ def _operand(buf, rows, ld, off=0, par=0) -> Operand:
     return o
 
 
-def _tile(a_row, b_row, c_row, c_col, rows, cols, flag=-1, kseg=0, mode=EPI_STORE, chunk=0, recv_row=0) -> Tile:
+def _tile(a_row, b_row, c_row, c_col, rows, cols, flag=-1, nflag=0, kseg=0, kstride=0, mode=EPI_STORE, chunk=0,
+          recv_row=0) -> Tile:
     t = Tile()
-    t.a_row, t.b_row, t.c_row, t.c_col = a_row, b_row, c_row, c_col
-    t.rows, t.cols, t.flag, t.kseg, t.mode, t.chunk, t.recv_row = rows, cols, flag, kseg, mode, chunk, recv_row
+    t.a_row, t.b_row, t.c_row, t.c_col, t.recv_row = a_row, b_row, c_row, c_col, recv_row
+    t.rows, t.cols, t.flag, t.nflag = rows, cols, flag, (nflag if flag >= 0 else 0)
+    t.kseg, t.kstride, t.mode, t.chunk = kseg, kstride, mode, chunk
     return t
+
+
+B200_SMS = 148
+
+
+def choose_tile_n(tiles_for_width, sms: int = B200_SMS) -> int:
+    """Tile width (UMMA N, B box rows) minimising persistent-kernel waves x width.
+
+    ``tiles_for_width(w)`` is the tile count at width w. A wave of the
+    persistent kernel is ``sms`` tiles; its duration scales with w, plus a
+    small per-tile fixed cost (prologue/epilogue). E.g. C2's N = 3584 at 256
+    gives 896 tiles = 6.05 waves (7 issued), at 224 gives 1024 tiles = 6.92.
+    """
+    best, best_w = None, TILE_WIDTHS[0]
+    for w in TILE_WIDTHS:
+        n = tiles_for_width(w)
+        cost = -(-n // sms) * w * (1.0 + 0.02 * 256 / w)
+        if best is None or cost < best - 1e-9:
+            best, best_w = cost, w
+    return best_w
 
 
 def _check_shape(m: int, n: int, k: int) -> None:
@@ -118,17 +143,26 @@ def _my_gemms(plan: ExecutionPlan, rank: int) -> list[GemmSpec]:
 
 
 def _publish(ops: list, g: int, world: int, row_bytes: int, shard_rows: int, gather_off: int, par: int,
-             src_buf: int) -> None:
-    """Local shard -> own slot, then the cross-rank publish barrier."""
+             src_buf: int, rounds: int) -> None:
+    """Local shard -> own slot (before the fork, on the compute stream), then the publish barrier.
+
+    Stream 0 marks the local rows present (LOCAL), runs the cross-rank
+    barrier (each rank sets its byte in everyone's PUB word and waits for all
+    bytes), records EV_START (every pull chain waits on it), and finally sets
+    XFER[c, g] for every round c so round-granular waits can span all G ranks.
+    """
     ops.append(_op(OP_COPY, src_buf=src_buf, dst_buf=BUF_WS, src_off=0, dst_off=gather_off + g * shard_rows * row_bytes,
-                   dst_par=par, width=shard_rows * row_bytes))
-    ops.append(_op(OP_SIGNAL, flag=F_LOCAL))
-    for p in range(world):
-        if p != g:
-            ops.append(_op(OP_NOTIFY, peer=p, flag=F_PUB + g))
-    for p in range(world):
-        if p != g:
-            ops.append(_op(OP_WAIT, flag=F_PUB + p))
+                   dst_par=par, width=shard_rows * row_bytes, stream=0))
+    ops.append(_op(OP_SIGNAL, flag=F_LOCAL, stream=0))
+    ops.append(_op(OP_BARRIER, flag=F_PUB, stream=0))
+    ops.append(_op(OP_RECORD, value=EV_START, stream=0))
+    for c in range(rounds):  # off the pull chains' critical path
+        ops.append(_op(OP_SIGNAL, flag=F_XFER + c * world + g, stream=0))
+
+
+def _peer_stream(p: int, g: int) -> int:
+    """Copy stream pulling from (or pushing to) peer p: one copy-engine chain per peer."""
+    return 1 + (p if p < g else p - 1)
 
 
 def lower_ag(plan: ExecutionPlan, rank: int, gathered: str = "A", alpha: float = 1.0, grid: int = 0,
@@ -158,82 +192,82 @@ def lower_ag(plan: ExecutionPlan, rank: int, gathered: str = "A", alpha: float =
     low.ws_bytes = FICCO_WS_DATA_OFFSET + 2 * low.gather_par
     ops = low.ops
     src_buf = BUF_A if gathered == "A" else BUF_B
-    _publish(ops, g, G, row_bytes, R, low.gather_off, low.gather_par, src_buf)
+    if G > MAX_WORLD:
+        raise PlanError(f"at most {MAX_WORLD} ranks")
+    _publish(ops, g, G, row_bytes, R, low.gather_off, low.gather_par, src_buf, G)
 
-    def pull(p: int, row0: int, nrows: int) -> CopyOp:
+    def pull(p: int, row0: int, nrows: int, stream: int) -> CopyOp:
         off = low.gather_off + row0 * row_bytes
         return _op(OP_COPY, peer=p, src_buf=BUF_WS, dst_buf=BUF_WS, src_off=off, dst_off=off,
-                   src_par=low.gather_par, dst_par=low.gather_par, width=nrows * row_bytes)
+                   src_par=low.gather_par, dst_par=low.gather_par, width=nrows * row_bytes, stream=stream)
 
-    # ---- copy program (mirrors the plan's TransferSpecs arriving at this rank)
+    # ---- copy program: the plan's TransferSpecs arriving at this rank, one pull chain per source peer
     xfers = [t.kind for t in plan.tasks if isinstance(t.kind, TransferSpec) and t.kind.dst == g]
     kseg = 0
-    if kind is ScheduleKind.SERIAL:
-        for x in xfers:
-            ops.append(pull(x.src, x.src * R, R))
-        ops.append(_op(OP_SIGNAL, flag=F_ALL))
-    elif kind is ScheduleKind.SHARD_OVERLAP_P2P:
+    if kind is ScheduleKind.SHARD_OVERLAP_P2P:
+        # store-and-forward ring on one chain: step i pulls shard (g-i) from the left neighbour
         right = (g + 1) % G
-        if G > 1:
-            ops.append(_op(OP_NOTIFY, peer=right, flag=F_RINGN + 0))
-        for x in xfers:  # step i = round_idx + 1, from the left neighbour
+        ops.append(_op(OP_STREAM_WAIT, value=EV_START, stream=1))
+        ops.append(_op(OP_NOTIFY, peer=right, flag=F_RINGN + 0, stream=1))
+        for x in xfers:
             i = x.round_idx + 1
             shard = (g - i) % G
-            ops.append(_op(OP_WAIT, flag=F_RINGN + i - 1))
-            ops.append(pull(x.src, shard * R, R))
-            ops.append(_op(OP_SIGNAL, flag=F_RING + i))
+            ops.append(_op(OP_WAIT, flag=F_RINGN + i - 1, stream=1))
+            ops.append(pull(x.src, shard * R, R, 1))
+            ops.append(_op(OP_SIGNAL, flag=F_RING + i, stream=1))
             if i < G - 1:
-                ops.append(_op(OP_NOTIFY, peer=right, flag=F_RINGN + i))
-    elif kind is ScheduleKind.UNIFORM_FUSED_2D:
-        b = K // G
-        if b % TILE_K:
-            raise PlanError(f"uniform_fused_2d on B200 needs K/G={b} to be a multiple of {TILE_K}")
-        kseg = b // TILE_K
-        last_round = None
+                ops.append(_op(OP_NOTIFY, peer=right, flag=F_RINGN + i, stream=1))
+    else:
+        started: set[int] = set()
+        if kind is ScheduleKind.UNIFORM_FUSED_2D:
+            b = K // G
+            if b % TILE_K:
+                raise PlanError(f"uniform_fused_2d on B200 needs K/G={b} to be a multiple of {TILE_K}")
+            kseg = b // TILE_K
         for x in xfers:
-            if last_round is not None and x.round_idx != last_round:
-                ops.append(_op(OP_SIGNAL, flag=F_ROUND + last_round))
+            st = _peer_stream(x.src, g)
+            if x.src not in started:
+                ops.append(_op(OP_STREAM_WAIT, value=EV_START, stream=st))
+                started.add(x.src)
             c = x.round_idx
-            off = low.gather_off + x.src * R * row_bytes + c * b * ELT
-            ops.append(_op(OP_COPY, peer=x.src, src_buf=BUF_WS, dst_buf=BUF_WS, src_off=off, dst_off=off,
-                           src_par=low.gather_par, dst_par=low.gather_par, width=b * ELT, height=R,
-                           src_pitch=row_bytes, dst_pitch=row_bytes))
-            last_round = c
-        if last_round is not None:
-            ops.append(_op(OP_SIGNAL, flag=F_ROUND + last_round))
-    else:  # the three 1D fine-grain kinds
-        r = M // (G * G)
-        unfused = kind is ScheduleKind.HETERO_UNFUSED_1D
-        last_round = None
-        for x in xfers:
-            c = x.round_idx
-            if not unfused and last_round is not None and c != last_round:
-                ops.append(_op(OP_SIGNAL, flag=F_ROUND + last_round))
-            ops.append(pull(x.src, x.src * R + c * r, r))
-            if unfused:
-                ops.append(_op(OP_SIGNAL, flag=F_XFER + c * G + x.src))
-            last_round = c
-        if not unfused and last_round is not None:
-            ops.append(_op(OP_SIGNAL, flag=F_ROUND + last_round))
+            if kind is ScheduleKind.SERIAL:
+                ops.append(pull(x.src, x.src * R, R, st))
+            elif kind is ScheduleKind.UNIFORM_FUSED_2D:
+                b = K // G
+                off = low.gather_off + x.src * R * row_bytes + c * b * ELT
+                ops.append(_op(OP_COPY, peer=x.src, src_buf=BUF_WS, dst_buf=BUF_WS, src_off=off, dst_off=off,
+                               src_par=low.gather_par, dst_par=low.gather_par, width=b * ELT, height=R,
+                               src_pitch=row_bytes, dst_pitch=row_bytes, stream=st))
+            else:
+                r = M // (G * G)
+                ops.append(pull(x.src, x.src * R + c * r, r, st))
+            ops.append(_op(OP_SIGNAL, flag=F_XFER + c * G + x.src, stream=st))
 
-    # ---- tile program (mirrors this rank's GemmSpecs in plan order)
-    def rows_flag(start: int) -> int:
+    # ---- tile program: this rank's GemmSpecs in plan order, each fragment gated by the flags it reads
+    r_chunk = M // (G * G)
+
+    def gate(start: int) -> tuple[int, int, int, int]:
+        """(flag, nflag, kseg, kstride) for rows starting at `start` (one owner)."""
         owner = start // R
-        if owner == g:
-            return F_LOCAL
         if kind is ScheduleKind.SERIAL:
-            return F_ALL
+            return F_XFER, G, 0, 0                      # the whole gather (round 0 of every rank)
         if kind is ScheduleKind.SHARD_OVERLAP_P2P:
-            return F_RING + (g - owner) % G
-        c = (start - owner * R) // (M // (G * G))
-        if kind is ScheduleKind.HETERO_UNFUSED_1D:
-            return F_XFER + c * G + owner
-        return F_ROUND + c
+            return (F_LOCAL, 1, 0, 0) if owner == g else (F_RING + (g - owner) % G, 1, 0, 0)
+        if kind is ScheduleKind.UNIFORM_FUSED_2D:
+            return (F_LOCAL, 1, 0, 0) if owner == g else (F_XFER + owner, 1, kseg, G)
+        c = (start - owner * R) // r_chunk
+        if kind is ScheduleKind.UNIFORM_FUSED_1D:
+            return F_XFER + c * G, G, 0, 0              # the step waits for its whole round (gather)
+        if owner == g:
+            return F_LOCAL, 1, 0, 0                     # hetero: local shard runs at t = 0
+        if kind is ScheduleKind.HETERO_FUSED_1D:
+            return F_XFER + c * G, G, 0, 0              # one fused GEMM per round
+        return F_XFER + c * G + owner, 1, 0, 0          # unfused: exactly its own chunk
 
     Q = other_rows if gathered == "B" else None
     if gathered == "B" and Q is None:
         raise ValueError("gathered='B' needs other_rows (query rows)")
-    tiles = low.tiles
+    frag_lists = []
     for spec in _my_gemms(plan, g):
         if spec.col_block is not None:  # uniform_fused_2d: one output-stationary pass over all K
             if spec.col_block[0] != 0:
@@ -247,25 +281,30 @@ def lower_ag(plan: ExecutionPlan, rank: int, gathered: str = "A", alpha: float =
                     stop = min(end, (start // R + 1) * R)
                     frags.append((start, stop - start))
                     start = stop
-        for start, count in frags:
-            owner = start // R
-            if kind is ScheduleKind.UNIFORM_FUSED_2D:
-                flag, ks = (F_LOCAL, 0) if owner == g else (F_ROUND, kseg)
-            else:
-                flag, ks = rows_flag(start), 0
-            # split the fragment so that no tile straddles an owner (flag) boundary
-            if gathered == "A":
-                for m0 in range(start, start + count, TILE_M):
-                    rows = min(TILE_M, start + count - m0)
-                    for n0 in range(0, N, TILE_N):
-                        tiles.append(_tile(m0, n0, m0, n0, rows, min(TILE_N, N - n0), flag, ks))
-            else:
-                if count % 32:
-                    raise PlanError(f"gathered-B fragments must be multiples of 32 rows, got {count}")
-                for n0 in range(start, start + count, TILE_N):
-                    cols = min(TILE_N, start + count - n0)
-                    for m0 in range(0, Q, TILE_M):
-                        tiles.append(_tile(m0, n0, m0, n0, min(TILE_M, Q - m0), cols, flag, ks))
+        frag_lists.extend(frags)
+
+    def cdiv(a: int, b: int) -> int:
+        return -(-a // b)
+
+    if gathered == "A":
+        tn = choose_tile_n(lambda w: sum(cdiv(c, TILE_M) for _, c in frag_lists) * cdiv(N, w))
+    else:
+        tn = choose_tile_n(lambda w: sum(cdiv(c, w) for _, c in frag_lists) * cdiv(Q, TILE_M))
+    tiles = low.tiles
+    for start, count in frag_lists:
+        flag, nflag, ks, kstride = gate(start)
+        if gathered == "A":
+            for m0 in range(start, start + count, TILE_M):
+                rows = min(TILE_M, start + count - m0)
+                for n0 in range(0, N, tn):
+                    tiles.append(_tile(m0, n0, m0, n0, rows, min(tn, N - n0), flag, nflag, ks, kstride))
+        else:
+            if count % 32:
+                raise PlanError(f"gathered-B fragments must be multiples of 32 rows, got {count}")
+            for n0 in range(start, start + count, tn):
+                cols = min(tn, start + count - n0)
+                for m0 in range(0, Q, TILE_M):
+                    tiles.append(_tile(m0, n0, m0, n0, min(TILE_M, Q - m0), cols, flag, nflag, ks, kstride))
 
     d = low.desc
     gat = _operand(BUF_WS, M, K, low.gather_off, low.gather_par)
@@ -275,7 +314,7 @@ def lower_ag(plan: ExecutionPlan, rank: int, gathered: str = "A", alpha: float =
         d.a, d.b, d.c = _operand(BUF_A, Q, K), gat, _operand(BUF_C, Q, M)
     d.part = _operand(BUF_NONE, 0, 0)
     d.recv = _operand(BUF_NONE, 0, 0)
-    d.k, d.alpha, d.grid = K, alpha, grid
+    d.k, d.alpha, d.grid, d.tile_n = K, alpha, grid, tn
     low.notes = {"kind": kind.value, "rank": g, "world": G, "gathered": gathered}
     return low
 
@@ -287,7 +326,7 @@ def rs_plan(scenario: Scenario, kind: ScheduleKind) -> ExecutionPlan:
     return build_plan(scenario, kind)
 
 
-def lower_rs(scenario: Scenario, kind: ScheduleKind, rank: int, grid: int = 0) -> Lowered:
+def lower_rs(scenario: Scenario, kind: ScheduleKind, rank: int, grid: int = 0, virtual: bool = False) -> Lowered:
     """GEMM -> reduce-scatter (not in the reference, parity unpinned).
 
     Rank g holds A_g [M, Kg] and W_g [N, Kg]; P_g = A_g @ W_g^T [M, N]; rank q
@@ -306,7 +345,7 @@ def lower_rs(scenario: Scenario, kind: ScheduleKind, rank: int, grid: int = 0) -
     g, G = rank, scenario.n_gpus
     M, N, K = scenario.gemm.m, scenario.gemm.n, scenario.gemm.k
     _check_shape(M, N, K)
-    if G - 1 > MAX_RECV:
+    if G - 1 > MAX_RECV or G > MAX_WORLD:
         raise PlanError(f"at most {MAX_RECV + 1} ranks")
     R, r = M // G, M // (G * G)
     row_bytes = N * ELT
@@ -314,8 +353,8 @@ def lower_rs(scenario: Scenario, kind: ScheduleKind, rank: int, grid: int = 0) -
     part_off = FICCO_WS_DATA_OFFSET
     low.recv_off = part_off + M * row_bytes
     low.recv_slot = R * row_bytes
-    low.recv_par = (G - 1) * low.recv_slot
-    low.ws_bytes = low.recv_off + 2 * low.recv_par
+    low.recv_par = 0  # single buffer: a peer pushes run e only after our DONE(e), i.e. after run e-1 finished
+    low.ws_bytes = low.recv_off + (G - 1) * low.recv_slot
     ops, tiles = low.ops, low.tiles
     unfused = kind is ScheduleKind.HETERO_UNFUSED_1D
 
@@ -339,36 +378,44 @@ def lower_rs(scenario: Scenario, kind: ScheduleKind, rank: int, grid: int = 0) -
         order += [("own", g, c) for c in range(G)]
     unit_of = {qc: uid for uid, qcs in units for qc in qcs}
 
-    tiles_per_chunk = ((r + TILE_M - 1) // TILE_M) * ((N + TILE_N - 1) // TILE_N)
+    tn = choose_tile_n(lambda w: G * G * (-(-r // TILE_M)) * (-(-N // w)))
+    tiles_per_chunk = ((r + TILE_M - 1) // TILE_M) * ((N + tn - 1) // tn)
     for what, q, c in order:
         row0 = q * R + c * r
         for m0 in range(row0, row0 + r, TILE_M):
             rows = min(TILE_M, row0 + r - m0)
-            for n0 in range(0, N, TILE_N):
-                cols = min(TILE_N, N - n0)
+            for n0 in range(0, N, tn):
+                cols = min(tn, N - n0)
                 if what == "remote":
                     tiles.append(_tile(m0, n0, m0, n0, rows, cols, mode=EPI_STORE_SIGNAL, chunk=unit_of[(q, c)]))
                 else:
                     local = m0 - g * R
                     tiles.append(_tile(m0, n0, local, n0, rows, cols, mode=EPI_REDUCE, chunk=c, recv_row=local))
 
-    # copy program
-    for p in range(G):
-        if p != g:
-            ops.append(_op(OP_NOTIFY, peer=p, flag=F_DONE + g))
-    waited_done: set[int] = set()
+    # copy program. Stream 0: DONE barrier (every peer has started this run, so its
+    # receive slots are free), then one counter wait per push unit, each published as
+    # an event the owners' push chains (one per peer q) wait on before their copies.
+    if virtual:  # stand-in peers never push: their partials are pre-loaded, mark them landed
+        for c in range(G):
+            for j in range(G - 1):
+                ops.append(_op(OP_SIGNAL, flag=F_RS + c * (G - 1) + j, stream=0))
+    ops.append(_op(OP_BARRIER, flag=F_DONE, stream=0))
+    ops.append(_op(OP_RECORD, value=EV_START, stream=0))
+    for q in range(G):
+        if q != g:
+            ops.append(_op(OP_STREAM_WAIT, value=EV_START, stream=_peer_stream(q, g)))
     for uid, qcs in units:
-        ops.append(_op(OP_WAIT_COUNTER, flag=uid, value=tiles_per_chunk * len(qcs)))
+        slot = 1 + uid % 63
+        ops.append(_op(OP_WAIT_COUNTER, flag=uid, value=tiles_per_chunk * len(qcs), stream=0))
+        ops.append(_op(OP_RECORD, value=slot, stream=0))
         for q, c in qcs:
-            if q not in waited_done:
-                ops.append(_op(OP_WAIT, flag=F_DONE + q, value=1))
-                waited_done.add(q)
+            st = _peer_stream(q, g)
+            ops.append(_op(OP_STREAM_WAIT, value=slot, stream=st))
             src = part_off + (q * R + c * r) * row_bytes
             dst = low.recv_off + slot_of(g, q) * low.recv_slot + c * r * row_bytes
             ops.append(_op(OP_COPY, src_buf=BUF_WS, dst_buf=BUF_WS, dst_peer=q, src_off=src, dst_off=dst,
-                           dst_par=low.recv_par, width=r * row_bytes))
-        for q, c in qcs:
-            ops.append(_op(OP_NOTIFY, peer=q, flag=F_RS + c * (G - 1) + slot_of(g, q)))
+                           width=r * row_bytes, stream=st))
+            ops.append(_op(OP_NOTIFY, peer=q, flag=F_RS + c * (G - 1) + slot_of(g, q), stream=st))
 
     d = low.desc
     d.a, d.b = _operand(BUF_A, M, K), _operand(BUF_B, N, K)
@@ -377,10 +424,11 @@ def lower_rs(scenario: Scenario, kind: ScheduleKind, rank: int, grid: int = 0) -
     d.recv = _operand(BUF_WS, R, N, low.recv_off, low.recv_par)
     d.recv_slot, d.n_recv, d.rs_flag0 = low.recv_slot, G - 1, F_RS
     d.n_counters = len(units)
-    d.k, d.alpha, d.grid = K, 1.0, grid
+    d.k, d.alpha, d.grid, d.tile_n = K, 1.0, grid, tn
     if len(units) >= 4096 - 1:
         raise PlanError("too many push units")
+    if F_RS + G * (G - 1) >= 4096:
+        raise PlanError("too many ranks for the RS flag area")
     low.notes = {"kind": kind.value, "rank": g, "world": G, "op": "rs", "units": len(units),
                  "tiles_per_chunk": tiles_per_chunk}
-    assert FICCO_FLAG_COUNTERS > F_RS + G * (G - 1)
     return low

@@ -28,7 +28,7 @@ import math
 import torch
 
 from .domain import Collective, GemmShape, Parallelism, Scenario
-from .lowering import F_RS, Lowered, lower_ag, lower_rs
+from .lowering import Lowered, lower_ag, lower_rs
 from .machines import b200_machine
 from .routing import PlanError, ScheduleKind, build_plan
 from .runtime import FICCO_WS_DATA_OFFSET, Communicator, Plan
@@ -75,9 +75,6 @@ class FiccoGroup:
             self.comm.close()
         if self.virtual:
             self.comm = Communicator.virtual(self.world, self.rank, nbytes)
-            # peers never notify in virtual mode: pre-satisfy every receive flag
-            self.comm.set_flags(F_RS, 2048, 0x7FFFFFFF)
-            torch.cuda.synchronize()
         else:
             self.comm = Communicator.from_process_group(nbytes, self.pg)
         self._ws_bytes = nbytes
@@ -133,6 +130,8 @@ class FiccoGroup:
             for par in (0, 1):
                 off = low.recv_off + par * low.recv_par + j * low.recv_slot
                 self.ws_tensor(self.rank, off, (rows, cols)).copy_(part)
+                if not low.recv_par:
+                    break
 
 
 def _wrap_device_ptr(ptr: int, shape, dtype) -> torch.Tensor:
@@ -167,7 +166,7 @@ def prepare_rs(grp: FiccoGroup, M: int, K: int, N: int, kind=None):
     kd = choose_kind(sc, kind)
     if kd not in (ScheduleKind.UNIFORM_FUSED_1D, ScheduleKind.HETERO_FUSED_1D, ScheduleKind.HETERO_UNFUSED_1D):
         kd = ScheduleKind.HETERO_FUSED_1D  # the 2D/serial choices have no RS adjoint on this executor
-    plan, low = grp.plan(("rs", M, N, K, kd), lambda: lower_rs(sc, kd, grp.rank))
+    plan, low = grp.plan(("rs", M, N, K, kd), lambda: lower_rs(sc, kd, grp.rank, virtual=grp.virtual))
     return plan, low, kd
 
 
@@ -198,7 +197,7 @@ def all_gather_matmul(a_shard: torch.Tensor, weight: torch.Tensor, kind=None, gr
         out = torch.empty(M, N, dtype=torch.bfloat16, device=a_shard.device)
     plan.run(a_shard, weight, out, stream)
     if return_gathered:
-        par = grp.comm.epoch() & 1
+        par = (grp.comm.epoch() - 1) & 1  # parity of the run just enqueued
         gathered = grp.ws_tensor(grp.rank, low.gather_off + par * low.gather_par, (M, K))
         return out, gathered
     return out

@@ -23,13 +23,18 @@ LIB_PATH = pathlib.Path(__file__).resolve().parent / "libficco_b200.so"
 
 FICCO_WS_FLAG_WORDS = 16384
 FICCO_WS_DATA_OFFSET = FICCO_WS_FLAG_WORDS * 4
+FICCO_FLAG_BLOCK = 4096
+FICCO_FLAG_RUN_LOCAL = 256
 FICCO_FLAG_ABORT = FICCO_WS_FLAG_WORDS - 1
-FICCO_FLAG_COUNTERS = 12288
+FICCO_FLAG_COUNTERS = 2048  # block-relative
+FICCO_MAX_STREAMS = 16
 
-OP_COPY, OP_SIGNAL, OP_NOTIFY, OP_WAIT, OP_WAIT_COUNTER = 0, 1, 2, 3, 4
+OP_COPY, OP_SIGNAL, OP_NOTIFY, OP_WAIT, OP_WAIT_COUNTER, OP_BARRIER, OP_RECORD, OP_STREAM_WAIT = range(8)
+FICCO_MAX_EVENTS = 64
 BUF_NONE, BUF_A, BUF_B, BUF_C, BUF_WS = 0, 1, 2, 3, 4
 EPI_STORE, EPI_STORE_SIGNAL, EPI_REDUCE = 0, 1, 2
 TILE_M, TILE_N, TILE_K = 128, 256, 64
+TILE_WIDTHS = (256, 224, 192, 160, 128)
 MAX_RECV = 15
 
 EXPORTED = (
@@ -37,7 +42,7 @@ EXPORTED = (
     "ficco_ipc_handle_size", "ficco_ipc_get_handle", "ficco_ipc_open", "ficco_ipc_close",
     "ficco_comm_create", "ficco_comm_destroy", "ficco_comm_epoch", "ficco_comm_check", "ficco_comm_set_flags",
     "ficco_plan_create", "ficco_plan_destroy", "ficco_plan_run", "ficco_plan_run_parts",
-    "ficco_gemm_bf16", "ficco_copy_batch",
+    "ficco_gemm_bf16", "ficco_copy_batch", "ficco_plan_set_trace", "ficco_plan_info",
 )
 
 
@@ -46,13 +51,14 @@ class CopyOp(C.Structure):
                 ("dst_buf", C.c_int32), ("dst_peer", C.c_int32), ("src_off", C.c_int64), ("dst_off", C.c_int64),
                 ("src_par", C.c_int64), ("dst_par", C.c_int64), ("width", C.c_int64), ("height", C.c_int64),
                 ("src_pitch", C.c_int64), ("dst_pitch", C.c_int64), ("value", C.c_uint32),
-                ("reserved", C.c_uint32)]
+                ("stream", C.c_int32)]
 
 
 class Tile(C.Structure):
     _fields_ = [("a_row", C.c_int32), ("b_row", C.c_int32), ("c_row", C.c_int32), ("c_col", C.c_int32),
-                ("rows", C.c_int16), ("cols", C.c_int16), ("flag", C.c_int16), ("kseg", C.c_int16),
-                ("mode", C.c_int16), ("chunk", C.c_int16), ("recv_row", C.c_int32)]
+                ("recv_row", C.c_int32), ("rows", C.c_int16), ("cols", C.c_int16), ("flag", C.c_int16),
+                ("nflag", C.c_int16), ("kseg", C.c_int16), ("kstride", C.c_int16), ("mode", C.c_int16),
+                ("chunk", C.c_int16), ("reserved", C.c_int32)]
 
 
 class Operand(C.Structure):
@@ -65,10 +71,10 @@ class PlanDesc(C.Structure):
                 ("tiles", C.POINTER(Tile)), ("a", Operand), ("b", Operand), ("c", Operand), ("part", Operand),
                 ("recv", Operand), ("recv_slot", C.c_int64), ("k", C.c_int64), ("n_recv", C.c_int32),
                 ("rs_flag0", C.c_int32), ("n_counters", C.c_int32), ("grid", C.c_int32), ("alpha", C.c_float),
-                ("reserved", C.c_int32)]
+                ("tile_n", C.c_int32)]
 
 
-assert C.sizeof(CopyOp) == 96 and C.sizeof(Tile) == 32 and C.sizeof(Operand) == 40
+assert C.sizeof(CopyOp) == 96 and C.sizeof(Tile) == 40 and C.sizeof(Operand) == 40
 
 _lib = None
 _lock = threading.Lock()
@@ -106,6 +112,8 @@ def load_library(path: os.PathLike | str | None = None) -> C.CDLL:
             "ficco_plan_run_parts": ([vp, vp, vp, vp, vp, i32, i32], i32),
             "ficco_gemm_bf16": ([vp, vp, vp, i64, i64, i64, C.c_float, i32, vp], i32),
             "ficco_copy_batch": ([C.POINTER(vp), C.POINTER(vp), C.POINTER(sz), sz, vp], i32),
+            "ficco_plan_set_trace": ([vp, vp], i32),
+            "ficco_plan_info": ([vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)], i32),
         }
         for name, (args, res) in sig.items():
             fn = getattr(lib, name)
@@ -260,10 +268,28 @@ class Plan:
         self.handle, self.comm, self.desc = h.value, comm, desc
         self.n_ops, self.n_tiles = len(ops), len(tiles)
 
-    def run(self, a, b, c, stream=None, copies: bool = True, tiles: bool = True) -> None:
+    def run(self, a, b, c, stream=None) -> None:
+        """One execution replayed from the plan's CUDA graph (see ficco_plan_run)."""
+        ptr = lambda t: C.c_void_p(0 if t is None else t.data_ptr())  # noqa: E731
+        check(load_library().ficco_plan_run(C.c_void_p(self.handle), ptr(a), ptr(b), ptr(c),
+                                            C.c_void_p(_stream_ptr(stream))))
+
+    def run_parts(self, a, b, c, stream=None, copies: bool = True, tiles: bool = True) -> None:
+        """The same run enqueued directly on streams (no graph); halves selectable."""
         ptr = lambda t: C.c_void_p(0 if t is None else t.data_ptr())  # noqa: E731
         check(load_library().ficco_plan_run_parts(C.c_void_p(self.handle), ptr(a), ptr(b), ptr(c),
                                                   C.c_void_p(_stream_ptr(stream)), int(copies), int(tiles)))
+
+    def info(self) -> dict:
+        n, g, s = C.c_int(), C.c_int(), C.c_int()
+        check(load_library().ficco_plan_info(C.c_void_p(self.handle), C.byref(n), C.byref(g), C.byref(s)))
+        return {"tiles": n.value, "grid": g.value, "streams": s.value}
+
+    def set_trace(self, buf) -> None:
+        """Attach a device int64 tensor of >= grid + 2*tiles entries (None detaches)."""
+        self._trace = buf
+        check(load_library().ficco_plan_set_trace(C.c_void_p(self.handle),
+                                                  C.c_void_p(0 if buf is None else buf.data_ptr())))
 
     def close(self) -> None:
         if self.handle:

@@ -1,0 +1,81 @@
+"""Measured timeline of one FiCCO AG->GEMM run (C2, virtual 8 ranks): where does the time go?
+
+For every schedule kind: event-timed op latency, the tile kernel's span
+(first CTA start -> last tile stored, from %globaltimer stamps), and per
+dependency group (tiles sharing a readiness gate) when their loads could start
+and when their last tile was stored — i.e. when each round's chunks arrived
+relative to the compute.
+"""
+import json
+import os
+import statistics
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2512_10236_b200 import ops, runtime  # noqa: E402
+
+
+def main():
+    M, N, K, G = 8192, 3584, 4096, 8
+    if len(sys.argv) > 1:
+        M, N, K, G = map(int, sys.argv[1:5])
+    R = M // G
+    runtime.load_library()
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    shards = [(torch.rand(R, K, generator=gen, device="cuda") * 2 - 1).to(torch.bfloat16) for _ in range(G)]
+    w = (torch.randn(N, K, generator=gen, device="cuda") / K ** 0.5).to(torch.bfloat16)
+    out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    grp = ops.FiccoGroup.virtual_group(G, 0)
+    res = {}
+    for kind in ["serial", "shard_overlap_p2p", "uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d",
+                 "uniform_fused_2d"]:
+        plan, low, _ = ops.prepare_ag(grp, R, K, N, kind)
+        grp.load_peer_shards(low, shards)
+        info = plan.info()
+        trace = torch.zeros(info["grid"] + 2 * info["tiles"], dtype=torch.int64, device="cuda")
+        plan.set_trace(trace)
+        # stream (non-graph) path for comparison
+        ts_stream = []
+        for _ in range(10):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            plan.run_parts(shards[0], w, out)
+            b.record()
+            b.synchronize()
+            ts_stream.append(a.elapsed_time(b) * 1e3)
+        for _ in range(5):
+            ops.all_gather_matmul(shards[0], w, kind=kind, group=grp, out=out)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(10):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            ops.all_gather_matmul(shards[0], w, kind=kind, group=grp, out=out)
+            b.record()
+            b.synchronize()
+            ts.append(a.elapsed_time(b) * 1e3)
+        grp.comm.check()
+        tr = trace.cpu().tolist()
+        g = info["grid"]
+        t0 = min(tr[:g])
+        ready = [(tr[g + 2 * i] - t0) / 1e3 for i in range(info["tiles"])]
+        done = [(tr[g + 2 * i + 1] - t0) / 1e3 for i in range(info["tiles"])]
+        groups = {}
+        for i, t in enumerate(low.tiles):
+            key = f"flag{t.flag}x{t.nflag}" + (f"/k{t.kseg}" if t.kseg else "")
+            groups.setdefault(key, []).append(i)
+        per = {k: {"n": len(v), "ready_min": round(min(ready[i] for i in v), 1),
+                   "ready_med": round(statistics.median(ready[i] for i in v), 1),
+                   "done_max": round(max(done[i] for i in v), 1)} for k, v in groups.items()}
+        res[kind] = {"op_us": round(statistics.median(ts), 1), "op_us_streams": round(statistics.median(ts_stream), 1),
+                     "cta_start_spread_us": round((max(tr[:g]) - t0) / 1e3, 1),
+                     "kernel_span_us": round(max(done), 1), "groups": per}
+        plan.set_trace(None)
+    print(json.dumps(res, indent=1))
+    grp.close()
+
+
+if __name__ == "__main__":
+    main()
