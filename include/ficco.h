@@ -118,7 +118,7 @@ typedef struct {
   int32_t c_row;    /* first output row */
   int32_t c_col;    /* first output column */
   int32_t recv_row; /* REDUCE: row offset into every receive slot */
-  int16_t rows;     /* valid output rows (<= 128) */
+  int16_t rows;     /* valid output rows (<= 128; 0 = padding half of a CTA pair) */
   int16_t cols;     /* valid output columns (<= tile_n, multiple of 32) */
   int16_t flag;     /* first readiness flag gating the A/B loads (-1: none) */
   int16_t nflag;    /* consecutive flags [flag, flag+nflag) that must all be set (>= 1) */
@@ -155,7 +155,10 @@ typedef struct {
   int32_t n_counters; /* counters [0, n_counters) reset to 0 before each run */
   int32_t grid;       /* persistent CTAs (0: one per SM) */
   float alpha;        /* epilogue scale (STORE) */
-  int32_t tile_n;     /* tile width = B box rows: 128, 160, 192, 224 or 256 (0: 256) */
+  int32_t tile_n;     /* tile width (UMMA N): 128, 160, 192, 224 or 256 (0: 256) */
+  int32_t cta_group;  /* 1: one CTA per 128-row tile; 2: CTA pairs, tiles (2p, 2p+1) share b_row/c_col
+                         and form one 256-row UMMA (0: 1) */
+  int32_t reserved;
 } ficco_plan_desc;
 
 int ficco_abi_version(void);
@@ -206,6 +209,9 @@ int ficco_plan_info(ficco_plan_t* plan, int* n_tiles, int* grid, int* n_streams)
 /* stand-alone primitives (calibration, benchmarks) */
 int ficco_gemm_bf16(const void* a, const void* b, void* c, int64_t m, int64_t n, int64_t k, float alpha,
                     int grid, void* stream);
+/* tile_n 0 / cta_group 0: automatic (waves x width model, CTA pairs) */
+int ficco_gemm_bf16_cfg(const void* a, const void* b, void* c, int64_t m, int64_t n, int64_t k, float alpha,
+                        int grid, int tile_n, int cta_group, void* stream);
 int ficco_copy_batch(void* const* dsts, const void* const* srcs, const size_t* sizes, size_t count,
                      void* stream);
 

@@ -102,27 +102,27 @@ int encode_bf16_2d(Driver* drv, CUtensorMap* map, const void* base, int64_t rows
   return 0;
 }
 
-// Resolve the tile-width instantiation: kernel entry point and dynamic smem size.
-int kernel_for(int tn, const void** fn, int* smem) {
-  switch (tn) {
-#define FICCO_CASE(T)                                                  \
-  case T:                                                              \
-    *fn = reinterpret_cast<const void*>(ficco::tile_gemm_kernel<T>);   \
-    *smem = ficco::TileCfg<T>::SMEM_BYTES;                             \
-    return 0;
-    FICCO_FOR_EACH_TN(FICCO_CASE)
-#undef FICCO_CASE
-    default: return fail(FICCO_EINVAL, "unsupported tile width " + std::to_string(tn));
+// Resolve the (tile width, CTA group) instantiation: entry point, dynamic smem, B box rows.
+int kernel_for(int tn, int cg, const void** fn, int* smem, int* b_rows) {
+#define FICCO_CASE(T, G)                                                  \
+  if (tn == T && cg == G) {                                               \
+    *fn = reinterpret_cast<const void*>(ficco::tile_gemm_kernel<T, G>);   \
+    *smem = ficco::TileCfg<T, G>::SMEM_BYTES;                             \
+    *b_rows = ficco::TileCfg<T, G>::B_ROWS;                               \
+    return 0;                                                             \
   }
+  FICCO_FOR_EACH_CFG(FICCO_CASE)
+#undef FICCO_CASE
+  return fail(FICCO_EINVAL, "unsupported tile config " + std::to_string(tn) + "x" + std::to_string(cg));
 }
 
 int configure_kernels(int dev) {
   static int configured = -1;
   if (configured == dev) return 0;
-#define FICCO_CFG(T)                                                                              \
-  CK(cudaFuncSetAttribute(ficco::tile_gemm_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                          ficco::TileCfg<T>::SMEM_BYTES));
-  FICCO_FOR_EACH_TN(FICCO_CFG)
+#define FICCO_CFG(T, G)                                                                              \
+  CK(cudaFuncSetAttribute(ficco::tile_gemm_kernel<T, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                          ficco::TileCfg<T, G>::SMEM_BYTES));
+  FICCO_FOR_EACH_CFG(FICCO_CFG)
 #undef FICCO_CFG
   configured = dev;
   return 0;
@@ -165,7 +165,8 @@ struct ficco_plan {
   cudaGraphNode_t captured_kernel = nullptr;
   std::vector<std::pair<cudaGraphNode_t, int>> captured_copies;  // (node, op index) touching call arguments
   unsigned long long* trace = nullptr;  // optional device timeline buffer
-  int tile_n = 256;                     // B box rows = tile width (kernel instantiation)
+  int tile_n = 256;                     // tile width (UMMA N)
+  int cta_group = 1;                    // 1: one CTA per tile; 2: CTA pair (cluster of 2, UMMA M = 256)
   ficco_plan_desc desc{};
   GraphInst graph[2];
 };
@@ -317,7 +318,12 @@ int make_params(ficco_plan* p, uint32_t parity, const void* a, const void* b, vo
   if ((r = resolve(cm, parity, d.a.buf, -1, d.a.off, d.a.par, a, b, c, &pa))) return r;
   if ((r = resolve(cm, parity, d.b.buf, -1, d.b.off, d.b.par, a, b, c, &pb))) return r;
   if ((r = encode_bf16_2d(cm->drv, &prm->tmap_a, pa, d.a.rows, d.k, d.a.ld, ficco::BM))) return r;
-  if ((r = encode_bf16_2d(cm->drv, &prm->tmap_b, pb, d.b.rows, d.k, d.b.ld, p->tile_n))) return r;
+  {
+    const void* fn;
+    int smem, b_rows;
+    if ((r = kernel_for(p->tile_n, p->cta_group, &fn, &smem, &b_rows))) return r;
+    if ((r = encode_bf16_2d(cm->drv, &prm->tmap_b, pb, d.b.rows, d.k, d.b.ld, b_rows))) return r;
+  }
   uint8_t* po = nullptr;
   if (d.c.buf != FICCO_BUF_NONE && (r = resolve(cm, parity, d.c.buf, -1, d.c.off, d.c.par, a, b, c, &po))) return r;
   uint8_t* pp = nullptr;
@@ -347,6 +353,7 @@ int make_params(ficco_plan* p, uint32_t parity, const void* a, const void* b, vo
   prm->trace = p->trace;
   int g = d.grid > 0 ? d.grid : cm->sms;
   if (g > p->n_tiles) g = p->n_tiles;
+  if (p->cta_group == 2) g &= ~1;  // whole clusters
   *grid = g;
   return 0;
 }
@@ -356,12 +363,24 @@ int launch_tiles(ficco_plan* p, uint32_t parity, const void* a, const void* b, v
   int r = configure_kernels(p->comm->device);
   if (r) return r;
   ficco::TileParams prm;
-  int grid, smem;
+  int grid, smem, b_rows;
   const void* fn;
-  if ((r = kernel_for(p->tile_n, &fn, &smem))) return r;
+  if ((r = kernel_for(p->tile_n, p->cta_group, &fn, &smem, &b_rows))) return r;
   if ((r = make_params(p, parity, a, b, c, &prm, &grid))) return r;
   void* args[] = {&prm};
-  CK(cudaLaunchKernel(fn, dim3(grid), dim3(ficco::NUM_THREADS), args, size_t(smem), s));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(ficco::NUM_THREADS);
+  cfg.dynamicSmemBytes = size_t(smem);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = unsigned(p->cta_group);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelExC(&cfg, fn, args));
   cudaStreamCaptureStatus st;
   CK(cudaStreamIsCapturing(s, &st));
   if (st == cudaStreamCaptureStatusActive) {  // remember the kernel node so later runs can re-point it
@@ -418,8 +437,8 @@ int repoint_graph(ficco_plan* p, uint32_t parity, const void* a, const void* b, 
     if (r) return r;
     void* args[] = {&prm};
     const void* fn;
-    int smem;
-    if ((r = kernel_for(p->tile_n, &fn, &smem))) return r;
+    int smem, b_rows;
+    if ((r = kernel_for(p->tile_n, p->cta_group, &fn, &smem, &b_rows))) return r;
     cudaKernelNodeParams kp{};
     kp.func = const_cast<void*>(fn);
     kp.gridDim = dim3(grid);
@@ -579,15 +598,18 @@ int ficco_plan_create(ficco_comm_t* c, const ficco_plan_desc* d, ficco_plan_t** 
   if (d->n_counters < 0 || FICCO_FLAG_COUNTERS + d->n_counters > FICCO_FLAG_BLOCK)
     return fail(FICCO_EINVAL, "too many counters");
   const int tile_n = d->tile_n > 0 ? d->tile_n : 256;
+  const int cta_group = d->cta_group > 0 ? d->cta_group : 1;
   {
     const void* fn;
-    int smem;
-    int r = kernel_for(tile_n, &fn, &smem);
+    int smem, b_rows;
+    int r = kernel_for(tile_n, cta_group, &fn, &smem, &b_rows);
     if (r) return r;
+    if (cta_group == 2 && d->n_tiles % 2) return fail(FICCO_EINVAL, "cta_group 2 needs an even tile list (pairs)");
   }
   for (int i = 0; i < d->n_tiles; ++i) {
     const ficco_tile& t = d->tiles[i];
-    if (t.rows < 1 || t.rows > ficco::BM || t.cols < 32 || t.cols > tile_n || t.cols % 32)
+    if (t.rows < 0 || t.rows > ficco::BM || (t.rows == 0 && cta_group == 1) || t.cols < 32 || t.cols > tile_n ||
+        t.cols % 32)
       return fail(FICCO_EINVAL, "tile " + std::to_string(i) + ": rows/cols out of range");
     if (t.mode < FICCO_EPI_STORE || t.mode > FICCO_EPI_REDUCE)
       return fail(FICCO_EINVAL, "tile " + std::to_string(i) + ": bad epilogue mode");
@@ -617,6 +639,8 @@ int ficco_plan_create(ficco_comm_t* c, const ficco_plan_desc* d, ficco_plan_t** 
   p->desc.tiles = nullptr;
   p->n_tiles = d->n_tiles;
   p->tile_n = tile_n;
+  p->cta_group = cta_group;
+  if (cta_group == 2 && p->desc.grid % 2) p->desc.grid = p->desc.grid > 1 ? p->desc.grid - 1 : 2;  // whole pairs
   p->n_streams = n_streams;
   p->user_copies = user;
   if (d->n_tiles > 0) {
@@ -701,16 +725,18 @@ int ficco_copy_batch(void* const* dsts, const void* const* srcs, const size_t* s
   return 0;
 }
 
-int ficco_gemm_bf16(const void* a, const void* b, void* c, int64_t m, int64_t n, int64_t k, float alpha, int grid,
-                    void* stream) {
-  // Plain C = alpha * A @ B^T through the same tile kernel (no flags), cached per shape.
+int ficco_gemm_bf16_cfg(const void* a, const void* b, void* c, int64_t m, int64_t n, int64_t k, float alpha,
+                        int grid, int tile_n, int cta_group, void* stream) {
+  // Plain C = alpha * A @ B^T through the same tile kernel (no flags), cached per shape/config.
   if (m <= 0 || n <= 0 || k <= 0 || n % 32 || k % 8) return fail(FICCO_EINVAL, "gemm: need N%32==0, K%8==0");
+  if (cta_group == 0) cta_group = 2;
+  if (cta_group != 1 && cta_group != 2) return fail(FICCO_EINVAL, "cta_group must be 1 or 2");
   static std::mutex mu;
-  static std::map<std::tuple<int64_t, int64_t, int, int>, std::pair<ficco_comm*, ficco_plan*>> cache;
+  static std::map<std::tuple<int64_t, int64_t, int, int, int, int>, std::pair<ficco_comm*, ficco_plan*>> cache;
   std::lock_guard<std::mutex> lock(mu);
   int dev;
   CK(cudaGetDevice(&dev));
-  auto key = std::make_tuple(m, n, grid, dev);
+  auto key = std::make_tuple(m, n, grid, dev, tile_n, cta_group);
   auto it = cache.find(key);
   if (it == cache.end()) {
     static std::map<int, void*> ws_by_dev;
@@ -724,34 +750,40 @@ int ficco_gemm_bf16(const void* a, const void* b, void* c, int64_t m, int64_t n,
     void* w = ws_by_dev[dev];
     int r = ficco_comm_create(0, 1, &w, FICCO_WS_DATA_OFFSET, 1, &cm);
     if (r) return r;
-    // tile width minimising (waves x width) over the instantiated widths
-    int tn = 256;
-    double best = 1e30;
-    const int widths[] = {256, 224, 192, 160, 128};
-    for (int w : widths) {
-      const int64_t tiles_n = (n + w - 1) / w, tiles_m = (m + ficco::BM - 1) / ficco::BM;
-      const int64_t waves = (tiles_n * tiles_m + cm->sms - 1) / cm->sms;
-      const double cost = double(waves) * w * (1.0 + 0.02 * (256.0 / w));  // small per-tile overhead term
-      if (cost < best - 1e-9) {
-        best = cost;
-        tn = w;
+    int tn = tile_n;
+    if (tn == 0) {  // tile width minimising (waves x width) over the instantiated widths
+      double best = 1e30;
+      const int widths[] = {256, 224, 192, 160, 128};
+      const int units = cm->sms / cta_group;
+      for (int wdt : widths) {
+        const int64_t tiles_n = (n + wdt - 1) / wdt;
+        const int64_t tiles_m = ((m + ficco::BM - 1) / ficco::BM + cta_group - 1) / cta_group;
+        const int64_t waves = (tiles_n * tiles_m + units - 1) / units;
+        const double cost = double(waves) * wdt * (1.0 + 0.02 * (256.0 / wdt));
+        if (cost < best - 1e-9) {
+          best = cost;
+          tn = wdt;
+        }
       }
     }
     std::vector<ficco_tile> tiles;
-    for (int64_t i = 0; i < m; i += ficco::BM)
-      for (int64_t j = 0; j < n; j += tn) {
-        ficco_tile t{};
-        t.a_row = int32_t(i);
-        t.b_row = int32_t(j);
-        t.c_row = int32_t(i);
-        t.c_col = int32_t(j);
-        t.rows = int16_t(m - i < ficco::BM ? m - i : ficco::BM);
-        t.cols = int16_t(n - j < tn ? n - j : tn);
-        t.flag = -1;
-        t.nflag = 0;
-        t.mode = FICCO_EPI_STORE;
-        tiles.push_back(t);
-      }
+    const int64_t mstep = int64_t(ficco::BM) * cta_group;
+    for (int64_t i = 0; i < m; i += mstep)
+      for (int64_t j = 0; j < n; j += tn)
+        for (int h = 0; h < cta_group; ++h) {
+          const int64_t row = i + h * ficco::BM;
+          ficco_tile t{};
+          t.a_row = int32_t(row < m ? row : i);
+          t.b_row = int32_t(j);
+          t.c_row = int32_t(row);
+          t.c_col = int32_t(j);
+          t.rows = int16_t(row >= m ? 0 : (m - row < ficco::BM ? m - row : ficco::BM));
+          t.cols = int16_t(n - j < tn ? n - j : tn);
+          t.flag = -1;
+          t.nflag = 0;
+          t.mode = FICCO_EPI_STORE;
+          tiles.push_back(t);
+        }
     ficco_plan_desc d{};
     d.n_tiles = int32_t(tiles.size());
     d.tiles = tiles.data();
@@ -759,6 +791,7 @@ int ficco_gemm_bf16(const void* a, const void* b, void* c, int64_t m, int64_t n,
     d.alpha = 1.0f;
     d.k = k;
     d.tile_n = tn;
+    d.cta_group = cta_group;
     ficco_plan* p;
     if ((r = ficco_plan_create(cm, &d, &p))) return r;
     it = cache.emplace(key, std::make_pair(cm, p)).first;
@@ -770,6 +803,11 @@ int ficco_gemm_bf16(const void* a, const void* b, void* c, int64_t m, int64_t n,
   p->desc.k = k;
   p->desc.alpha = alpha;
   return ficco_plan_run_parts(p, a, b, c, stream, 0, 1);  // no flags: direct launch
+}
+
+int ficco_gemm_bf16(const void* a, const void* b, void* c, int64_t m, int64_t n, int64_t k, float alpha, int grid,
+                    void* stream) {
+  return ficco_gemm_bf16_cfg(a, b, c, m, n, k, alpha, grid, 0, 0, stream);
 }
 
 }  // extern "C"

@@ -1,7 +1,13 @@
 // Persistent, flag-gated tcgen05 tile kernel: the compute half of every FiCCO schedule.
 //
 // One CTA per SM walks a host-lowered tile list (ficco_tile) in order; tile t
-// goes to CTA t mod gridDim.x. Warp roles (192 threads):
+// goes to CTA t mod gridDim.x. With CG = 2 (cta_group::2) the CTAs of a
+// cluster pair process tiles 2p (leader, even CTA) and 2p+1 together as one
+// 256 x TN MMA tile: each CTA TMA-loads its own 128 A rows and half of the B
+// rows, the leader issues tcgen05.mma.cta_group::2 over both CTAs' shared
+// memory, and each CTA's epilogue drains its own TMEM half. The two halves
+// may come from different (non-adjacent) row fragments — e.g. fine chunks of
+// two different peers — since A rows are loaded per CTA. Warp roles (192 threads):
 //   warp 0      TMA producer: waits the tile's readiness flag(s) (written by
 //               copy-engine stream memops or by peers), then streams 128x64 A
 //               and 256x64 B boxes (128B swizzle) into a STAGES-deep ring.
@@ -28,7 +34,7 @@
 
 namespace ficco {
 
-constexpr int BM = 128;
+constexpr int BM = 128;      // rows per CTA (UMMA M = 128 * CG)
 constexpr int BN_MAX = 256;  // widest tile (UMMA N <= 256); per-plan tile width TN in {128,...,256}
 constexpr int BK = 64;       // 64 bf16 = 128 B = one swizzle row
 constexpr int UMMA_K = 16;
@@ -40,13 +46,16 @@ constexpr int MAX_RECV = 15;
 constexpr uint32_t SPIN_LIMIT = 1u << 25;  // ~4-10 s of polling before declaring a timeout
 constexpr int SMEM_LIMIT = 227 * 1024;
 
-// Per tile-width configuration: as many pipeline stages as fit in shared memory.
-template <int TN>
+// Per (tile width, CTA group) configuration: as many pipeline stages as fit.
+template <int TN, int CG>
 struct TileCfg {
   static_assert(TN % 32 == 0 && TN >= 64 && TN <= 256, "tile width");
-  static constexpr int B_STAGE = TN * BK * 2;
+  static_assert(CG == 1 || CG == 2, "cta group");
+  static constexpr int B_ROWS = TN / CG;  // B rows loaded by each CTA
+  static constexpr int B_STAGE = B_ROWS * BK * 2;
   static constexpr int STAGE = A_STAGE + B_STAGE;
-  static constexpr int STAGES = (SMEM_LIMIT - 1024 - 256) / STAGE > 6 ? 6 : (SMEM_LIMIT - 1024 - 256) / STAGE;
+  static constexpr int MAX_STAGES = (SMEM_LIMIT - 1024 - 256) / STAGE;
+  static constexpr int STAGES = MAX_STAGES > 8 ? 8 : MAX_STAGES;
   static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE + 256;
 };
 
@@ -97,15 +106,16 @@ __device__ __forceinline__ void wait_flag(const uint32_t* f, uint32_t epoch, uin
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-template <int TN>
+template <int TN, int CG>
 __device__ __forceinline__ void producer_loop(const TileParams& p, uint8_t* sA, uint8_t* sB, uint64_t* full,
-                                              uint64_t* empty) {
-  using Cfg = TileCfg<TN>;
+                                              uint64_t* empty, uint32_t rank) {
+  using Cfg = TileCfg<TN, CG>;
   const uint64_t hint_a = policy_evict_first();
   const uint64_t hint_b = policy_evict_last();
   uint32_t stage = 0, phase = 0;
   for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
     const ficco_tile td = p.tiles[t];
+    const int b_row = td.b_row + int(rank) * Cfg::B_ROWS;
     for (int kb = 0; kb < p.num_kb; ++kb) {
       if (td.flag >= 0) {
         if (td.kseg == 0) {
@@ -118,9 +128,16 @@ __device__ __forceinline__ void producer_loop(const TileParams& p, uint8_t* sA, 
       }
       if (kb == 0 && p.trace) p.trace[gridDim.x + 2 * t] = globaltimer();
       mbar_wait(&empty[stage], phase ^ 1u);
-      mbar_arrive_expect_tx(&full[stage], Cfg::STAGE);
-      tma_load_2d(sA + stage * A_STAGE, &p.tmap_a, &full[stage], kb * BK, td.a_row, hint_a);
-      tma_load_2d(sB + stage * Cfg::B_STAGE, &p.tmap_b, &full[stage], kb * BK, td.b_row, hint_b);
+      if constexpr (CG == 1) {
+        mbar_arrive_expect_tx(&full[stage], Cfg::STAGE);
+        tma_load_2d(sA + stage * A_STAGE, &p.tmap_a, &full[stage], kb * BK, td.a_row, hint_a);
+        tma_load_2d(sB + stage * Cfg::B_STAGE, &p.tmap_b, &full[stage], kb * BK, b_row, hint_b);
+      } else {
+        // both CTAs' bytes complete on the leader's barrier; the leader arms it for the pair
+        if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE);
+        tma_load_2d_pair(sA + stage * A_STAGE, &p.tmap_a, &full[stage], kb * BK, td.a_row, hint_a);
+        tma_load_2d_pair(sB + stage * Cfg::B_STAGE, &p.tmap_b, &full[stage], kb * BK, b_row, hint_b);
+      }
       if (++stage == Cfg::STAGES) {
         stage = 0;
         phase ^= 1u;
@@ -129,11 +146,11 @@ __device__ __forceinline__ void producer_loop(const TileParams& p, uint8_t* sA, 
   }
 }
 
-template <int TN>
+template <int TN, int CG>
 __device__ __forceinline__ void mma_loop(const TileParams& p, uint8_t* sA, uint8_t* sB, uint64_t* full,
                                          uint64_t* empty, uint64_t* tfull, uint64_t* tempty, uint32_t tmem) {
-  using Cfg = TileCfg<TN>;
-  constexpr uint32_t idesc = make_idesc_bf16(BM, TN);
+  using Cfg = TileCfg<TN, CG>;
+  constexpr uint32_t idesc = make_idesc_bf16(BM * CG, TN);
   uint32_t stage = 0, phase = 0, it = 0;
   for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
     const uint32_t acc = it & 1u;
@@ -148,19 +165,28 @@ __device__ __forceinline__ void mma_loop(const TileParams& p, uint8_t* sA, uint8
 #pragma unroll
       for (int k = 0; k < BK / UMMA_K; ++k) {
         // +32 bytes per K step inside the 128B swizzle row (>>4 in the descriptor)
-        umma_bf16(d, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc, (kb | k) != 0);
+        if constexpr (CG == 1)
+          umma_bf16(d, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc, (kb | k) != 0);
+        else
+          umma_bf16_pair(d, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc, (kb | k) != 0);
       }
-      umma_commit(&empty[stage]);  // smem slot free once these MMAs retire
+      if constexpr (CG == 1)
+        umma_commit(&empty[stage]);  // smem slot free once these MMAs retire
+      else
+        umma_commit_pair(&empty[stage]);  // ... in both CTAs of the pair
       if (++stage == Cfg::STAGES) {
         stage = 0;
         phase ^= 1u;
       }
     }
-    umma_commit(&tfull[acc]);  // accumulator complete
+    if constexpr (CG == 1)
+      umma_commit(&tfull[acc]);  // accumulator complete
+    else
+      umma_commit_pair(&tfull[acc]);
   }
 }
 
-template <int TN>
+template <int TN, int CG>
 __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfull, uint64_t* tempty,
                                               uint32_t tmem) {
   const int warp = threadIdx.x / 32;
@@ -227,7 +253,10 @@ __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfu
       }
     }
     tc_fence_before();
-    mbar_arrive(&tempty[acc]);
+    if constexpr (CG == 1)
+      mbar_arrive(&tempty[acc]);
+    else
+      mbar_arrive_leader(&tempty[acc]);  // the leader's MMA reuses the pair's accumulator
     if (p.trace && threadIdx.x == 64) p.trace[gridDim.x + 2 * t + 1] = globaltimer();
     if (td.mode == FICCO_EPI_STORE_SIGNAL) {
       named_bar_sync(1, EPI_THREADS);  // every row of the tile is stored
@@ -239,9 +268,9 @@ __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfu
   }
 }
 
-template <int TN>
+template <int TN, int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1) tile_gemm_kernel(const __grid_constant__ TileParams p) {
-  using Cfg = TileCfg<TN>;
+  using Cfg = TileCfg<TN, CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = base;
@@ -254,6 +283,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tile_gemm_kernel(const __grid_
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
   if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x] = globaltimer();
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&p.tmap_a);
@@ -264,31 +294,48 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tile_gemm_kernel(const __grid_
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], EPI_THREADS);
+      mbar_init(&tempty[a], EPI_THREADS * CG);
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
+  if (warp == 1) {
+    if constexpr (CG == 1)
+      tmem_alloc(tmem_slot, TMEM_COLS);
+    else
+      tmem_alloc_pair(tmem_slot, TMEM_COLS);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 1)
+    __syncthreads();
+  else
+    cluster_sync();  // peer barriers initialised before any remote arrive / TMA complete_tx
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) producer_loop<TN>(p, sA, sB, full, empty);
+    if (lane == 0) producer_loop<TN, CG>(p, sA, sB, full, empty, rank);
   } else if (warp == 1) {
-    if (lane == 0) mma_loop<TN>(p, sA, sB, full, empty, tfull, tempty, tmem);
+    if (lane == 0 && rank == 0) mma_loop<TN, CG>(p, sA, sB, full, empty, tfull, tempty, tmem);
   } else {
-    epilogue_loop<TN>(p, tfull, tempty, tmem);
+    epilogue_loop<TN, CG>(p, tfull, tempty, tmem);
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 1)
+    __syncthreads();
+  else
+    cluster_sync();
   tc_fence_after();
-  if (warp == 1) tmem_dealloc(tmem, TMEM_COLS);
+  if (warp == 1) {
+    if constexpr (CG == 1)
+      tmem_dealloc(tmem, TMEM_COLS);
+    else
+      tmem_dealloc_pair(tmem, TMEM_COLS);
+  }
 }
 
-// Tile widths instantiated for the per-plan choice (see lowering.choose_tile_n).
-#define FICCO_FOR_EACH_TN(X) X(128) X(160) X(192) X(224) X(256)
+// (tile width, CTA group) instantiations for the per-plan choice (see lowering.choose_tile_n).
+#define FICCO_FOR_EACH_CFG(X) \
+  X(128, 1) X(160, 1) X(192, 1) X(224, 1) X(256, 1) X(128, 2) X(160, 2) X(192, 2) X(224, 2) X(256, 2)
 
 }  // namespace ficco

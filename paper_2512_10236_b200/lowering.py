@@ -114,6 +114,35 @@ def _tile(a_row, b_row, c_row, c_col, rows, cols, flag=-1, nflag=0, kseg=0, kstr
 B200_SMS = 148
 
 
+DEFAULT_CTA_GROUP = 2
+
+
+def pair_tiles(tiles: list[Tile]) -> list[Tile]:
+    """Re-order a 128-row tile list into CTA pairs (cta_group::2).
+
+    Tiles (2p, 2p+1) of the result share b_row / c_col / cols (one 256 x TN
+    UMMA over two independent 128-row A pieces); a tile is emitted with the next
+    tile of the same column range, so the order stays close to plan order.
+    Unmatched tiles get a padding partner (rows = 0: loads, no stores/signals)
+    that inherits the partner's readiness gates: each CTA of a pair loads half
+    of the B rows, so B-side gates (CP: the gathered K rows) bind both CTAs.
+    """
+    pending: dict[tuple, Tile] = {}
+    out: list[Tile] = []
+    for t in tiles:
+        key = (t.b_row, t.c_col, t.cols)
+        mate = pending.pop(key, None)
+        if mate is None:
+            pending[key] = t
+        else:
+            out += [mate, t]
+    for t in pending.values():
+        # the padding CTA still loads half of B, so it must honour the same gates
+        pad = _tile(t.a_row, t.b_row, t.c_row, t.c_col, 0, t.cols, t.flag, t.nflag, t.kseg, t.kstride)
+        out += [t, pad]
+    return out
+
+
 def choose_tile_n(tiles_for_width, sms: int = B200_SMS) -> int:
     """Tile width (UMMA N, B box rows) minimising persistent-kernel waves x width.
 
@@ -166,7 +195,7 @@ def _peer_stream(p: int, g: int) -> int:
 
 
 def lower_ag(plan: ExecutionPlan, rank: int, gathered: str = "A", alpha: float = 1.0, grid: int = 0,
-             other_rows: int | None = None) -> Lowered:
+             other_rows: int | None = None, cta_group: int = DEFAULT_CTA_GROUP) -> Lowered:
     """All-gather -> GEMM family (AG->GEMM and the CP KV-gather -> QK^T).
 
     gathered="A": C[M,N] = A_all[M,K] @ W[N,K]^T; call args (a=A_shard[R,K], b=W, c=C).
@@ -286,10 +315,13 @@ def lower_ag(plan: ExecutionPlan, rank: int, gathered: str = "A", alpha: float =
     def cdiv(a: int, b: int) -> int:
         return -(-a // b)
 
+    units = B200_SMS // cta_group
     if gathered == "A":
-        tn = choose_tile_n(lambda w: sum(cdiv(c, TILE_M) for _, c in frag_lists) * cdiv(N, w))
+        tn = choose_tile_n(lambda w: cdiv(sum(cdiv(c, TILE_M) for _, c in frag_lists), cta_group) * cdiv(N, w),
+                           units)
     else:
-        tn = choose_tile_n(lambda w: sum(cdiv(c, w) for _, c in frag_lists) * cdiv(Q, TILE_M))
+        tn = choose_tile_n(lambda w: sum(cdiv(c, w) for _, c in frag_lists) * cdiv(cdiv(Q, TILE_M), cta_group),
+                           units)
     tiles = low.tiles
     for start, count in frag_lists:
         flag, nflag, ks, kstride = gate(start)
@@ -306,6 +338,8 @@ def lower_ag(plan: ExecutionPlan, rank: int, gathered: str = "A", alpha: float =
                 for m0 in range(0, Q, TILE_M):
                     tiles.append(_tile(m0, n0, m0, n0, min(TILE_M, Q - m0), cols, flag, nflag, ks, kstride))
 
+    if cta_group == 2:
+        low.tiles[:] = pair_tiles(low.tiles)
     d = low.desc
     gat = _operand(BUF_WS, M, K, low.gather_off, low.gather_par)
     if gathered == "A":
@@ -314,7 +348,7 @@ def lower_ag(plan: ExecutionPlan, rank: int, gathered: str = "A", alpha: float =
         d.a, d.b, d.c = _operand(BUF_A, Q, K), gat, _operand(BUF_C, Q, M)
     d.part = _operand(BUF_NONE, 0, 0)
     d.recv = _operand(BUF_NONE, 0, 0)
-    d.k, d.alpha, d.grid, d.tile_n = K, alpha, grid, tn
+    d.k, d.alpha, d.grid, d.tile_n, d.cta_group = K, alpha, grid, tn, cta_group
     low.notes = {"kind": kind.value, "rank": g, "world": G, "gathered": gathered}
     return low
 
@@ -326,7 +360,8 @@ def rs_plan(scenario: Scenario, kind: ScheduleKind) -> ExecutionPlan:
     return build_plan(scenario, kind)
 
 
-def lower_rs(scenario: Scenario, kind: ScheduleKind, rank: int, grid: int = 0, virtual: bool = False) -> Lowered:
+def lower_rs(scenario: Scenario, kind: ScheduleKind, rank: int, grid: int = 0, virtual: bool = False,
+             cta_group: int = DEFAULT_CTA_GROUP) -> Lowered:
     """GEMM -> reduce-scatter (not in the reference, parity unpinned).
 
     Rank g holds A_g [M, Kg] and W_g [N, Kg]; P_g = A_g @ W_g^T [M, N]; rank q
@@ -378,7 +413,7 @@ def lower_rs(scenario: Scenario, kind: ScheduleKind, rank: int, grid: int = 0, v
         order += [("own", g, c) for c in range(G)]
     unit_of = {qc: uid for uid, qcs in units for qc in qcs}
 
-    tn = choose_tile_n(lambda w: G * G * (-(-r // TILE_M)) * (-(-N // w)))
+    tn = choose_tile_n(lambda w: -(-(G * G * (-(-r // TILE_M))) // cta_group) * (-(-N // w)), B200_SMS // cta_group)
     tiles_per_chunk = ((r + TILE_M - 1) // TILE_M) * ((N + tn - 1) // tn)
     for what, q, c in order:
         row0 = q * R + c * r
@@ -391,6 +426,9 @@ def lower_rs(scenario: Scenario, kind: ScheduleKind, rank: int, grid: int = 0, v
                 else:
                     local = m0 - g * R
                     tiles.append(_tile(m0, n0, local, n0, rows, cols, mode=EPI_REDUCE, chunk=c, recv_row=local))
+
+    if cta_group == 2:
+        tiles[:] = pair_tiles(tiles)
 
     # copy program. Stream 0: DONE barrier (every peer has started this run, so its
     # receive slots are free), then one counter wait per push unit, each published as
@@ -424,7 +462,7 @@ def lower_rs(scenario: Scenario, kind: ScheduleKind, rank: int, grid: int = 0, v
     d.recv = _operand(BUF_WS, R, N, low.recv_off, low.recv_par)
     d.recv_slot, d.n_recv, d.rs_flag0 = low.recv_slot, G - 1, F_RS
     d.n_counters = len(units)
-    d.k, d.alpha, d.grid, d.tile_n = K, 1.0, grid, tn
+    d.k, d.alpha, d.grid, d.tile_n, d.cta_group = K, 1.0, grid, tn, cta_group
     if len(units) >= 4096 - 1:
         raise PlanError("too many push units")
     if F_RS + G * (G - 1) >= 4096:

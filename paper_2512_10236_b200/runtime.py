@@ -42,7 +42,7 @@ EXPORTED = (
     "ficco_ipc_handle_size", "ficco_ipc_get_handle", "ficco_ipc_open", "ficco_ipc_close",
     "ficco_comm_create", "ficco_comm_destroy", "ficco_comm_epoch", "ficco_comm_check", "ficco_comm_set_flags",
     "ficco_plan_create", "ficco_plan_destroy", "ficco_plan_run", "ficco_plan_run_parts",
-    "ficco_gemm_bf16", "ficco_copy_batch", "ficco_plan_set_trace", "ficco_plan_info",
+    "ficco_gemm_bf16", "ficco_copy_batch", "ficco_plan_set_trace", "ficco_plan_info", "ficco_gemm_bf16_cfg",
 )
 
 
@@ -71,7 +71,7 @@ class PlanDesc(C.Structure):
                 ("tiles", C.POINTER(Tile)), ("a", Operand), ("b", Operand), ("c", Operand), ("part", Operand),
                 ("recv", Operand), ("recv_slot", C.c_int64), ("k", C.c_int64), ("n_recv", C.c_int32),
                 ("rs_flag0", C.c_int32), ("n_counters", C.c_int32), ("grid", C.c_int32), ("alpha", C.c_float),
-                ("tile_n", C.c_int32)]
+                ("tile_n", C.c_int32), ("cta_group", C.c_int32), ("reserved", C.c_int32)]
 
 
 assert C.sizeof(CopyOp) == 96 and C.sizeof(Tile) == 40 and C.sizeof(Operand) == 40
@@ -111,6 +111,7 @@ def load_library(path: os.PathLike | str | None = None) -> C.CDLL:
             "ficco_plan_run": ([vp, vp, vp, vp, vp], i32),
             "ficco_plan_run_parts": ([vp, vp, vp, vp, vp, i32, i32], i32),
             "ficco_gemm_bf16": ([vp, vp, vp, i64, i64, i64, C.c_float, i32, vp], i32),
+            "ficco_gemm_bf16_cfg": ([vp, vp, vp, i64, i64, i64, C.c_float, i32, i32, i32, vp], i32),
             "ficco_copy_batch": ([C.POINTER(vp), C.POINTER(vp), C.POINTER(sz), sz, vp], i32),
             "ficco_plan_set_trace": ([vp, vp], i32),
             "ficco_plan_info": ([vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)], i32),
@@ -303,10 +304,13 @@ class Plan:
             pass
 
 
-def gemm_bf16(a, b, out, alpha: float = 1.0, grid: int = 0, stream=None) -> None:
-    """out[M,N] = alpha * a[M,K] @ b[N,K]^T with the tcgen05 tile kernel (no flags)."""
+def gemm_bf16(a, b, out, alpha: float = 1.0, grid: int = 0, stream=None, tile_n: int = 0,
+              cta_group: int = 0) -> None:
+    """out[M,N] = alpha * a[M,K] @ b[N,K]^T with the tcgen05 tile kernel (no flags).
+
+    tile_n / cta_group 0 = automatic (wave model; CTA pairs)."""
     m, k = a.shape
     n = b.shape[0]
-    check(load_library().ficco_gemm_bf16(C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()),
-                                         C.c_void_p(out.data_ptr()), m, n, k, alpha, grid,
-                                         C.c_void_p(_stream_ptr(stream))))
+    check(load_library().ficco_gemm_bf16_cfg(C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()),
+                                             C.c_void_p(out.data_ptr()), m, n, k, alpha, grid, tile_n, cta_group,
+                                             C.c_void_p(_stream_ptr(stream))))

@@ -32,13 +32,15 @@ def lib():
     return runtime
 
 
+@pytest.mark.parametrize("cfg", [(0, 1), (0, 2), (128, 1), (160, 2), (192, 2), (224, 2), (256, 2), (224, 1)])
 @pytest.mark.parametrize("m,n,k", [(128, 256, 64), (256, 512, 1024), (384, 544, 520), (1000, 96, 200),
                                    (2048, 3584, 4096)])
-def test_tile_gemm_matches_fp32(lib, m, n, k):
+def test_tile_gemm_matches_fp32(lib, m, n, k, cfg):
+    tile_n, cg = cfg
     a = orc.seeded_inputs(0, 0, (m, k))
     w = orc.seeded_inputs(0, 1, (n, k), "normal")
     out = torch.empty(m, n, dtype=torch.bfloat16, device="cuda")
-    lib.gemm_bf16(_t(a), _t(w), out)
+    lib.gemm_bf16(_t(a), _t(w), out, tile_n=tile_n, cta_group=cg)
     torch.cuda.synchronize()
     np.testing.assert_allclose(_np(out), a @ w.T, rtol=RTOL, atol=ATOL)
 
