@@ -120,13 +120,15 @@ typedef struct {
   int32_t recv_row; /* REDUCE: row offset into every receive slot */
   int16_t rows;     /* valid output rows (<= 128; 0 = padding half of a CTA pair) */
   int16_t cols;     /* valid output columns (<= tile_n, multiple of 32) */
-  int16_t flag;     /* first readiness flag gating the A/B loads (-1: none) */
-  int16_t nflag;    /* consecutive flags [flag, flag+nflag) that must all be set (>= 1) */
-  int16_t kseg;     /* k-blocks (64 elements) per segment; segment s waits flag + s*kstride (0: off) */
+  int16_t flag;     /* base readiness flag gating the A/B loads (-1: none) */
+  uint16_t fmask;   /* flags flag+i for every set bit i must all be set before the loads */
+  int16_t kseg;     /* k-blocks (64 elements) per segment; segment s waits (flag + s*kstride, fmask) (0: off) */
   int16_t kstride;  /* flag stride between k segments */
   int16_t mode;     /* FICCO_EPI_* */
   int16_t chunk;    /* counter index (STORE_SIGNAL) or rs-flag group (REDUCE) */
-  int32_t reserved;
+  uint8_t a_src;    /* 0: A operand map; 1: alternate A map (a call argument, e.g. the local shard) */
+  uint8_t b_src;    /* 0: B operand map; 1: alternate B map */
+  uint16_t reserved;
 } ficco_tile;
 
 typedef struct {
@@ -148,6 +150,8 @@ typedef struct {
   ficco_operand c;    /* output, bf16 */
   ficco_operand part; /* STORE_SIGNAL destination (RS partials) */
   ficco_operand recv; /* REDUCE sources: slot j at off + j*recv_slot (+par on odd runs) */
+  ficco_operand a2;   /* alternate A source for tiles with a_src = 1 (FICCO_BUF_NONE: unused) */
+  ficco_operand b2;   /* alternate B source for tiles with b_src = 1 */
   int64_t recv_slot;  /* bytes between receive slots */
   int64_t k;          /* reduction length in elements (multiple of 8) */
   int32_t n_recv;     /* receive slots summed by REDUCE tiles */

@@ -215,15 +215,18 @@ int enqueue_run(ficco_plan* p, uint32_t parity, const void* a, const void* b, vo
                 bool copies, bool tiles, int (*launch)(ficco_plan*, uint32_t, const void*, const void*, void*,
                                                       cudaStream_t)) {
   ficco_comm* cm = p->comm;
-  const uint32_t* blk = cm->block(cm->rank, parity);
-  // run-local flags and tile counters start at 0
-  CK(cudaMemsetAsync(const_cast<uint32_t*>(blk) + FICCO_FLAG_RUN_LOCAL, 0,
-                     4 * size_t(FICCO_FLAG_BLOCK - FICCO_FLAG_RUN_LOCAL), s));
+  // Run-local flags and counters of THIS run's block were cleared during the previous run;
+  // clear the other block for the next run on a side stream, concurrently with this one.
+  // (Runs r-1 and r+1 share that block; r-1 is complete, and peers only write its run-local
+  // words after the owner's next DONE/PUB barrier, which follows this memset.)
+  cudaStream_t side = cm->copy[FICCO_MAX_STREAMS - 1];
+  CK(cudaEventRecord(cm->ev_fork, s));
+  CK(cudaStreamWaitEvent(side, cm->ev_fork, 0));
+  CK(cudaMemsetAsync(cm->block(cm->rank, parity ^ 1u) + FICCO_FLAG_RUN_LOCAL, 0,
+                     4 * size_t(FICCO_FLAG_BLOCK - FICCO_FLAG_RUN_LOCAL), side));
   const bool fork = copies && p->n_streams > 0;
-  if (fork) {
-    CK(cudaEventRecord(cm->ev_fork, s));
+  if (fork)
     for (int i = 0; i < p->n_streams; ++i) CK(cudaStreamWaitEvent(cm->copy[i], cm->ev_fork, 0));
-  }
   if (tiles) {
     int r = launch(p, parity, a, b, c, s);
     if (r) return r;
@@ -305,6 +308,8 @@ int enqueue_run(ficco_plan* p, uint32_t parity, const void* a, const void* b, vo
       CK(cudaStreamWaitEvent(s, cm->ev_join[i], 0));
     }
   }
+  CK(cudaEventRecord(cm->ev_join[FICCO_MAX_STREAMS - 1], side));
+  CK(cudaStreamWaitEvent(s, cm->ev_join[FICCO_MAX_STREAMS - 1], 0));
   return 0;
 }
 
@@ -323,6 +328,18 @@ int make_params(ficco_plan* p, uint32_t parity, const void* a, const void* b, vo
     int smem, b_rows;
     if ((r = kernel_for(p->tile_n, p->cta_group, &fn, &smem, &b_rows))) return r;
     if ((r = encode_bf16_2d(cm->drv, &prm->tmap_b, pb, d.b.rows, d.k, d.b.ld, b_rows))) return r;
+    prm->tmap_a2 = prm->tmap_a;
+    prm->tmap_b2 = prm->tmap_b;
+    if (d.a2.buf != FICCO_BUF_NONE) {
+      uint8_t* p2;
+      if ((r = resolve(cm, parity, d.a2.buf, -1, d.a2.off, d.a2.par, a, b, c, &p2))) return r;
+      if ((r = encode_bf16_2d(cm->drv, &prm->tmap_a2, p2, d.a2.rows, d.k, d.a2.ld, ficco::BM))) return r;
+    }
+    if (d.b2.buf != FICCO_BUF_NONE) {
+      uint8_t* p2;
+      if ((r = resolve(cm, parity, d.b2.buf, -1, d.b2.off, d.b2.par, a, b, c, &p2))) return r;
+      if ((r = encode_bf16_2d(cm->drv, &prm->tmap_b2, p2, d.b2.rows, d.k, d.b2.ld, b_rows))) return r;
+    }
   }
   uint8_t* po = nullptr;
   if (d.c.buf != FICCO_BUF_NONE && (r = resolve(cm, parity, d.c.buf, -1, d.c.off, d.c.par, a, b, c, &po))) return r;
@@ -614,16 +631,20 @@ int ficco_plan_create(ficco_comm_t* c, const ficco_plan_desc* d, ficco_plan_t** 
     if (t.mode < FICCO_EPI_STORE || t.mode > FICCO_EPI_REDUCE)
       return fail(FICCO_EINVAL, "tile " + std::to_string(i) + ": bad epilogue mode");
     if (t.flag >= 0) {
-      const int last = t.flag + (t.nflag - 1) + (t.kseg ? (int((d->k + 63) / 64) / t.kseg) * t.kstride : 0);
-      if (t.nflag < 1 || last >= FICCO_FLAG_BLOCK || t.kseg < 0)
+      int top = 15;
+      while (top > 0 && !(t.fmask & (1u << top))) --top;
+      const int last = t.flag + top + (t.kseg ? (int((d->k + 63) / 64) / t.kseg) * t.kstride : 0);
+      if (t.fmask == 0 || last >= FICCO_FLAG_BLOCK || t.kseg < 0)
         return fail(FICCO_EINVAL, "tile " + std::to_string(i) + ": flag range out of the flag block");
     }
+    if ((t.a_src && d->a2.buf == FICCO_BUF_NONE) || (t.b_src && d->b2.buf == FICCO_BUF_NONE))
+      return fail(FICCO_EINVAL, "tile " + std::to_string(i) + ": alternate operand not provided");
   }
   int n_streams = 0;
   bool user = false;
   for (int i = 0; i < d->n_ops; ++i) {
     const ficco_copy_op& op = d->ops[i];
-    if (op.stream < 0 || op.stream >= FICCO_MAX_STREAMS) return fail(FICCO_EINVAL, "op stream out of range");
+    if (op.stream < 0 || op.stream >= FICCO_MAX_STREAMS - 1) return fail(FICCO_EINVAL, "op stream out of range");
     if (op.op < FICCO_OP_COPY || op.op > FICCO_OP_STREAM_WAIT) return fail(FICCO_EINVAL, "bad copy opcode");
     if ((op.op == FICCO_OP_SIGNAL || op.op == FICCO_OP_NOTIFY || op.op == FICCO_OP_WAIT ||
          op.op == FICCO_OP_BARRIER) && (op.flag < 0 || op.flag + 4 > FICCO_FLAG_BLOCK))
@@ -780,7 +801,7 @@ int ficco_gemm_bf16_cfg(const void* a, const void* b, void* c, int64_t m, int64_
           t.rows = int16_t(row >= m ? 0 : (m - row < ficco::BM ? m - row : ficco::BM));
           t.cols = int16_t(n - j < tn ? n - j : tn);
           t.flag = -1;
-          t.nflag = 0;
+          t.fmask = 0;
           t.mode = FICCO_EPI_STORE;
           tiles.push_back(t);
         }

@@ -62,6 +62,8 @@ struct TileCfg {
 struct alignas(64) TileParams {
   CUtensorMap tmap_a;
   CUtensorMap tmap_b;
+  CUtensorMap tmap_a2;  // alternate sources (e.g. the caller's local shard, read in place)
+  CUtensorMap tmap_b2;
   const ficco_tile* tiles;
   int num_tiles;
   int num_kb;
@@ -116,27 +118,30 @@ __device__ __forceinline__ void producer_loop(const TileParams& p, uint8_t* sA, 
   for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
     const ficco_tile td = p.tiles[t];
     const int b_row = td.b_row + int(rank) * Cfg::B_ROWS;
+    const CUtensorMap* map_a = td.a_src ? &p.tmap_a2 : &p.tmap_a;
+    const CUtensorMap* map_b = td.b_src ? &p.tmap_b2 : &p.tmap_b;
     for (int kb = 0; kb < p.num_kb; ++kb) {
       if (td.flag >= 0) {
+        int base = -1;
         if (td.kseg == 0) {
-          if (kb == 0)
-            for (int f = 0; f < td.nflag; ++f) wait_flag(p.flags + td.flag + f, p.epoch, p.abort_word);
+          if (kb == 0) base = td.flag;
         } else if (kb % td.kseg == 0) {
-          const int base = td.flag + (kb / td.kseg) * td.kstride;
-          for (int f = 0; f < td.nflag; ++f) wait_flag(p.flags + base + f, p.epoch, p.abort_word);
+          base = td.flag + (kb / td.kseg) * td.kstride;
         }
+        if (base >= 0)
+          for (uint32_t m = td.fmask; m; m &= m - 1) wait_flag(p.flags + base + (__ffs(m) - 1), p.epoch, p.abort_word);
       }
       if (kb == 0 && p.trace) p.trace[gridDim.x + 2 * t] = globaltimer();
       mbar_wait(&empty[stage], phase ^ 1u);
       if constexpr (CG == 1) {
         mbar_arrive_expect_tx(&full[stage], Cfg::STAGE);
-        tma_load_2d(sA + stage * A_STAGE, &p.tmap_a, &full[stage], kb * BK, td.a_row, hint_a);
-        tma_load_2d(sB + stage * Cfg::B_STAGE, &p.tmap_b, &full[stage], kb * BK, b_row, hint_b);
+        tma_load_2d(sA + stage * A_STAGE, map_a, &full[stage], kb * BK, td.a_row, hint_a);
+        tma_load_2d(sB + stage * Cfg::B_STAGE, map_b, &full[stage], kb * BK, b_row, hint_b);
       } else {
         // both CTAs' bytes complete on the leader's barrier; the leader arms it for the pair
         if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE);
-        tma_load_2d_pair(sA + stage * A_STAGE, &p.tmap_a, &full[stage], kb * BK, td.a_row, hint_a);
-        tma_load_2d_pair(sB + stage * Cfg::B_STAGE, &p.tmap_b, &full[stage], kb * BK, b_row, hint_b);
+        tma_load_2d_pair(sA + stage * A_STAGE, map_a, &full[stage], kb * BK, td.a_row, hint_a);
+        tma_load_2d_pair(sB + stage * Cfg::B_STAGE, map_b, &full[stage], kb * BK, b_row, hint_b);
       }
       if (++stage == Cfg::STAGES) {
         stage = 0;
@@ -288,6 +293,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tile_gemm_kernel(const __grid_
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&p.tmap_a);
     tma_prefetch_desc(&p.tmap_b);
+    tma_prefetch_desc(&p.tmap_a2);
+    tma_prefetch_desc(&p.tmap_b2);
     for (int s = 0; s < Cfg::STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);

@@ -102,18 +102,16 @@ def _operand(buf, rows, ld, off=0, par=0) -> Operand:
     return o
 
 
-def _tile(a_row, b_row, c_row, c_col, rows, cols, flag=-1, nflag=0, kseg=0, kstride=0, mode=EPI_STORE, chunk=0,
-          recv_row=0) -> Tile:
+def _tile(a_row, b_row, c_row, c_col, rows, cols, flag=-1, fmask=0, kseg=0, kstride=0, mode=EPI_STORE, chunk=0,
+          recv_row=0, a_src=0, b_src=0) -> Tile:
     t = Tile()
     t.a_row, t.b_row, t.c_row, t.c_col, t.recv_row = a_row, b_row, c_row, c_col, recv_row
-    t.rows, t.cols, t.flag, t.nflag = rows, cols, flag, (nflag if flag >= 0 else 0)
-    t.kseg, t.kstride, t.mode, t.chunk = kseg, kstride, mode, chunk
+    t.rows, t.cols, t.flag, t.fmask = rows, cols, flag, (fmask if flag >= 0 else 0)
+    t.kseg, t.kstride, t.mode, t.chunk, t.a_src, t.b_src = kseg, kstride, mode, chunk, a_src, b_src
     return t
 
 
 B200_SMS = 148
-
-
 DEFAULT_CTA_GROUP = 2
 
 
@@ -130,7 +128,7 @@ def pair_tiles(tiles: list[Tile]) -> list[Tile]:
     pending: dict[tuple, Tile] = {}
     out: list[Tile] = []
     for t in tiles:
-        key = (t.b_row, t.c_col, t.cols)
+        key = (t.b_row, t.c_col, t.cols, t.b_src)
         mate = pending.pop(key, None)
         if mate is None:
             pending[key] = t
@@ -138,7 +136,8 @@ def pair_tiles(tiles: list[Tile]) -> list[Tile]:
             out += [mate, t]
     for t in pending.values():
         # the padding CTA still loads half of B, so it must honour the same gates
-        pad = _tile(t.a_row, t.b_row, t.c_row, t.c_col, 0, t.cols, t.flag, t.nflag, t.kseg, t.kstride)
+        pad = _tile(t.a_row, t.b_row, t.c_row, t.c_col, 0, t.cols, t.flag, t.fmask, t.kseg, t.kstride,
+                    a_src=t.a_src, b_src=t.b_src)
         out += [t, pad]
     return out
 
@@ -172,21 +171,19 @@ def _my_gemms(plan: ExecutionPlan, rank: int) -> list[GemmSpec]:
 
 
 def _publish(ops: list, g: int, world: int, row_bytes: int, shard_rows: int, gather_off: int, par: int,
-             src_buf: int, rounds: int) -> None:
-    """Local shard -> own slot (before the fork, on the compute stream), then the publish barrier.
+             src_buf: int) -> None:
+    """Local shard -> own slot of the gathered buffer (stream 0), then the publish barrier.
 
-    Stream 0 marks the local rows present (LOCAL), runs the cross-rank
-    barrier (each rank sets its byte in everyone's PUB word and waits for all
-    bytes), records EV_START (every pull chain waits on it), and finally sets
-    XFER[c, g] for every round c so round-granular waits can span all G ranks.
+    The tile kernel reads the local rows in place from the call argument (the
+    alternate operand map), so nothing local gates a tile: the copy exists for
+    the peers' pulls and for the gathered output. Stream 0 then runs the
+    cross-rank barrier (each rank sets its byte in everyone's PUB word and waits
+    for all bytes) and records EV_START, which every pull chain waits on.
     """
     ops.append(_op(OP_COPY, src_buf=src_buf, dst_buf=BUF_WS, src_off=0, dst_off=gather_off + g * shard_rows * row_bytes,
                    dst_par=par, width=shard_rows * row_bytes, stream=0))
-    ops.append(_op(OP_SIGNAL, flag=F_LOCAL, stream=0))
     ops.append(_op(OP_BARRIER, flag=F_PUB, stream=0))
     ops.append(_op(OP_RECORD, value=EV_START, stream=0))
-    for c in range(rounds):  # off the pull chains' critical path
-        ops.append(_op(OP_SIGNAL, flag=F_XFER + c * world + g, stream=0))
 
 
 def _peer_stream(p: int, g: int) -> int:
@@ -223,7 +220,7 @@ def lower_ag(plan: ExecutionPlan, rank: int, gathered: str = "A", alpha: float =
     src_buf = BUF_A if gathered == "A" else BUF_B
     if G > MAX_WORLD:
         raise PlanError(f"at most {MAX_WORLD} ranks")
-    _publish(ops, g, G, row_bytes, R, low.gather_off, low.gather_par, src_buf, G)
+    _publish(ops, g, G, row_bytes, R, low.gather_off, low.gather_par, src_buf)
 
     def pull(p: int, row0: int, nrows: int, stream: int) -> CopyOp:
         off = low.gather_off + row0 * row_bytes
@@ -275,23 +272,26 @@ def lower_ag(plan: ExecutionPlan, rank: int, gathered: str = "A", alpha: float =
     # ---- tile program: this rank's GemmSpecs in plan order, each fragment gated by the flags it reads
     r_chunk = M // (G * G)
 
+    peers_mask = ((1 << G) - 1) & ~(1 << g)
+
     def gate(start: int) -> tuple[int, int, int, int]:
-        """(flag, nflag, kseg, kstride) for rows starting at `start` (one owner)."""
+        """(flag, fmask, kseg, kstride) for rows starting at `start` (one owner)."""
         owner = start // R
-        if kind is ScheduleKind.SERIAL:
-            return F_XFER, G, 0, 0                      # the whole gather (round 0 of every rank)
-        if kind is ScheduleKind.SHARD_OVERLAP_P2P:
-            return (F_LOCAL, 1, 0, 0) if owner == g else (F_RING + (g - owner) % G, 1, 0, 0)
-        if kind is ScheduleKind.UNIFORM_FUSED_2D:
-            return (F_LOCAL, 1, 0, 0) if owner == g else (F_XFER + owner, 1, kseg, G)
-        c = (start - owner * R) // r_chunk
-        if kind is ScheduleKind.UNIFORM_FUSED_1D:
-            return F_XFER + c * G, G, 0, 0              # the step waits for its whole round (gather)
+        if kind is ScheduleKind.UNIFORM_FUSED_1D:       # the step waits for its whole round (the gather)
+            c = (start - owner * R) // r_chunk
+            return F_XFER + c * G, peers_mask, 0, 0
         if owner == g:
-            return F_LOCAL, 1, 0, 0                     # hetero: local shard runs at t = 0
+            return -1, 0, 0, 0                           # local rows: read in place, no wait
+        if kind is ScheduleKind.SERIAL:
+            return F_XFER, peers_mask, 0, 0              # the whole all-gather
+        if kind is ScheduleKind.SHARD_OVERLAP_P2P:
+            return F_RING + (g - owner) % G, 1, 0, 0
+        if kind is ScheduleKind.UNIFORM_FUSED_2D:
+            return F_XFER + owner, 1, kseg, G            # k-segment c waits chunk (owner, c)
+        c = (start - owner * R) // r_chunk
         if kind is ScheduleKind.HETERO_FUSED_1D:
-            return F_XFER + c * G, G, 0, 0              # one fused GEMM per round
-        return F_XFER + c * G + owner, 1, 0, 0          # unfused: exactly its own chunk
+            return F_XFER + c * G, peers_mask, 0, 0      # one fused GEMM per round
+        return F_XFER + c * G + owner, 1, 0, 0           # unfused: exactly its own chunk
 
     Q = other_rows if gathered == "B" else None
     if gathered == "B" and Q is None:
@@ -324,19 +324,23 @@ def lower_ag(plan: ExecutionPlan, rank: int, gathered: str = "A", alpha: float =
                            units)
     tiles = low.tiles
     for start, count in frag_lists:
-        flag, nflag, ks, kstride = gate(start)
+        flag, fmask, ks, kstride = gate(start)
+        local = start // R == g  # rows of the own shard come from the call argument (alternate map)
+        shift = g * R if local else 0
         if gathered == "A":
             for m0 in range(start, start + count, TILE_M):
                 rows = min(TILE_M, start + count - m0)
                 for n0 in range(0, N, tn):
-                    tiles.append(_tile(m0, n0, m0, n0, rows, min(tn, N - n0), flag, nflag, ks, kstride))
+                    tiles.append(_tile(m0 - shift, n0, m0, n0, rows, min(tn, N - n0), flag, fmask, ks, kstride,
+                                       a_src=int(local)))
         else:
             if count % 32:
                 raise PlanError(f"gathered-B fragments must be multiples of 32 rows, got {count}")
             for n0 in range(start, start + count, tn):
                 cols = min(tn, start + count - n0)
                 for m0 in range(0, Q, TILE_M):
-                    tiles.append(_tile(m0, n0, m0, n0, min(TILE_M, Q - m0), cols, flag, nflag, ks, kstride))
+                    tiles.append(_tile(m0, n0 - shift, m0, n0, min(TILE_M, Q - m0), cols, flag, fmask, ks, kstride,
+                                       b_src=int(local)))
 
     if cta_group == 2:
         low.tiles[:] = pair_tiles(low.tiles)
@@ -344,8 +348,10 @@ def lower_ag(plan: ExecutionPlan, rank: int, gathered: str = "A", alpha: float =
     gat = _operand(BUF_WS, M, K, low.gather_off, low.gather_par)
     if gathered == "A":
         d.a, d.b, d.c = gat, _operand(BUF_B, N, K), _operand(BUF_C, M, N)
+        d.a2, d.b2 = _operand(BUF_A, R, K), _operand(BUF_NONE, 0, 0)
     else:
         d.a, d.b, d.c = _operand(BUF_A, Q, K), gat, _operand(BUF_C, Q, M)
+        d.a2, d.b2 = _operand(BUF_NONE, 0, 0), _operand(BUF_B, R, K)
     d.part = _operand(BUF_NONE, 0, 0)
     d.recv = _operand(BUF_NONE, 0, 0)
     d.k, d.alpha, d.grid, d.tile_n, d.cta_group = K, alpha, grid, tn, cta_group
@@ -460,6 +466,7 @@ def lower_rs(scenario: Scenario, kind: ScheduleKind, rank: int, grid: int = 0, v
     d.c = _operand(BUF_C, R, N)
     d.part = _operand(BUF_WS, M, N, part_off)
     d.recv = _operand(BUF_WS, R, N, low.recv_off, low.recv_par)
+    d.a2, d.b2 = _operand(BUF_NONE, 0, 0), _operand(BUF_NONE, 0, 0)
     d.recv_slot, d.n_recv, d.rs_flag0 = low.recv_slot, G - 1, F_RS
     d.n_counters = len(units)
     d.k, d.alpha, d.grid, d.tile_n, d.cta_group = K, 1.0, grid, tn, cta_group

@@ -57,8 +57,8 @@ class CopyOp(C.Structure):
 class Tile(C.Structure):
     _fields_ = [("a_row", C.c_int32), ("b_row", C.c_int32), ("c_row", C.c_int32), ("c_col", C.c_int32),
                 ("recv_row", C.c_int32), ("rows", C.c_int16), ("cols", C.c_int16), ("flag", C.c_int16),
-                ("nflag", C.c_int16), ("kseg", C.c_int16), ("kstride", C.c_int16), ("mode", C.c_int16),
-                ("chunk", C.c_int16), ("reserved", C.c_int32)]
+                ("fmask", C.c_uint16), ("kseg", C.c_int16), ("kstride", C.c_int16), ("mode", C.c_int16),
+                ("chunk", C.c_int16), ("a_src", C.c_uint8), ("b_src", C.c_uint8), ("reserved", C.c_uint16)]
 
 
 class Operand(C.Structure):
@@ -69,7 +69,8 @@ class Operand(C.Structure):
 class PlanDesc(C.Structure):
     _fields_ = [("n_ops", C.c_int32), ("n_tiles", C.c_int32), ("ops", C.POINTER(CopyOp)),
                 ("tiles", C.POINTER(Tile)), ("a", Operand), ("b", Operand), ("c", Operand), ("part", Operand),
-                ("recv", Operand), ("recv_slot", C.c_int64), ("k", C.c_int64), ("n_recv", C.c_int32),
+                ("recv", Operand), ("a2", Operand), ("b2", Operand), ("recv_slot", C.c_int64), ("k", C.c_int64),
+                ("n_recv", C.c_int32),
                 ("rs_flag0", C.c_int32), ("n_counters", C.c_int32), ("grid", C.c_int32), ("alpha", C.c_float),
                 ("tile_n", C.c_int32), ("cta_group", C.c_int32), ("reserved", C.c_int32)]
 

@@ -1,0 +1,135 @@
+"""Cross-rank protocol of the lowered programs, executed by the multi-rank interpreter (CPU).
+
+Every executable schedule is lowered for every rank of a G-rank job and run
+for several consecutive calls under randomised interleavings
+(tests/protocol_sim.py). After each call each rank's outputs must match the
+oracle: gathered buffers bit-exact, GEMM outputs within bf16 tolerance, RS
+shards equal to the rank-ordered sum of partials. Stale or not-yet-written
+bytes (a missing dependency, an early buffer reuse) show up as mismatches;
+a missing signal shows up as a deadlock.
+"""
+import numpy as np
+import pytest
+
+from oracle import ficco_oracle as orc
+from paper_2512_10236_b200.lowering import lower_ag, lower_rs
+from paper_2512_10236_b200.ops import _scenario
+from paper_2512_10236_b200.routing import ScheduleKind, build_plan
+
+from protocol_sim import World, bf16_bits, bits_f32
+
+AG_KINDS = ["serial", "shard_overlap_p2p", "uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d",
+            "uniform_fused_2d"]
+RUNS = 3
+
+
+def _ag_world(kind, G, R, K, N, cta_group, seed):
+    sc = _scenario("sim", R * G, N, K, G)
+    lows = [lower_ag(build_plan(sc, ScheduleKind(kind)), g, "A", cta_group=cta_group) for g in range(G)]
+    ws = max(low.ws_bytes for low in lows)
+    for low in lows:
+        low.ws_bytes = ws
+    w = orc.seeded_inputs(seed, 999, (N, K), "normal")
+    args, expect = [], []
+    for run in range(RUNS):
+        shards = [orc.seeded_inputs(seed * 10 + run, g, (R, K)) for g in range(G)]
+        full = np.concatenate(shards)
+        expect.append((full, full @ w.T))
+        args.append([{"a": bf16_bits(shards[g]), "b": bf16_bits(w),
+                      "c": np.zeros((R * G, N), dtype=np.uint16)} for g in range(G)])
+    return lows, args, expect
+
+
+@pytest.mark.parametrize("kind", AG_KINDS)
+@pytest.mark.parametrize("G", [2, 4])
+@pytest.mark.parametrize("cta_group", [1, 2])
+def test_ag_protocol(kind, G, cta_group):
+    R, K, N = 64, 256, 64
+    for seed in range(3):
+        lows, args, expect = _ag_world(kind, G, R, K, N, cta_group, seed)
+        world = World(lows, args, seed=seed)
+        checked = []
+
+        def on_done(rank, run, world=world):
+            full, c_ref = expect[run]
+            low = lows[rank]
+            off = low.gather_off + (low.gather_par if run & 1 else 0)
+            gat = world.ranks[rank].ws[off: off + full.size * 2].view(np.uint16).reshape(full.shape)
+            assert np.array_equal(bits_f32(gat), full), (kind, rank, run, "gathered")
+            c = bits_f32(args[run][rank]["c"])
+            np.testing.assert_allclose(c, c_ref, rtol=2e-2, atol=2e-2, err_msg=f"{kind} rank {rank} run {run}")
+            checked.append((rank, run))
+
+        world.on_run_done = on_done
+        world.run(RUNS)
+        assert len(checked) == G * RUNS
+
+
+@pytest.mark.parametrize("kind", ["uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d"])
+@pytest.mark.parametrize("G", [2, 3, 4])
+@pytest.mark.parametrize("cta_group", [1, 2])
+def test_rs_protocol(kind, G, cta_group):
+    r, Kg, N = 16, 64, 64
+    M = r * G * G
+    R = M // G
+    for seed in range(3):
+        sc = _scenario("rs", M, N, Kg, G)
+        lows = [lower_rs(sc, ScheduleKind(kind), g, cta_group=cta_group) for g in range(G)]
+        ws = max(low.ws_bytes for low in lows)
+        for low in lows:
+            low.ws_bytes = ws
+        args, expect = [], []
+        for run in range(RUNS):
+            a = [orc.seeded_inputs(seed * 10 + run, g, (M, Kg)) for g in range(G)]
+            w = [orc.seeded_inputs(seed * 10 + run, 50 + g, (N, Kg), "normal") for g in range(G)]
+            expect.append(orc.execute_rs(a, w))
+            args.append([{"a": bf16_bits(a[g]), "b": bf16_bits(w[g]), "c": np.zeros((R, N), dtype=np.uint16)}
+                         for g in range(G)])
+        world = World(lows, args, seed=seed)
+        done = []
+
+        def on_done(rank, run):
+            np.testing.assert_allclose(bits_f32(args[run][rank]["c"]), expect[run][rank], rtol=2e-2, atol=3e-2,
+                                       err_msg=f"{kind} rank {rank} run {run}")
+            done.append(1)
+
+        world.on_run_done = on_done
+        world.run(RUNS)
+        assert len(done) == G * RUNS
+
+
+@pytest.mark.parametrize("kind", ["uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d", "serial",
+                                  "shard_overlap_p2p"])
+@pytest.mark.parametrize("cta_group", [1, 2])
+def test_cp_protocol(kind, cta_group):
+    G, d, Tq, Tkv = 4, 64, 96, 512
+    sc = _scenario("cp", Tkv, Tq, d, G)
+    lows = [lower_ag(build_plan(sc, ScheduleKind(kind)), g, "B", alpha=0.125, other_rows=Tq, cta_group=cta_group)
+            for g in range(G)]
+    ws = max(low.ws_bytes for low in lows)
+    for low in lows:
+        low.ws_bytes = ws
+    args, expect = [], []
+    for run in range(RUNS):
+        q = orc.seeded_inputs(run, 77, (Tq, d), "normal")
+        ks = [orc.seeded_inputs(run, g, (Tkv // G, d), "normal") for g in range(G)]
+        expect.append(orc.execute_cp_qk(q, ks, 0.125)[0])
+        args.append([{"a": bf16_bits(q), "b": bf16_bits(ks[g]), "c": np.zeros((Tq, Tkv), dtype=np.uint16)}
+                     for g in range(G)])
+    world = World(lows, args, seed=7)
+
+    def on_done(rank, run):
+        np.testing.assert_allclose(bits_f32(args[run][rank]["c"]), expect[run], rtol=2e-2, atol=2e-2)
+
+    world.on_run_done = on_done
+    world.run(RUNS)
+
+
+def test_missing_signal_deadlocks():
+    """The interpreter really enforces gating: dropping a pull chain's signals must deadlock."""
+    from paper_2512_10236_b200.runtime import OP_SIGNAL
+    from protocol_sim import Deadlock
+    lows, args, _ = _ag_world("hetero_unfused_1d", 2, 64, 256, 64, 1, 0)
+    lows[1].ops = [op for op in lows[1].ops if op.op != OP_SIGNAL]
+    with pytest.raises(Deadlock):
+        World(lows, args).run(1)
