@@ -1,26 +1,30 @@
 """FiCCO hot-path benchmark (driver contract: one JSON line from rank 0).
 
-Workload (BASELINE.json configs[1]): Llama-3-8B TP/SP MLP up-projection
-all-gather -> GEMM, bf16, seq 8192, per-GPU post-gather GEMM (M, N, K) =
-(8192, 3584 = gate||up of 14336/8, 4096).
+Default workload (BASELINE.json configs[1], the config the metric is quoted on):
+C2 — Llama-3-8B TP/SP MLP up-projection all-gather -> GEMM, bf16, seq 8192,
+per-GPU post-gather GEMM (M, N, K) = (8192, 3584 = gate||up of 14336/8, 4096).
+``--workload c3`` (Llama-3-70B down-proj GEMM -> reduce-scatter, seq 16384,
+(M, N, K) = (16384, 8192, 28672/G)) and ``--workload c4`` (context-parallel KV
+all-gather -> QK^T, 128K context, d=128, 16384 local queries) measure the
+other configs the same way.
 
 * N = 1 (default): decomposition-only mode: this GPU plays
-  rank 0 of an 8-rank job; the 7 peers' shards sit in local HBM stand-in
-  workspaces, so the copy engines move the same 56 MiB of chunks (locally) and
-  the tile kernel does exactly rank 0's work.
-* N > 1 (torchrun): G = N real ranks over NVLink (copy-engine pulls from
-  peers' IPC-mapped workspaces), same per-GPU GEMM -> weak scaling.
+  rank 0 of an 8-rank job; the 7 peers' data sits in local HBM stand-in
+  workspaces, so the copy engines move the same chunks (locally) and the tile
+  kernel does exactly rank 0's work.
+* N > 1 (torchrun): G = N real ranks over NVLink (copy-engine pulls/pushes on
+  IPC-mapped workspaces), same per-GPU GEMM -> weak scaling.
 
-A step = one overlapped AG->GEMM call (``ops.all_gather_matmul``) on inputs
-already in HBM; per-step CUDA events on the compute stream, L2 flushed (256 MiB
-write) between steps outside the events, max over ranks. ``value`` is the
-median step time of the best FiCCO schedule in microseconds
-(higher_is_better = false); every schedule, the serialized baseline
-(NCCL all-gather / copy-engine gather, then cuBLAS), the ideal-overlap
-roofline T* and the speedup are reported beside it.
+A step = one overlapped op call through the public API on inputs already in
+HBM. Per-step CUDA events on the compute stream, L2 flushed (256 MiB write)
+between steps outside the events, all steps enqueued asynchronously between a
+barrier + synchronize on each side, max over ranks. ``value`` = median step
+time (µs, lower is better) of the best FiCCO schedule; every schedule of the
+design space, the serialized baseline (NCCL collective / copy-engine stand-in,
+then cuBLAS), the ideal-overlap roofline T* and the speedup sit beside it.
 
 ``--impl reference`` times the CPU restatement of the reference's path
-(oracle/ficco_oracle.py; the reference itself is a pure-Python simulator with
+(oracle/ficco_oracle.py — the reference itself is a pure-Python simulator with
 no tensor execution) on the host cores, same metric/unit/config.
 """
 
@@ -39,28 +43,23 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-M_ROWS, N_COLS, K_DIM, G_CFG = 8192, 3584, 4096, 8
 METRIC = "AG/RS+GEMM µs & speedup vs serialized NCCL+GEMM, % ideal overlap, 2/4/8 B200"
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 NVLINK_NOMINAL = 900e9
-KINDS = ["uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d", "uniform_fused_2d", "shard_overlap_p2p",
-         "serial"]
+G_VIRTUAL = 8
 
 
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            d = json.load(f)
-        return d, "measured"
+            return json.load(f), "measured"
     except Exception:
         return dict(PEAKS_FALLBACK), "fallback"
 
 
 def dist_env():
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return world, rank, local
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
 
 
 class ClockSampler:
@@ -78,8 +77,7 @@ class ClockSampler:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
                  "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
+            threading.Thread(target=self._read, daemon=True).start()
         except Exception:
             self.proc = None
         return self
@@ -101,20 +99,20 @@ class ClockSampler:
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        num = lambda x: x.replace(".", "", 1).isdigit()  # noqa: E731
+        sm = [float(r[0]) for r in self.rows if num(r[0])]
+        mx = [float(r[1]) for r in self.rows if num(r[1])]
+        pw = [float(r[2]) for r in self.rows if num(r[2])]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "power_w_max": max(pw) if pw else None, "reasons": reasons, "samples": len(self.rows)}
 
 
 def time_steps(fn, steps: int, warmup: int, flush, stream, barrier=None) -> list[float]:
-    """Per-step device times (ms): CUDA events on `stream` around each step, L2 flushed
-    (256 MiB write) between steps outside the events. Everything is enqueued
-    asynchronously (the host runs ahead, so launch latency hides behind the
-    flush as it would in a pipelined job); the K timed steps are bracketed by a
-    barrier + synchronize on both sides."""
+    """Per-step device times (ms): CUDA events on `stream` around each step, L2 flushed between
+    steps outside the events, everything enqueued asynchronously (launch latency hides behind
+    the flush as in a pipelined job); barrier + synchronize on both sides of the timed steps."""
     import torch
     for _ in range(warmup):
         flush()
@@ -135,39 +133,293 @@ def time_steps(fn, steps: int, warmup: int, flush, stream, barrier=None) -> list
     return [a.elapsed_time(b) for a, b in evs]
 
 
+# ------------------------------------------------------------------------------------------ workloads
+
+class AGWorkload:
+    """C2: all-gather -> GEMM (TP/SP up-projection)."""
+
+    key = "c2"
+    title = "C2 Llama-3-8B TP/SP MLP up-proj AG->GEMM"
+    kinds = ["uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d", "uniform_fused_2d", "shard_overlap_p2p",
+             "serial"]
+
+    def __init__(self, torch, dev, G, rank, world, ops):
+        self.t, self.dev, self.G, self.rank, self.world, self.ops = torch, dev, G, rank, world, ops
+        self.M, self.N, self.K = 8192, 3584, 4096
+        self.R = self.M // G
+        gen = torch.Generator(device=dev).manual_seed(rank)
+        self.shards = [(torch.rand(self.R, self.K, generator=gen, device=dev) * 2 - 1).to(torch.bfloat16)
+                       for _ in range(G)]
+        wgen = torch.Generator(device=dev).manual_seed(99)
+        self.w = (torch.randn(self.N, self.K, generator=wgen, device=dev) / math.sqrt(self.K)).to(torch.bfloat16)
+        self.out = torch.empty(self.M, self.N, dtype=torch.bfloat16, device=dev)
+        self.gathered = torch.empty(self.M, self.K, dtype=torch.bfloat16, device=dev)
+        self.flops = 2.0 * self.M * self.N * self.K
+        self.comm_bytes = (G - 1) * self.R * self.K * 2
+
+    def config(self):
+        return {"M": self.M, "N": self.N, "K": self.K, "seq_len": self.M}
+
+    def prepare(self, grp, kind):
+        _, low, _ = self.ops.prepare_ag(grp, self.R, self.K, self.N, kind)
+        if grp.virtual:
+            grp.load_peer_shards(low, self.shards)
+
+    def step(self, grp, kind):
+        return lambda: self.ops.all_gather_matmul(self.shards[0], self.w, kind=kind, group=grp, out=self.out)
+
+    def serial(self):
+        t = self.t
+        if self.world > 1:
+            def fn():
+                t.distributed.all_gather_into_tensor(self.gathered, self.shards[0])
+                t.matmul(self.gathered, self.w.T, out=self.out)
+            return fn, "NCCL all_gather_into_tensor + cuBLAS"
+
+        def fn():
+            for p in range(self.G):
+                self.gathered[p * self.R:(p + 1) * self.R].copy_(self.shards[p], non_blocking=True)
+            t.matmul(self.gathered, self.w.T, out=self.out)
+        return fn, "copy-engine gather of the 7 peer shards + cuBLAS (virtual peers)"
+
+    def cublas(self):
+        a = self.t.cat(self.shards)
+        return lambda: self.t.matmul(a, self.w.T, out=self.out)
+
+    def kernel(self, runtime):
+        a = self.t.cat(self.shards)
+        return lambda: runtime.gemm_bf16(a, self.w, self.out), "tensor", self.flops
+
+    def check(self):
+        rows = slice(0, 256)
+        ref = self.t.cat(self.shards)[rows].float() @ self.w.float().T
+        return bool(self.t.allclose(self.out[rows].float(), ref, rtol=1.6e-2, atol=1e-2))
+
+    def e2e(self, grp, kind):
+        t = self.t
+        host_a = self.shards[0].cpu().pin_memory()
+        host_c = t.empty(self.M, self.N, dtype=t.bfloat16).pin_memory()
+        dev_a = t.empty_like(self.shards[0])
+
+        def fn():
+            dev_a.copy_(host_a, non_blocking=True)
+            self.ops.all_gather_matmul(dev_a, self.w, kind=kind, group=grp, out=self.out)
+            host_c.copy_(self.out, non_blocking=True)
+        return fn, self.R * self.K * 2, self.M * self.N * 2
+
+    def ideal_us(self, peaks):
+        return max(self.flops / (peaks["bf16_tflops"] * 1e12), self.comm_bytes / NVLINK_NOMINAL) * 1e6
+
+    def cpu_sample(self, orc, kind):
+        sh = [s.float().cpu().numpy() for s in self.shards]
+        w = self.w.float().cpu().numpy()
+        frags = orc.gemm_fragments(kind, self.M, self.K, self.G, 0)
+        rows_first = sum(c for rows, _ in frags[:1] for _, c in rows)
+        orc.execute_ag_rank(kind, sh, w, 0, steps=1)
+        t0, reps = time.perf_counter(), 0
+        while reps < 5 and time.perf_counter() - t0 < 10.0:
+            orc.execute_ag_rank(kind, sh, w, 0, steps=1)
+            reps += 1
+        per_op = (time.perf_counter() - t0) / reps * (self.M / rows_first)
+        return per_op, (f"oracle execute_ag_rank({kind}): first GemmSpec ({rows_first}/{self.M} rows) x{reps}, "
+                        f"scaled linearly to the full op")
+
+
+class RSWorkload(AGWorkload):
+    """C3: GEMM -> reduce-scatter (TP/SP down-projection)."""
+
+    key = "c3"
+    title = "C3 Llama-3-70B TP/SP down-proj GEMM->RS"
+    kinds = ["uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d"]
+
+    def __init__(self, torch, dev, G, rank, world, ops):
+        self.t, self.dev, self.G, self.rank, self.world, self.ops = torch, dev, G, rank, world, ops
+        self.M, self.N, self.K = 16384, 8192, 28672 // G
+        self.R = self.M // G
+        gen = torch.Generator(device=dev).manual_seed(rank)
+        self.a = (torch.rand(self.M, self.K, generator=gen, device=dev) * 2 - 1).to(torch.bfloat16)
+        self.w = (torch.randn(self.N, self.K, generator=gen, device=dev) / math.sqrt(self.K)).to(torch.bfloat16)
+        self.peer_parts = [(torch.randn(self.R, self.N, generator=gen, device=dev) * 0.1).to(torch.bfloat16)
+                           for _ in range(G - 1)]
+        self.out = torch.empty(self.R, self.N, dtype=torch.bfloat16, device=dev)
+        self.part = torch.empty(self.M, self.N, dtype=torch.bfloat16, device=dev)
+        self.sink = torch.empty((G - 1) * self.R, self.N, dtype=torch.bfloat16, device=dev)
+        self.flops = 2.0 * self.M * self.N * self.K
+        self.comm_bytes = (G - 1) * self.R * self.N * 2
+
+    def config(self):
+        return {"M": self.M, "N": self.N, "K": self.K, "seq_len": self.M}
+
+    def prepare(self, grp, kind):
+        _, low, _ = self.ops.prepare_rs(grp, self.M, self.K, self.N, kind)
+        if grp.virtual:
+            grp.load_peer_partials(low, self.peer_parts)
+
+    def step(self, grp, kind):
+        return lambda: self.ops.matmul_reduce_scatter(self.a, self.w, kind=kind, group=grp, out=self.out)
+
+    def serial(self):
+        t = self.t
+        if self.world > 1:
+            def fn():
+                t.matmul(self.a, self.w.T, out=self.part)
+                t.distributed.reduce_scatter_tensor(self.out, self.part)
+            return fn, "cuBLAS + NCCL reduce_scatter_tensor"
+        R = self.R
+
+        def fn():
+            t.matmul(self.a, self.w.T, out=self.part)
+            self.sink.copy_(self.part[R:], non_blocking=True)  # the 7 remote shards leave (copy engine)
+            acc = self.part[:R].float()
+            for p in self.peer_parts:
+                acc += p.float()
+            self.out.copy_(acc)
+        return fn, "cuBLAS + copy-engine egress of 7 shards + reduction of 8 partials (virtual peers)"
+
+    def cublas(self):
+        return lambda: self.t.matmul(self.a, self.w.T, out=self.part)
+
+    def kernel(self, runtime):
+        return lambda: runtime.gemm_bf16(self.a, self.w, self.part), "tensor", self.flops
+
+    def check(self):
+        ref = self.a[:self.R].float() @ self.w.float().T
+        for p in self.peer_parts:
+            ref += p.float()
+        return bool(self.t.allclose(self.out.float(), ref, rtol=1.6e-2, atol=3e-2))
+
+    def e2e(self, grp, kind):
+        t = self.t
+        host_a = self.a.cpu().pin_memory()
+        host_c = t.empty(self.R, self.N, dtype=t.bfloat16).pin_memory()
+        dev_a = t.empty_like(self.a)
+
+        def fn():
+            dev_a.copy_(host_a, non_blocking=True)
+            self.ops.matmul_reduce_scatter(dev_a, self.w, kind=kind, group=grp, out=self.out)
+            host_c.copy_(self.out, non_blocking=True)
+        return fn, self.M * self.K * 2, self.R * self.N * 2
+
+    def cpu_sample(self, orc, kind):
+        a = self.a[: self.R].float().cpu().numpy()
+        w = self.w.float().cpu().numpy()
+        t0 = time.perf_counter()
+        a @ w.T
+        per_op = (time.perf_counter() - t0) * self.G
+        return per_op, f"numpy fp32 GEMM of one {self.R}-row chunk, scaled x{self.G} (partials of the whole op)"
+
+
+class CPWorkload(AGWorkload):
+    """C4: context-parallel KV all-gather -> attention scores S = Q K^T / sqrt(d)."""
+
+    key = "c4"
+    title = "C4 CP KV all-gather -> QK^T, 128K context, d=128"
+    kinds = ["uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d", "shard_overlap_p2p", "serial"]
+
+    def __init__(self, torch, dev, G, rank, world, ops):
+        self.t, self.dev, self.G, self.rank, self.world, self.ops = torch, dev, G, rank, world, ops
+        self.Tkv, self.Tq, self.d = 131072, 131072 // G, 128
+        self.R = self.Tkv // G
+        gen = torch.Generator(device=dev).manual_seed(rank)
+        self.q = torch.randn(self.Tq, self.d, generator=gen, device=dev).to(torch.bfloat16)
+        self.shards = [torch.randn(self.R, self.d, generator=gen, device=dev).to(torch.bfloat16) for _ in range(G)]
+        self.out = torch.empty(self.Tq, self.Tkv, dtype=torch.bfloat16, device=dev)
+        self.kall = torch.empty(self.Tkv, self.d, dtype=torch.bfloat16, device=dev)
+        self.scale = 1.0 / math.sqrt(self.d)
+        self.flops = 2.0 * self.Tq * self.Tkv * self.d
+        self.out_bytes = self.Tq * self.Tkv * 2
+        self.comm_bytes = (G - 1) * self.R * self.d * 2
+
+    def config(self):
+        return {"Tkv": self.Tkv, "Tq": self.Tq, "d": self.d, "seq_len": self.Tkv}
+
+    def prepare(self, grp, kind):
+        _, low, _ = self.ops.prepare_cp(grp, self.Tq, self.d, self.Tkv, kind)
+        if grp.virtual:
+            grp.load_peer_shards(low, self.shards)
+
+    def step(self, grp, kind):
+        return lambda: self.ops.cp_kv_all_gather_qk(self.q, self.shards[0], kind=kind, group=grp, out=self.out)
+
+    def serial(self):
+        t = self.t
+        if self.world > 1:
+            def fn():
+                t.distributed.all_gather_into_tensor(self.kall, self.shards[0])
+                t.addmm(self.out, self.q, self.kall.T, beta=0, alpha=self.scale, out=self.out)
+            return fn, "NCCL all_gather_into_tensor + cuBLAS (alpha = 1/sqrt(d))"
+
+        def fn():
+            for p in range(self.G):
+                self.kall[p * self.R:(p + 1) * self.R].copy_(self.shards[p], non_blocking=True)
+            t.addmm(self.out, self.q, self.kall.T, beta=0, alpha=self.scale, out=self.out)
+        return fn, "copy-engine gather of the 7 peer K shards + cuBLAS (virtual peers)"
+
+    def cublas(self):
+        k = self.t.cat(self.shards)
+        return lambda: self.t.addmm(self.out, self.q, k.T, beta=0, alpha=self.scale, out=self.out)
+
+    def kernel(self, runtime):
+        k = self.t.cat(self.shards)
+        return lambda: runtime.gemm_bf16(self.q, k, self.out, alpha=self.scale), "hbm", self.out_bytes
+
+    def check(self):
+        k = self.t.cat(self.shards)
+        ref = (self.q[:256].float() @ k.float().T) * self.scale
+        return bool(self.t.allclose(self.out[:256].float(), ref, rtol=1.6e-2, atol=1e-2))
+
+    def e2e(self, grp, kind):
+        t = self.t
+        host_q = self.q.cpu().pin_memory()
+        host_k = self.shards[0].cpu().pin_memory()
+        host_s = t.empty(self.Tq, self.Tkv, dtype=t.bfloat16).pin_memory()
+        dq, dk = t.empty_like(self.q), t.empty_like(self.shards[0])
+
+        def fn():
+            dq.copy_(host_q, non_blocking=True)
+            dk.copy_(host_k, non_blocking=True)
+            self.ops.cp_kv_all_gather_qk(dq, dk, kind=kind, group=grp, out=self.out)
+            host_s.copy_(self.out, non_blocking=True)
+        return fn, (self.Tq + self.R) * self.d * 2, self.out_bytes
+
+    def ideal_us(self, peaks):
+        t_hbm = (self.out_bytes + (self.Tq + self.Tkv) * self.d * 2) / (peaks["hbm_gbs"] * 1e9)
+        t_gemm = max(self.flops / (peaks["bf16_tflops"] * 1e12), t_hbm)
+        return max(t_gemm, self.comm_bytes / NVLINK_NOMINAL) * 1e6
+
+    def cpu_sample(self, orc, kind):
+        q = self.q[:512].float().cpu().numpy()
+        k = self.t.cat(self.shards).float().cpu().numpy()
+        t0 = time.perf_counter()
+        (q @ k.T) * self.scale
+        per_op = (time.perf_counter() - t0) * (self.Tq / 512)
+        return per_op, f"numpy fp32 scores for 512 of {self.Tq} queries, scaled linearly"
+
+
+WORKLOADS = {"c2": AGWorkload, "c3": RSWorkload, "c4": CPWorkload}
+
+
 def our_arm(args) -> None:
     import torch
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        torch.distributed.init_process_group("nccl", device_id=dev)
     from oracle import ficco_oracle as orc  # checker + CPU baseline only
     from paper_2512_10236_b200 import ops, routing, runtime
     from paper_2512_10236_b200.machines import b200_machine
     from paper_2512_10236_b200.selector import select_schedule
     runtime.load_library()
 
-    G = G_CFG if world == 1 else world
-    R = M_ROWS // G
+    G = G_VIRTUAL if world == 1 else world
     peaks, peaks_src = load_peaks()
-    torch.manual_seed(0)
-    gen = torch.Generator(device=dev).manual_seed(1000 * 0 + rank)
-    shards = [(torch.rand(R, K_DIM, generator=gen, device=dev) * 2 - 1).to(torch.bfloat16) for _ in range(G)]
-    wgen = torch.Generator(device=dev).manual_seed(99)
-    weight = (torch.randn(N_COLS, K_DIM, generator=wgen, device=dev) / math.sqrt(K_DIM)).to(torch.bfloat16)
-    if world > 1:
-        grp = ops.FiccoGroup.distributed()
-        my = shards[0]
-    else:
-        grp = ops.FiccoGroup.virtual_group(G, 0)
-        my = shards[0]
-    out = torch.empty(M_ROWS, N_COLS, dtype=torch.bfloat16, device=dev)
+    wl = WORKLOADS[args.workload](torch, dev, G, rank, world, ops)
+    grp = ops.FiccoGroup.distributed() if world > 1 else ops.FiccoGroup.virtual_group(G, 0)
     flush_buf = torch.empty(256 * 2**20, dtype=torch.uint8, device=dev)
     flush = lambda: flush_buf.fill_(1)  # noqa: E731
     stream = torch.cuda.current_stream()
-    barrier = (lambda: __import__("torch.distributed").distributed.barrier()) if world > 1 else None
+    barrier = (lambda: torch.distributed.barrier()) if world > 1 else None
 
     def maxrank(ms: float) -> float:
         if world == 1:
@@ -176,168 +428,108 @@ def our_arm(args) -> None:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return float(t.item())
 
-    # ---- every schedule of the design space
+    # every schedule of the design space
     sched = {}
-    for kind in KINDS:
+    for kind in (args.kinds.split(",") if args.kinds else wl.kinds):
         try:
-            _, low, _ = ops.prepare_ag(grp, R, K_DIM, N_COLS, kind)
+            wl.prepare(grp, kind)
         except routing.PlanError as exc:
             sched[kind] = {"error": str(exc)}
             continue
-        if world == 1:
-            grp.load_peer_shards(low, shards)
-        fn = lambda k=kind: ops.all_gather_matmul(my, weight, kind=k, group=grp, out=out)  # noqa: E731
-        ts = time_steps(fn, args.steps, args.warmup, flush, stream, barrier)
+        ts = time_steps(wl.step(grp, kind), args.steps, args.warmup, flush, stream, barrier)
         grp.comm.check()
         sched[kind] = {"us": maxrank(statistics.median(ts)) * 1e3, "mean_us": maxrank(statistics.mean(ts)) * 1e3}
-
-    # correctness spot-check of the headline path against the oracle (rank 0 rows of the best kind)
     best = min((k for k in sched if "us" in sched[k] and k != "serial"), key=lambda k: sched[k]["us"])
-    ops.all_gather_matmul(my, weight, kind=best, group=grp, out=out)
+    wl.prepare(grp, best)
+    wl.step(grp, best)()
     grp.comm.check()
-    rows = slice(0, 256)
-    ref = (torch.cat(shards)[rows].float() @ weight.float().T) if world == 1 else None
-    parity = None
-    if ref is not None:
-        parity = bool(torch.allclose(out[rows].float(), ref, rtol=1.6e-2, atol=1e-2))
+    parity = wl.check() if world == 1 else None
 
-    # ---- serialized baseline: gather (NCCL all-gather / copy-engine copies) then cuBLAS
-    gathered = torch.empty(M_ROWS, K_DIM, dtype=torch.bfloat16, device=dev)
-    if world > 1:
-        def serial():
-            torch.distributed.all_gather_into_tensor(gathered, my)
-            torch.matmul(gathered, weight.T, out=out)
+    serial_fn, serial_desc = wl.serial()
+    serial_us = maxrank(statistics.median(time_steps(serial_fn, args.steps, args.warmup, flush, stream,
+                                                     barrier))) * 1e3
+    cublas_us = statistics.median(time_steps(wl.cublas(), args.steps, args.warmup, flush, stream)) * 1e3
+    kern_fn, bound, work = wl.kernel(runtime)
+    kern_us = statistics.median(time_steps(kern_fn, args.steps, args.warmup, flush, stream)) * 1e3
+    if bound == "tensor":
+        achieved, peak, unit = work / (kern_us * 1e-6) / 1e12, peaks["bf16_tflops"], "TFLOP/s"
     else:
-        def serial():
-            for p in range(G):
-                gathered[p * R:(p + 1) * R].copy_(shards[p], non_blocking=True)
-            torch.matmul(gathered, weight.T, out=out)
-    ts = time_steps(serial, args.steps, args.warmup, flush, stream, barrier)
-    serial_us = maxrank(statistics.median(ts)) * 1e3
+        achieved, peak, unit = work / (kern_us * 1e-6) / 1e9, peaks["hbm_gbs"], "GB/s"
 
-    # ---- dominant kernel alone (same tile kernel, no flags): roofline numerator
-    a_full = torch.cat(shards)
-    ker = lambda: runtime.gemm_bf16(a_full, weight, out)  # noqa: E731
-    kts = time_steps(ker, args.steps, args.warmup, flush, stream)
-    kern_ms = statistics.median(kts)
-    flops = 2.0 * M_ROWS * N_COLS * K_DIM
-    achieved_tf = flops / (kern_ms * 1e-3) / 1e12
-
-    # ---- clocks while the headline op runs back to back (~1.5 s)
-    with ClockSampler(local) as cs:
+    with ClockSampler(local) as cs:  # clocks while the headline op runs back to back (~1.5 s)
+        fn = wl.step(grp, best)
         t_end = time.time() + 1.5
         while time.time() < t_end:
-            for _ in range(20):
-                ops.all_gather_matmul(my, weight, kind=best, group=grp, out=out)
+            for _ in range(10):
+                fn()
             torch.cuda.synchronize()
     clocks = cs.summary()
 
-    # ---- e2e through the public API with host buffers (pinned): H2D of A_shard, D2H of C
-    host_a = my.cpu().pin_memory()
-    host_c = torch.empty(M_ROWS, N_COLS, dtype=torch.bfloat16).pin_memory()
-    dev_a = torch.empty_like(my)
+    e2e_fn, h2d, d2h = wl.e2e(grp, best)
+    e2e_us = maxrank(statistics.median(time_steps(e2e_fn, max(3, args.steps // 3), 3, flush, stream,
+                                                  barrier))) * 1e3
 
-    def e2e():
-        dev_a.copy_(host_a, non_blocking=True)
-        ops.all_gather_matmul(dev_a, weight, kind=best, group=grp, out=out)
-        host_c.copy_(out, non_blocking=True)
-    ets = time_steps(e2e, max(3, args.steps // 2), max(3, args.warmup // 2), flush, stream, barrier)
-    e2e_us = maxrank(statistics.median(ets)) * 1e3
-
-    # ---- CPU baseline: oracle port of one FiCCO step (1/G of the op) on host cores, extrapolated
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_sample(orc, shards, weight, best, G)
+        per_op, sample = wl.cpu_sample(orc, best)
+        cpu = {"value": round(per_op * 1e6, 1), "unit": "us", "cores": torch.get_num_threads(), "kind": "port",
+               "sample": sample}
 
-    selector_kind = select_schedule(ops._scenario("c2", M_ROWS, N_COLS, K_DIM, G), b200_machine().machine,
-                                    b200_machine().t_ref).value
+    b200 = b200_machine()
+    sc = ops._scenario(wl.key, *((wl.M, wl.N, wl.K) if hasattr(wl, "M") else (wl.Tkv, wl.Tq, wl.d)), G)
+    selector_kind = select_schedule(sc, b200.machine, b200.t_ref).value
     value = sched[best]["us"]
-    ingress = (G - 1) * R * K_DIM * 2
-    t_gemm = flops / (peaks["bf16_tflops"] * 1e12)
-    t_comm = ingress / NVLINK_NOMINAL
-    t_star = max(t_gemm, t_comm) * 1e6
+    t_star = wl.ideal_us(peaks)
     if rank == 0:
-        line = {
-            "metric": METRIC,
-            "value": round(value, 2),
-            "unit": "us",
-            "n_gpus": world,
-            "steps": args.steps,
-            "warmup": args.warmup,
-            "ms_per_step": round(value / 1e3, 5),
-            "higher_is_better": False,
-            "scaling": "weak",
-            "vs_baseline": None,
-            "dtype": "bf16",
-            "data": "synthetic (A ~ U(-1,1), W ~ N(0,1)/sqrt(K), seeded)",
-            "config": {"workload": "C2 Llama-3-8B TP/SP MLP up-proj AG->GEMM", "M": M_ROWS, "N": N_COLS,
-                       "K": K_DIM, "ranks": G, "virtual_peers": world == 1, "seq_len": M_ROWS,
-                       "schedule": best, "selector_schedule": selector_kind,
-                       "l2": "flushed (256 MiB write) between timed steps"},
-            "speedup_vs_serial": round(serial_us / value, 4),
-            "serial_us": round(serial_us, 2),
-            "serial_baseline": "NCCL all_gather_into_tensor + cuBLAS" if world > 1 else
-                               "copy-engine gather of 7 shards + cuBLAS (virtual peers)",
-            "ideal_overlap_us": round(t_star, 2),
-            "pct_ideal_overlap": round(t_star / value, 4),
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", f"r01_ncu_traffic_{wl.key}.json")) as f:
+                traffic = json.load(f).get("dram_bytes_per_launch")
+        except Exception:
+            pass
+        print(json.dumps({
+            "metric": METRIC, "value": round(value, 2), "unit": "us", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(value / 1e3, 5), "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded uniform/normal inputs of the config's shapes)",
+            "config": dict(workload=wl.title, ranks=G, virtual_peers=world == 1, schedule=best,
+                           selector_schedule=selector_kind, l2="flushed (256 MiB write) between timed steps",
+                           **wl.config()),
+            "speedup_vs_serial": round(serial_us / value, 4), "serial_us": round(serial_us, 2),
+            "serial_baseline": serial_desc, "cublas_gemm_us": round(cublas_us, 2),
+            "ideal_overlap_us": round(t_star, 2), "pct_ideal_overlap": round(t_star / value, 4),
             "schedules": {k: ({"us": round(v["us"], 2)} if "us" in v else v) for k, v in sched.items()},
             "parity_spot_check": parity,
-            "roofline": {"bound": "tensor", "achieved": round(achieved_tf, 1),
-                         "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
-                         "frac": round(achieved_tf / peaks["bf16_tflops"], 4), "traffic": None,
-                         "kernel": "ficco::tile_gemm_kernel", "kernel_us": round(kern_ms * 1e3, 2),
-                         "peak_source": f"MEASURED_PEAKS.json bf16_tflops (burst, {peaks_src})",
-                         "frac_of_sustained": round(achieved_tf / peaks.get("bf16_tflops_sustained", 1332.2), 4)},
+            "roofline": {"bound": bound, "achieved": round(achieved, 1), "peak": peak, "unit": unit,
+                         "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "kernel": "ficco::tile_gemm_kernel (flag-free run of the same tile program)",
+                         "kernel_us": round(kern_us, 2),
+                         "peak_source": f"MEASURED_PEAKS.json ({peaks_src}; burst figure, kernel timed alone)"},
             "cpu_baseline": cpu,
-            "e2e": {"value": round(e2e_us, 2), "unit": "us", "h2d_bytes_per_step": R * K_DIM * 2,
-                    "d2h_bytes_per_step": M_ROWS * N_COLS * 2},
+            "e2e": {"value": round(e2e_us, 2), "unit": "us", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": args.steps,
             "clocks": clocks,
-        }
-        print(json.dumps(line))
+        }))
     grp.close()
     if world > 1:
         torch.distributed.destroy_process_group()
 
 
-def cpu_sample(orc, shards, weight, kind, G):
-    import numpy as np
-    import torch
-    sh = [s.float().cpu().numpy() for s in shards]
-    w = weight.float().cpu().numpy()
-    orc.execute_ag_rank(kind, sh, w, 0, steps=1)  # warm-up
-    t0 = time.perf_counter()
-    reps = 0
-    while True:
-        orc.execute_ag_rank(kind, sh, w, 0, steps=1)
-        reps += 1
-        if time.perf_counter() - t0 > 10.0 or reps >= 5:
-            break
-    per_step = (time.perf_counter() - t0) / reps
-    frags = orc.gemm_fragments(kind, M_ROWS, K_DIM, G, 0)
-    rows_first = sum(c for rows, _ in frags[:1] for _, c in rows)
-    per_op = per_step * (M_ROWS / rows_first)
-    del np
-    return {"value": round(per_op * 1e6, 1), "unit": "us", "cores": torch.get_num_threads(), "kind": "port",
-            "sample": f"oracle execute_ag_rank({kind}) first GemmSpec ({rows_first} of {M_ROWS} rows) x{reps}, "
-                      f"scaled linearly to the full op"}
-
-
 def reference_arm(args) -> None:
+    """CPU restatement of the reference's path (the oracle port) on the host cores, C2 config."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    import numpy as np
     import torch
     from oracle import ficco_oracle as orc
-    G = G_CFG
-    R = M_ROWS // G
-    shards = [orc.seeded_inputs(0, p, (R, K_DIM)) for p in range(G)]
-    w = orc.seeded_inputs(0, 99, (N_COLS, K_DIM), "normal")
+    G, M, N, K = G_VIRTUAL, 8192, 3584, 4096
+    R = M // G
+    shards = [orc.seeded_inputs(0, p, (R, K)) for p in range(G)]
+    w = orc.seeded_inputs(0, 99, (N, K), "normal")
     kind = "uniform_fused_1d"
-    frags = orc.gemm_fragments(kind, M_ROWS, K_DIM, G, 0)
+    frags = orc.gemm_fragments(kind, M, K, G, 0)
     rows_first = sum(c for rows, _ in frags[:1] for _, c in rows)
-    scale = M_ROWS / rows_first
+    scale = M / rows_first
     for _ in range(max(1, min(args.warmup, 2))):
         orc.execute_ag_rank(kind, shards, w, 0, steps=1)
     times = []
@@ -346,19 +538,17 @@ def reference_arm(args) -> None:
         orc.execute_ag_rank(kind, shards, w, 0, steps=1)
         times.append((time.perf_counter() - t0) * scale)
     us = statistics.median(times) * 1e6
-    cores = torch.get_num_threads()
-    sample = (f"oracle port (numpy fp32 BLAS) of rank 0's {kind} op: first step ({rows_first}/{M_ROWS} rows) "
+    sample = (f"oracle port (numpy fp32 BLAS) of rank 0's {kind} AG->GEMM: first step ({rows_first}/{M} rows) "
               f"per timed step, scaled x{scale:g}")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(us, 1), "unit": "us", "n_gpus": world,
         "steps": len(times), "warmup": args.warmup, "ms_per_step": round(us / 1e3, 3), "higher_is_better": False,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "C2 Llama-3-8B TP/SP MLP up-proj AG->GEMM", "M": M_ROWS, "N": N_COLS, "K": K_DIM,
-                   "ranks": G, "schedule": kind},
-        "cpu_baseline": {"value": round(us, 1), "unit": "us", "cores": cores, "kind": "port", "sample": sample},
+        "config": {"workload": AGWorkload.title, "M": M, "N": N, "K": K, "ranks": G, "schedule": kind},
+        "cpu_baseline": {"value": round(us, 1), "unit": "us", "cores": torch.get_num_threads(), "kind": "port",
+                         "sample": sample},
         "e2e": {"value": round(us, 1), "unit": "us", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
-    del np
 
 
 def main() -> None:
@@ -367,10 +557,11 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ficco", choices=["ficco", "reference"])
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--kinds", default="", help="comma-separated subset of schedules")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
     args = ap.parse_args()
-    if args.warmup < 3:
-        args.warmup = 3
+    args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         reference_arm(args)
     else:

@@ -200,7 +200,8 @@ int ficco_plan_destroy(ficco_plan_t* plan);
 int ficco_plan_run(ficco_plan_t* plan, const void* a, const void* b, void* c, void* stream);
 /* Same semantics enqueued directly on streams (no graph); run_copies / run_tiles
  * select the halves (calibration of DIL/CIL; a tile half alone only terminates if
- * its flags are satisfied). */
+ * its flags are satisfied). run_tiles = 2: serialised — the kernel launches after
+ * the whole copy program (for kernel profilers that serialise work). */
 int ficco_plan_run_parts(ficco_plan_t* plan, const void* a, const void* b, void* c, void* stream,
                          int run_copies, int run_tiles);
 

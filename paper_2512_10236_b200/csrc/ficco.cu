@@ -88,6 +88,20 @@ int get_driver(Driver** out) {
   return 0;
 }
 
+// 32 x 32 bf16 store boxes with 64-byte swizzle (the epilogue's staging layout).
+int encode_store_map(Driver* drv, CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld) {
+  if (reinterpret_cast<uintptr_t>(base) % 16 != 0 || (ld * 2) % 16 != 0)
+    return fail(FICCO_EINVAL, "output not 16-byte aligned");
+  cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
+  cuuint64_t strides[1] = {cuuint64_t(ld * 2)};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CKD(drv->encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
+  return 0;
+}
+
 int encode_bf16_2d(Driver* drv, CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld,
                    int box_rows) {
   if (reinterpret_cast<uintptr_t>(base) % 16 != 0) return fail(FICCO_EINVAL, "operand base not 16-byte aligned");
@@ -165,6 +179,7 @@ struct ficco_plan {
   cudaGraphNode_t captured_kernel = nullptr;
   std::vector<std::pair<cudaGraphNode_t, int>> captured_copies;  // (node, op index) touching call arguments
   unsigned long long* trace = nullptr;  // optional device timeline buffer
+  bool concurrent = true;               // false: copies complete before the kernel starts (profilers)
   int tile_n = 256;                     // tile width (UMMA N)
   int cta_group = 1;                    // 1: one CTA per tile; 2: CTA pair (cluster of 2, UMMA M = 256)
   ficco_plan_desc desc{};
@@ -227,7 +242,8 @@ int enqueue_run(ficco_plan* p, uint32_t parity, const void* a, const void* b, vo
   const bool fork = copies && p->n_streams > 0;
   if (fork)
     for (int i = 0; i < p->n_streams; ++i) CK(cudaStreamWaitEvent(cm->copy[i], cm->ev_fork, 0));
-  if (tiles) {
+  const bool serialize = tiles && !p->concurrent;  // profiler mode: copies first, then the kernel
+  if (tiles && !serialize) {
     int r = launch(p, parity, a, b, c, s);
     if (r) return r;
   }
@@ -310,6 +326,10 @@ int enqueue_run(ficco_plan* p, uint32_t parity, const void* a, const void* b, vo
   }
   CK(cudaEventRecord(cm->ev_join[FICCO_MAX_STREAMS - 1], side));
   CK(cudaStreamWaitEvent(s, cm->ev_join[FICCO_MAX_STREAMS - 1], 0));
+  if (serialize) {
+    int r = launch(p, parity, a, b, c, s);
+    if (r) return r;
+  }
   return 0;
 }
 
@@ -347,6 +367,14 @@ int make_params(ficco_plan* p, uint32_t parity, const void* a, const void* b, vo
   if (d.part.buf != FICCO_BUF_NONE &&
       (r = resolve(cm, parity, d.part.buf, -1, d.part.off, d.part.par, a, b, c, &pp)))
     return r;
+  if (po && d.c.rows > 0) {
+    if ((r = encode_store_map(cm->drv, &prm->tmap_out, po, d.c.rows, d.c.ld, d.c.ld))) return r;
+    prm->has_out_map = 1;
+  }
+  if (pp && d.part.rows > 0) {
+    if ((r = encode_store_map(cm->drv, &prm->tmap_part, pp, d.part.rows, d.part.ld, d.part.ld))) return r;
+    prm->has_part_map = 1;
+  }
   prm->tiles = p->d_tiles;
   prm->num_tiles = p->n_tiles;
   prm->num_kb = int((d.k + ficco::BK - 1) / ficco::BK);
@@ -713,6 +741,7 @@ int ficco_plan_info(ficco_plan_t* p, int* n_tiles, int* grid, int* n_streams) {
 int ficco_plan_run_parts(ficco_plan_t* p, const void* a, const void* b, void* c, void* stream, int run_copies,
                          int run_tiles) {
   if (!p) return fail(FICCO_EINVAL, "null plan");
+  p->concurrent = run_tiles != 2;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const uint32_t parity = p->comm->runs & 1u;
   p->comm->runs += 1;

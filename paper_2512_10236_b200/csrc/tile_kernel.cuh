@@ -39,12 +39,17 @@ constexpr int BN_MAX = 256;  // widest tile (UMMA N <= 256); per-plan tile width
 constexpr int BK = 64;       // 64 bf16 = 128 B = one swizzle row
 constexpr int UMMA_K = 16;
 constexpr int A_STAGE = BM * BK * 2;  // 16 KiB
-constexpr int NUM_THREADS = 192;
-constexpr int EPI_THREADS = 128;
+constexpr int EPI_WARPS = 8;   // two epilogue warps per TMEM lane quarter (alternating 32-column chunks)
+constexpr int EPI_THREADS = EPI_WARPS * 32;
+constexpr int NUM_THREADS = 64 + EPI_THREADS;
 constexpr uint32_t TMEM_COLS = 512;  // two accumulators of up to 256 fp32 columns
 constexpr int MAX_RECV = 15;
 constexpr uint32_t SPIN_LIMIT = 1u << 25;  // ~4-10 s of polling before declaring a timeout
 constexpr int SMEM_LIMIT = 227 * 1024;
+// Epilogue output staging: per epilogue warp EPI_BUFS buffers of one 32 x 32 bf16 box
+// (64 B rows, TMA SWIZZLE_64B layout), stored with cp.async.bulk.tensor.
+constexpr int EPI_BUF_BYTES = 32 * 64;
+constexpr int EPI_BUFS = 2;
 
 // Per (tile width, CTA group) configuration: as many pipeline stages as fit.
 template <int TN, int CG>
@@ -54,9 +59,10 @@ struct TileCfg {
   static constexpr int B_ROWS = TN / CG;  // B rows loaded by each CTA
   static constexpr int B_STAGE = B_ROWS * BK * 2;
   static constexpr int STAGE = A_STAGE + B_STAGE;
-  static constexpr int MAX_STAGES = (SMEM_LIMIT - 1024 - 256) / STAGE;
+  static constexpr int EPI_STAGE_BYTES = EPI_BUFS * EPI_BUF_BYTES * EPI_WARPS;  // TMA-store staging
+  static constexpr int MAX_STAGES = (SMEM_LIMIT - 1024 - 256 - EPI_STAGE_BYTES) / STAGE;
   static constexpr int STAGES = MAX_STAGES > 8 ? 8 : MAX_STAGES;
-  static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE + 256;
+  static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE + EPI_STAGE_BYTES + 256;
 };
 
 struct alignas(64) TileParams {
@@ -64,6 +70,10 @@ struct alignas(64) TileParams {
   CUtensorMap tmap_b;
   CUtensorMap tmap_a2;  // alternate sources (e.g. the caller's local shard, read in place)
   CUtensorMap tmap_b2;
+  CUtensorMap tmap_out;   // 32 x 32 store boxes, SWIZZLE_64B (STORE / REDUCE destination)
+  CUtensorMap tmap_part;  // same for the STORE_SIGNAL destination
+  int has_out_map;
+  int has_part_map;
   const ficco_tile* tiles;
   int num_tiles;
   int num_kb;
@@ -191,12 +201,21 @@ __device__ __forceinline__ void mma_loop(const TileParams& p, uint8_t* sA, uint8
   }
 }
 
+// Byte offset of 16-byte chunk j of row t inside a 32-row x 64-byte TMA SWIZZLE_64B box
+// (Swizzle<2,4,3>: address bits [4,5] ^= bits [7,8]).
+__device__ __forceinline__ uint32_t swz64(uint32_t t, uint32_t j) { return t * 64u + ((j ^ ((t >> 1) & 3u)) << 4); }
+
 template <int TN, int CG>
 __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfull, uint64_t* tempty,
-                                              uint32_t tmem) {
+                                              uint32_t tmem, uint8_t* stage_smem) {
   const int warp = threadIdx.x / 32;
-  const int quarter = warp & 3;  // TMEM lane quarter this warp may access
-  const int row = quarter * 32 + (threadIdx.x & 31);
+  const int lane = threadIdx.x & 31;
+  const int quarter = warp & 3;           // TMEM lane quarter this warp may access
+  const int half = (warp - 2) / 4;        // which alternate 32-column chunks this warp drains
+  const int row = quarter * 32 + lane;
+  const uint64_t hint_out = policy_evict_first();  // results stream out; keep operands resident in L2
+  uint8_t* wbuf = stage_smem + (warp - 2) * (EPI_BUFS * EPI_BUF_BYTES);
+  uint32_t nbuf = 0;  // this warp's staging buffers used so far (ring of EPI_BUFS)
   uint32_t it = 0;
   for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
     const ficco_tile td = p.tiles[t];
@@ -213,48 +232,65 @@ __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfu
     tc_fence_after();
     const uint32_t taddr = tmem + (uint32_t(quarter * 32) << 16) + acc * BN_MAX;
     const bool row_ok = row < td.rows;
-    __nv_bfloat16* dst;
-    if (td.mode == FICCO_EPI_STORE_SIGNAL)
-      dst = p.part + int64_t(td.c_row + row) * p.ld_part + td.c_col;
-    else
-      dst = p.out + int64_t(td.c_row + row) * p.ld_out + td.c_col;
+    const bool signal = td.mode == FICCO_EPI_STORE_SIGNAL;
+    // whole 32-row warp boxes go out through TMA stores; ragged rows use direct stores
+    const int warp_rows = td.rows - quarter * 32;
+    const bool tma = warp_rows >= 32 && (signal ? p.has_part_map : p.has_out_map);
+    const CUtensorMap* map = signal ? &p.tmap_part : &p.tmap_out;
+    __nv_bfloat16* dst = signal ? p.part + int64_t(td.c_row + row) * p.ld_part + td.c_col
+                                : p.out + int64_t(td.c_row + row) * p.ld_out + td.c_col;
     const float scale = td.mode == FICCO_EPI_STORE ? p.alpha : 1.0f;
 #pragma unroll 1
-    for (int cc = 0; cc < TN / 32; ++cc) {
+    for (int cc = half; cc < TN / 32; cc += 2) {
       uint32_t v[32];
       tmem_ld_32x32b_x32(taddr + cc * 32, v);
       tmem_ld_wait();
-      if (row_ok && cc * 32 < td.cols) {
-        float f[32];
+      if (cc * 32 >= td.cols) continue;  // warp-uniform
+      float f[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]) * scale;
-        if (td.mode == FICCO_EPI_REDUCE) {
-          for (int j = 0; j < p.n_recv; ++j) {
-            const uint4* src = reinterpret_cast<const uint4*>(p.recv[j] + int64_t(td.recv_row + row) * p.ld_recv +
-                                                              td.c_col + cc * 32);
+      for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]) * scale;
+      if (td.mode == FICCO_EPI_REDUCE && row_ok) {
+        for (int j = 0; j < p.n_recv; ++j) {
+          const uint4* src = reinterpret_cast<const uint4*>(p.recv[j] + int64_t(td.recv_row + row) * p.ld_recv +
+                                                            td.c_col + cc * 32);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              uint4 w = __ldcs(src + q);
-              const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+          for (int q = 0; q < 4; ++q) {
+            uint4 w = __ldcs(src + q);
+            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                float2 x = __bfloat1622float2(h[e]);
-                f[q * 8 + 2 * e] += x.x;
-                f[q * 8 + 2 * e + 1] += x.y;
-              }
+            for (int e = 0; e < 4; ++e) {
+              float2 x = __bfloat1622float2(h[e]);
+              f[q * 8 + 2 * e] += x.x;
+              f[q * 8 + 2 * e + 1] += x.y;
             }
           }
         }
+      }
+      uint4 w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        w[q].x = pack_bf16x2(f[q * 8 + 0], f[q * 8 + 1]);
+        w[q].y = pack_bf16x2(f[q * 8 + 2], f[q * 8 + 3]);
+        w[q].z = pack_bf16x2(f[q * 8 + 4], f[q * 8 + 5]);
+        w[q].w = pack_bf16x2(f[q * 8 + 6], f[q * 8 + 7]);
+      }
+      if (tma) {
+        uint8_t* buf = wbuf + (nbuf % EPI_BUFS) * EPI_BUF_BYTES;
+        if (lane == 0 && nbuf >= EPI_BUFS) tma_store_wait_read<EPI_BUFS - 1>();  // buffer drained by its store
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 4; ++q) *reinterpret_cast<uint4*>(buf + swz64(lane, q)) = w[q];
+        fence_async_shared();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d_hint(map, buf, td.c_col + cc * 32, td.c_row + quarter * 32, hint_out);
+          tma_store_commit();
+        }
+        ++nbuf;
+      } else if (row_ok) {
         uint4* o = reinterpret_cast<uint4*>(dst + cc * 32);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint4 w;
-          w.x = pack_bf16x2(f[q * 8 + 0], f[q * 8 + 1]);
-          w.y = pack_bf16x2(f[q * 8 + 2], f[q * 8 + 3]);
-          w.z = pack_bf16x2(f[q * 8 + 4], f[q * 8 + 5]);
-          w.w = pack_bf16x2(f[q * 8 + 6], f[q * 8 + 7]);
-          o[q] = w;
-        }
+        for (int q = 0; q < 4; ++q) o[q] = w[q];
       }
     }
     tc_fence_before();
@@ -263,14 +299,16 @@ __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfu
     else
       mbar_arrive_leader(&tempty[acc]);  // the leader's MMA reuses the pair's accumulator
     if (p.trace && threadIdx.x == 64) p.trace[gridDim.x + 2 * t + 1] = globaltimer();
-    if (td.mode == FICCO_EPI_STORE_SIGNAL) {
-      named_bar_sync(1, EPI_THREADS);  // every row of the tile is stored
+    if (signal) {
+      if (lane == 0) tma_store_wait_all<0>();  // this warp's bulk stores are complete
+      named_bar_sync(1, EPI_THREADS);          // every row of the tile is stored
       if (threadIdx.x == 64) {
         __threadfence_system();
         red_release_add(p.counters + td.chunk, 1u);
       }
     }
   }
+  if (lane == 0) tma_store_wait_all<0>();  // staging smem must outlive the bulk stores
 }
 
 template <int TN, int CG>
@@ -280,7 +318,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tile_gemm_kernel(const __grid_
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = base;
   uint8_t* sB = base + Cfg::STAGES * A_STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + Cfg::STAGES * Cfg::B_STAGE);
+  uint8_t* sEpi = sB + Cfg::STAGES * Cfg::B_STAGE;  // 1024-aligned (stage sizes are multiples of 1 KiB)
+  uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + Cfg::EPI_STAGE_BYTES);
   uint64_t* empty = full + Cfg::STAGES;
   uint64_t* tfull = empty + Cfg::STAGES;
   uint64_t* tempty = tfull + 2;
@@ -295,6 +334,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tile_gemm_kernel(const __grid_
     tma_prefetch_desc(&p.tmap_b);
     tma_prefetch_desc(&p.tmap_a2);
     tma_prefetch_desc(&p.tmap_b2);
+    if (p.has_out_map) tma_prefetch_desc(&p.tmap_out);
+    if (p.has_part_map) tma_prefetch_desc(&p.tmap_part);
     for (int s = 0; s < Cfg::STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -324,7 +365,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tile_gemm_kernel(const __grid_
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) mma_loop<TN, CG>(p, sA, sB, full, empty, tfull, tempty, tmem);
   } else {
-    epilogue_loop<TN, CG>(p, tfull, tempty, tmem);
+    epilogue_loop<TN, CG>(p, tfull, tempty, tmem, sEpi);
   }
 
   tc_fence_before();

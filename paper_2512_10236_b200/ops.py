@@ -24,6 +24,7 @@ epoch) and caches lowered plans per (op, shape, kind). Two flavours:
 from __future__ import annotations
 
 import math
+import os
 
 import torch
 
@@ -33,6 +34,11 @@ from .machines import b200_machine
 from .routing import PlanError, ScheduleKind, build_plan
 from .runtime import FICCO_WS_DATA_OFFSET, Communicator, Plan
 from .selector import select_schedule
+
+
+# FICCO_SERIALIZE=1: run copy programs to completion before the tile kernel (kernel
+# profilers such as ncu serialise work, which would starve flag-gated tiles).
+SERIALIZE = os.environ.get("FICCO_SERIALIZE", "0") == "1"
 
 
 def _scenario(name: str, m: int, n: int, k: int, world: int, collective=Collective.ALL_GATHER) -> Scenario:
@@ -195,7 +201,10 @@ def all_gather_matmul(a_shard: torch.Tensor, weight: torch.Tensor, kind=None, gr
     plan, low, _ = prepare_ag(grp, R, K, N, kind)
     if out is None:
         out = torch.empty(M, N, dtype=torch.bfloat16, device=a_shard.device)
-    plan.run(a_shard, weight, out, stream)
+    if SERIALIZE:
+        plan.run_parts(a_shard, weight, out, stream, tiles=2)
+    else:
+        plan.run(a_shard, weight, out, stream)
     if return_gathered:
         par = (grp.comm.epoch() - 1) & 1  # parity of the run just enqueued
         gathered = grp.ws_tensor(grp.rank, low.gather_off + par * low.gather_par, (M, K))
@@ -212,7 +221,10 @@ def matmul_reduce_scatter(a: torch.Tensor, weight: torch.Tensor, kind=None, grou
     plan, _, _ = prepare_rs(grp, M, K, N, kind)
     if out is None:
         out = torch.empty(M // grp.world, N, dtype=torch.bfloat16, device=a.device)
-    plan.run(a, weight, out, stream)
+    if SERIALIZE:
+        plan.run_parts(a, weight, out, stream, tiles=2)
+    else:
+        plan.run(a, weight, out, stream)
     return out
 
 
@@ -228,5 +240,8 @@ def cp_kv_all_gather_qk(q: torch.Tensor, k_shard: torch.Tensor, kind=None, scale
     plan, _, _ = prepare_cp(grp, Tq, d, Tkv, kind, scale)
     if out is None:
         out = torch.empty(Tq, Tkv, dtype=torch.bfloat16, device=q.device)
-    plan.run(q, k_shard, out, stream)
+    if SERIALIZE:
+        plan.run_parts(q, k_shard, out, stream, tiles=2)
+    else:
+        plan.run(q, k_shard, out, stream)
     return out

@@ -276,8 +276,9 @@ class Plan:
         check(load_library().ficco_plan_run(C.c_void_p(self.handle), ptr(a), ptr(b), ptr(c),
                                             C.c_void_p(_stream_ptr(stream))))
 
-    def run_parts(self, a, b, c, stream=None, copies: bool = True, tiles: bool = True) -> None:
-        """The same run enqueued directly on streams (no graph); halves selectable."""
+    def run_parts(self, a, b, c, stream=None, copies: bool = True, tiles: bool | int = True) -> None:
+        """The same run enqueued directly on streams (no graph); halves selectable;
+        tiles=2 serialises (copies, then kernel) for profilers."""
         ptr = lambda t: C.c_void_p(0 if t is None else t.data_ptr())  # noqa: E731
         check(load_library().ficco_plan_run_parts(C.c_void_p(self.handle), ptr(a), ptr(b), ptr(c),
                                                   C.c_void_p(_stream_ptr(stream)), int(copies), int(tiles)))

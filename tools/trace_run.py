@@ -64,7 +64,7 @@ def main():
         done = [(tr[g + 2 * i + 1] - t0) / 1e3 for i in range(info["tiles"])]
         groups = {}
         for i, t in enumerate(low.tiles):
-            key = f"flag{t.flag}x{t.nflag}" + (f"/k{t.kseg}" if t.kseg else "")
+            key = f"flag{t.flag}m{t.fmask:x}" + (f"/k{t.kseg}" if t.kseg else "")
             groups.setdefault(key, []).append(i)
         per = {k: {"n": len(v), "ready_min": round(min(ready[i] for i in v), 1),
                    "ready_med": round(statistics.median(ready[i] for i in v), 1),
