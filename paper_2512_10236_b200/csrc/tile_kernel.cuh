@@ -45,7 +45,7 @@ constexpr int NUM_THREADS = 64 + EPI_THREADS;
 constexpr uint32_t TMEM_COLS = 512;  // two accumulators of up to 256 fp32 columns
 constexpr int MAX_RECV = 15;
 constexpr uint32_t SPIN_LIMIT = 1u << 25;  // ~4-10 s of polling before declaring a timeout
-constexpr int SMEM_LIMIT = 227 * 1024;
+constexpr int SMEM_LIMIT = 226 * 1024;  // leaves room for the static smem (seen-flag bitset)
 // Epilogue output staging: per epilogue warp EPI_BUFS buffers of one 32 x 32 bf16 box
 // (64 B rows, TMA SWIZZLE_64B layout), stored with cp.async.bulk.tensor.
 constexpr int EPI_BUF_BYTES = 32 * 64;
@@ -101,9 +101,11 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
-// Poll a flag written by another agent (copy engine memop, peer GPU) until it
-// reaches `epoch` (wrap-safe). On timeout raise the abort word and give up so
-// the kernel drains instead of hanging the device.
+// Poll a flag written by another agent (copy engine, peer GPU) until it reaches
+// `epoch` (wrap-safe) with acquire loads (a sys-scope fence per flag would cost
+// microseconds; the acquire load itself orders the following reads). On
+// timeout raise the abort word and give up so the kernel drains instead of
+// hanging the device.
 __device__ __forceinline__ void wait_flag(const uint32_t* f, uint32_t epoch, uint32_t* abort_word) {
   uint32_t spins = 0;
   while (static_cast<int32_t>(ld_acquire_sys(f) - epoch) < 0) {
@@ -118,9 +120,22 @@ __device__ __forceinline__ void wait_flag(const uint32_t* f, uint32_t epoch, uin
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
+// One-shot flags never go back to 0 within a run, so the (single-thread) producer
+// remembers which ones it has already seen: a tile gated by G-1 round flags costs
+// G-1 global polls only the first time, then a bit test per flag.
+constexpr int SEEN_WORDS = FICCO_FLAG_BLOCK / 32;
+
+__device__ __forceinline__ void wait_flag_cached(uint32_t* seen, const uint32_t* flags, int idx, uint32_t epoch,
+                                                 uint32_t* abort_word) {
+  const uint32_t bit = 1u << (idx & 31);
+  if (seen[idx >> 5] & bit) return;
+  wait_flag(flags + idx, epoch, abort_word);
+  seen[idx >> 5] |= bit;
+}
+
 template <int TN, int CG>
 __device__ __forceinline__ void producer_loop(const TileParams& p, uint8_t* sA, uint8_t* sB, uint64_t* full,
-                                              uint64_t* empty, uint32_t rank) {
+                                              uint64_t* empty, uint32_t rank, uint32_t* seen) {
   using Cfg = TileCfg<TN, CG>;
   const uint64_t hint_a = policy_evict_first();
   const uint64_t hint_b = policy_evict_last();
@@ -138,8 +153,14 @@ __device__ __forceinline__ void producer_loop(const TileParams& p, uint8_t* sA, 
         } else if (kb % td.kseg == 0) {
           base = td.flag + (kb / td.kseg) * td.kstride;
         }
-        if (base >= 0)
-          for (uint32_t m = td.fmask; m; m &= m - 1) wait_flag(p.flags + base + (__ffs(m) - 1), p.epoch, p.abort_word);
+        if (base >= 0) {
+          // fast path: every gating flag already observed (one 64-bit window test)
+          const uint32_t w0 = seen[base >> 5], w1 = (base >> 5) + 1 < SEEN_WORDS ? seen[(base >> 5) + 1] : 0u;
+          const uint32_t window = uint32_t(((uint64_t(w1) << 32) | w0) >> (base & 31));
+          if ((window & td.fmask) != td.fmask)
+            for (uint32_t m = td.fmask; m; m &= m - 1)
+              wait_flag_cached(seen, p.flags, base + (__ffs(m) - 1), p.epoch, p.abort_word);
+        }
       }
       if (kb == 0 && p.trace) p.trace[gridDim.x + 2 * t] = globaltimer();
       mbar_wait(&empty[stage], phase ^ 1u);
@@ -324,6 +345,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tile_gemm_kernel(const __grid_
   uint64_t* tfull = empty + Cfg::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  __shared__ uint32_t seen_flags[SEEN_WORDS];  // producer's record of flags already observed set
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
@@ -361,7 +383,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tile_gemm_kernel(const __grid_
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) producer_loop<TN, CG>(p, sA, sB, full, empty, rank);
+    if (lane == 0) {
+      for (int i = 0; i < SEEN_WORDS; ++i) seen_flags[i] = 0;
+      producer_loop<TN, CG>(p, sA, sB, full, empty, rank, seen_flags);
+    }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) mma_loop<TN, CG>(p, sA, sB, full, empty, tfull, tempty, tmem);
   } else {

@@ -336,11 +336,16 @@ def lower_ag(plan: ExecutionPlan, rank: int, gathered: str = "A", alpha: float =
         else:
             if count % 32:
                 raise PlanError(f"gathered-B fragments must be multiples of 32 rows, got {count}")
-            for n0 in range(start, start + count, tn):
-                cols = min(tn, start + count - n0)
-                for m0 in range(0, Q, TILE_M):
-                    tiles.append(_tile(m0, n0 - shift, m0, n0, min(TILE_M, Q - m0), cols, flag, fmask, ks, kstride,
-                                       b_src=int(local)))
+            # query-row-major inside the fragment: concurrently running tiles then write long
+            # contiguous row segments of the (HBM-bound) score matrix; 256-row steps keep CTA-pair
+            # partners (m0, m0 + 128) adjacent
+            step = TILE_M * cta_group
+            for mb in range(0, Q, step):
+                for n0 in range(start, start + count, tn):
+                    cols = min(tn, start + count - n0)
+                    for m0 in range(mb, min(Q, mb + step), TILE_M):
+                        tiles.append(_tile(m0, n0 - shift, m0, n0, min(TILE_M, Q - m0), cols, flag, fmask, ks,
+                                           kstride, b_src=int(local)))
 
     if cta_group == 2:
         low.tiles[:] = pair_tiles(low.tiles)

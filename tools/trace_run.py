@@ -18,21 +18,34 @@ from paper_2512_10236_b200 import ops, runtime  # noqa: E402
 
 
 def main():
-    M, N, K, G = 8192, 3584, 4096, 8
-    if len(sys.argv) > 1:
-        M, N, K, G = map(int, sys.argv[1:5])
+    cp = "--cp" in sys.argv
+    argv = [a for a in sys.argv[1:] if a != "--cp"]
+    M, N, K, G = (131072, 16384, 128, 8) if cp else (8192, 3584, 4096, 8)
+    if argv:
+        M, N, K, G = map(int, argv[:4])
     R = M // G
     runtime.load_library()
     gen = torch.Generator(device="cuda").manual_seed(0)
     shards = [(torch.rand(R, K, generator=gen, device="cuda") * 2 - 1).to(torch.bfloat16) for _ in range(G)]
     w = (torch.randn(N, K, generator=gen, device="cuda") / K ** 0.5).to(torch.bfloat16)
-    out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    out = torch.empty(N, M, dtype=torch.bfloat16, device="cuda") if cp else \
+        torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
     grp = ops.FiccoGroup.virtual_group(G, 0)
     res = {}
-    for kind in ["serial", "shard_overlap_p2p", "uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d",
-                 "uniform_fused_2d"]:
-        plan, low, _ = ops.prepare_ag(grp, R, K, N, kind)
+    kinds = ["serial", "shard_overlap_p2p", "uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d"]
+    if not cp:
+        kinds.append("uniform_fused_2d")
+    for kind in kinds:
+        if cp:
+            plan, low, _ = ops.prepare_cp(grp, N, K, M, kind)
+        else:
+            plan, low, _ = ops.prepare_ag(grp, R, K, N, kind)
         grp.load_peer_shards(low, shards)
+        def call(k, plan=plan):
+            if cp:
+                ops.cp_kv_all_gather_qk(w, shards[0], kind=k, group=grp, out=out)
+            else:
+                ops.all_gather_matmul(shards[0], w, kind=k, group=grp, out=out)
         info = plan.info()
         trace = torch.zeros(info["grid"] + 2 * info["tiles"], dtype=torch.int64, device="cuda")
         plan.set_trace(trace)
@@ -41,18 +54,18 @@ def main():
         for _ in range(10):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
-            plan.run_parts(shards[0], w, out)
+            plan.run_parts(w, shards[0], out) if cp else plan.run_parts(shards[0], w, out)
             b.record()
             b.synchronize()
             ts_stream.append(a.elapsed_time(b) * 1e3)
         for _ in range(5):
-            ops.all_gather_matmul(shards[0], w, kind=kind, group=grp, out=out)
+            call(kind)
         torch.cuda.synchronize()
         ts = []
         for _ in range(10):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
-            ops.all_gather_matmul(shards[0], w, kind=kind, group=grp, out=out)
+            call(kind)
             b.record()
             b.synchronize()
             ts.append(a.elapsed_time(b) * 1e3)
