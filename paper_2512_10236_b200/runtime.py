@@ -176,6 +176,17 @@ def ipc_close(ptr: int) -> None:
     check(load_library().ficco_ipc_close(C.c_void_p(ptr)))
 
 
+def exchange_handles(handle: bytes, group=None) -> list[bytes]:
+    """All ranks' workspace IPC handles in rank order (plain bytes; any torch.distributed backend)."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    handles: list = [None] * world
+    dist.all_gather_object(handles, bytes(handle), group=group)
+    if any(not isinstance(h, bytes) or len(h) != len(handle) for h in handles):
+        raise RuntimeError("workspace handle exchange returned malformed handles")
+    return handles
+
+
 class Communicator:
     """One rank's view of G symmetric workspaces (+ its copy stream and epoch).
 
@@ -208,8 +219,7 @@ class Communicator:
         import torch.distributed as dist
         rank, world = dist.get_rank(group), dist.get_world_size(group)
         mine = Workspace(nbytes)
-        handles: list = [None] * world
-        dist.all_gather_object(handles, mine.ipc_handle(), group=group)
+        handles = exchange_handles(mine.ipc_handle(), group)
         ptrs, opened = [], []
         for r, h in enumerate(handles):
             if r == rank:

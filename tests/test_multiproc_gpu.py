@@ -1,0 +1,99 @@
+"""Real multi-rank protocol on one B200: G processes share cuda:0.
+
+Each process is one rank of a G-rank job (torch.distributed over gloo for the
+handle exchange); symmetric workspaces are CUDA-IPC mapped across processes,
+so every cross-rank mechanism of the executor runs for real (publish / DONE
+barriers through peer memory, ring notifications, counter-gated pushes into
+peers' receive slots, one-shot parity flags across consecutive calls) — the
+parts the single-process virtual mode skips.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+AG_KINDS = ["serial", "shard_overlap_p2p", "uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d",
+            "uniform_fused_2d"]
+RS_KINDS = ["uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d"]
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    import math
+    import sys
+    import traceback
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+    from oracle import ficco_oracle as orc
+    from paper_2512_10236_b200 import ops
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    errors = []
+    try:
+        grp = ops.FiccoGroup.distributed()
+        t = lambda x: torch.from_numpy(x).to(torch.bfloat16).cuda()  # noqa: E731
+        R, K, N = 256, 512, 256
+        w = orc.seeded_inputs(1, 99, (N, K), "normal")
+        for kind in AG_KINDS:
+            for call in range(3):  # consecutive calls: both parities, flag reuse
+                shards = [orc.seeded_inputs(10 * call + 1, g, (R, K)) for g in range(world)]
+                out, gathered = ops.all_gather_matmul(t(shards[rank]), t(w), kind=kind, group=grp,
+                                                      return_gathered=True)
+                grp.comm.check()
+                full = np.concatenate(shards)
+                if not np.array_equal(gathered.float().cpu().numpy(), full):
+                    errors.append(f"AG {kind} call {call}: gathered buffer differs")
+                if not np.allclose(out.float().cpu().numpy(), full @ w.T, rtol=1.6e-2, atol=1e-2):
+                    errors.append(f"AG {kind} call {call}: output differs")
+        M, Kg, N2 = 64 * world * world, 256, 256
+        for kind in RS_KINDS:
+            for call in range(3):
+                a = [orc.seeded_inputs(20 + call, g, (M, Kg)) for g in range(world)]
+                ws = [orc.seeded_inputs(30 + call, g, (N2, Kg), "normal") for g in range(world)]
+                want = orc.execute_rs(a, ws)[rank]
+                out = ops.matmul_reduce_scatter(t(a[rank]), t(ws[rank]), kind=kind, group=grp)
+                grp.comm.check()
+                if not np.allclose(out.float().cpu().numpy(), want, rtol=1.6e-2, atol=1e-2 * math.sqrt(world)):
+                    errors.append(f"RS {kind} call {call}: output differs")
+        d, Tq, Tkv = 128, 256, 512 * world
+        q = orc.seeded_inputs(40, 7, (Tq, d), "normal")
+        for kind in ["hetero_unfused_1d", "shard_overlap_p2p"]:
+            ks = [orc.seeded_inputs(41, g, (Tkv // world, d), "normal") for g in range(world)]
+            want, _ = orc.execute_cp_qk(q, ks, 1.0 / math.sqrt(d))
+            out = ops.cp_kv_all_gather_qk(t(q), t(ks[rank]), kind=kind, group=grp)
+            grp.comm.check()
+            if not np.allclose(out.float().cpu().numpy(), want, rtol=1.6e-2, atol=1e-2):
+                errors.append(f"CP {kind}: output differs")
+        dist.barrier()
+        grp.close()
+    except Exception:
+        errors.append(traceback.format_exc())
+    q.put((rank, errors))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_ranks_sharing_one_gpu(world):
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+    for r in range(world):
+        assert results[r] == [], f"rank {r}: {results[r]}"
