@@ -47,6 +47,7 @@ def _worker(rank, world, port, q):
         R, K, N = 256, 512, 256
         w = orc.seeded_inputs(1, 99, (N, K), "normal")
         for kind in AG_KINDS:
+            print(f"rank {rank}: AG {kind}", flush=True)
             for call in range(3):  # consecutive calls: both parities, flag reuse
                 shards = [orc.seeded_inputs(10 * call + 1, g, (R, K)) for g in range(world)]
                 out, gathered = ops.all_gather_matmul(t(shards[rank]), t(w), kind=kind, group=grp,
@@ -59,6 +60,7 @@ def _worker(rank, world, port, q):
                     errors.append(f"AG {kind} call {call}: output differs")
         M, Kg, N2 = 64 * world * world, 256, 256
         for kind in RS_KINDS:
+            print(f"rank {rank}: RS {kind}", flush=True)
             for call in range(3):
                 a = [orc.seeded_inputs(20 + call, g, (M, Kg)) for g in range(world)]
                 ws = [orc.seeded_inputs(30 + call, g, (N2, Kg), "normal") for g in range(world)]
@@ -68,11 +70,12 @@ def _worker(rank, world, port, q):
                 if not np.allclose(out.float().cpu().numpy(), want, rtol=1.6e-2, atol=1e-2 * math.sqrt(world)):
                     errors.append(f"RS {kind} call {call}: output differs")
         d, Tq, Tkv = 128, 256, 512 * world
-        q = orc.seeded_inputs(40, 7, (Tq, d), "normal")
+        qm = orc.seeded_inputs(40, 7, (Tq, d), "normal")
         for kind in ["hetero_unfused_1d", "shard_overlap_p2p"]:
+            print(f"rank {rank}: CP {kind}", flush=True)
             ks = [orc.seeded_inputs(41, g, (Tkv // world, d), "normal") for g in range(world)]
-            want, _ = orc.execute_cp_qk(q, ks, 1.0 / math.sqrt(d))
-            out = ops.cp_kv_all_gather_qk(t(q), t(ks[rank]), kind=kind, group=grp)
+            want, _ = orc.execute_cp_qk(qm, ks, 1.0 / math.sqrt(d))
+            out = ops.cp_kv_all_gather_qk(t(qm), t(ks[rank]), kind=kind, group=grp)
             grp.comm.check()
             if not np.allclose(out.float().cpu().numpy(), want, rtol=1.6e-2, atol=1e-2):
                 errors.append(f"CP {kind}: output differs")
@@ -92,8 +95,15 @@ def test_ranks_sharing_one_gpu(world):
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    results = dict(q.get(timeout=600) for _ in range(world))
-    for p in procs:
-        p.join(timeout=120)
+    results = {}
+    try:
+        for _ in range(world):
+            r, errs = q.get(timeout=240)
+            results[r] = errs
+    finally:
+        for p in procs:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
     for r in range(world):
-        assert results[r] == [], f"rank {r}: {results[r]}"
+        assert results.get(r) == [], f"rank {r}: {results.get(r, 'no result (hung or crashed)')}"
