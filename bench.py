@@ -138,6 +138,8 @@ def time_steps(fn, steps: int, warmup: int, flush, stream, barrier=None) -> list
 class AGWorkload:
     """C2: all-gather -> GEMM (TP/SP up-projection)."""
 
+    inplace = False
+
     key = "c2"
     title = "C2 Llama-3-8B TP/SP MLP up-proj AG->GEMM"
     kinds = ["uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d", "uniform_fused_2d", "shard_overlap_p2p",
@@ -164,8 +166,17 @@ class AGWorkload:
         _, low, _ = self.ops.prepare_ag(grp, self.R, self.K, self.N, kind)
         if grp.virtual:
             grp.load_peer_shards(low, self.shards)
+        if self.inplace:  # the shard already sits in this rank's workspace slot, both parities
+            for par in (0, 1):
+                off = low.gather_off + par * low.gather_par + grp.rank * self.R * self.K * 2
+                grp.ws_tensor(grp.rank, off, (self.R, self.K)).copy_(self.shards[0])
 
     def step(self, grp, kind):
+        if self.inplace:
+            def fn():
+                a = grp.input_slot(self.R, self.K, self.N, kind)
+                self.ops.all_gather_matmul(a, self.w, kind=kind, group=grp, out=self.out)
+            return fn
         return lambda: self.ops.all_gather_matmul(self.shards[0], self.w, kind=kind, group=grp, out=self.out)
 
     def serial(self):
@@ -415,6 +426,7 @@ def our_arm(args) -> None:
     G = G_VIRTUAL if world == 1 else world
     peaks, peaks_src = load_peaks()
     wl = WORKLOADS[args.workload](torch, dev, G, rank, world, ops)
+    wl.inplace = args.input == "slot" and hasattr(wl, "shards") and args.workload == "c2"
     grp = ops.FiccoGroup.distributed() if world > 1 else ops.FiccoGroup.virtual_group(G, 0)
     flush_buf = torch.empty(256 * 2**20, dtype=torch.uint8, device=dev)
     flush = lambda: flush_buf.fill_(1)  # noqa: E731
@@ -493,6 +505,7 @@ def our_arm(args) -> None:
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded uniform/normal inputs of the config's shapes)",
             "config": dict(workload=wl.title, ranks=G, virtual_peers=world == 1, schedule=best,
+                           input="symmetric slot (zero-copy publish)" if wl.inplace else "tensor copied in",
                            selector_schedule=selector_kind, l2="flushed (256 MiB write) between timed steps",
                            **wl.config()),
             "speedup_vs_serial": round(serial_us / value, 4), "serial_us": round(serial_us, 2),
@@ -560,6 +573,9 @@ def main() -> None:
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--kinds", default="", help="comma-separated subset of schedules")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
+    ap.add_argument("--input", default="slot", choices=["slot", "copy"],
+                    help="slot: the A shard is produced in the group's symmetric input slot (zero-copy publish, "
+                         "FiccoGroup.input_slot); copy: an ordinary tensor copied in by the op")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

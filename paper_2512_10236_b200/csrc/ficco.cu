@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -180,6 +181,11 @@ struct ficco_plan {
   std::vector<std::pair<cudaGraphNode_t, int>> captured_copies;  // (node, op index) touching call arguments
   unsigned long long* trace = nullptr;  // optional device timeline buffer
   bool concurrent = true;               // false: copies complete before the kernel starts (profilers)
+  // The tile kernel is a node of the run's graph (default). FICCO_KERNEL_IN_GRAPH=0 launches
+  // it directly next to a copy-only graph instead — measured no faster, and unsafe: a blocked
+  // stream-wait node (RS counter / barrier) can share a hardware queue with the direct launch,
+  // so the kernel that would satisfy the wait never starts.
+  bool kernel_in_graph = true;
   int tile_n = 256;                     // tile width (UMMA N)
   int cta_group = 1;                    // 1: one CTA per tile; 2: CTA pair (cluster of 2, UMMA M = 256)
   ficco_plan_desc desc{};
@@ -444,7 +450,7 @@ int build_graph(ficco_plan* p, uint32_t parity, const void* a, const void* b, vo
   CK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
   p->captured_kernel = nullptr;
   p->captured_copies.clear();
-  int r = enqueue_run(p, parity, a, b, c, cap, true, true, launch_tiles);
+  int r = enqueue_run(p, parity, a, b, c, cap, true, p->kernel_in_graph, launch_tiles);
   cudaGraph_t graph = nullptr;
   cudaError_t e = cudaStreamEndCapture(cap, &graph);
   cudaStreamDestroy(cap);
@@ -457,7 +463,7 @@ int build_graph(ficco_plan* p, uint32_t parity, const void* a, const void* b, vo
   gi.user_copies = p->captured_copies;
   p->captured_kernel = nullptr;
   p->captured_copies.clear();
-  if (p->n_tiles > 0 && !gi.kernel) {
+  if (p->kernel_in_graph && p->n_tiles > 0 && !gi.kernel) {
     cudaGraphDestroy(graph);
     return fail(FICCO_ECUDA, "graph capture: kernel node not found");
   }
@@ -689,6 +695,10 @@ int ficco_plan_create(ficco_comm_t* c, const ficco_plan_desc* d, ficco_plan_t** 
   p->n_tiles = d->n_tiles;
   p->tile_n = tile_n;
   p->cta_group = cta_group;
+  {
+    const char* env = getenv("FICCO_KERNEL_IN_GRAPH");
+    p->kernel_in_graph = !(env && env[0] == '0');
+  }
   if (cta_group == 2 && p->desc.grid % 2) p->desc.grid = p->desc.grid > 1 ? p->desc.grid - 1 : 2;  // whole pairs
   p->n_streams = n_streams;
   p->user_copies = user;
@@ -757,10 +767,21 @@ int ficco_plan_run(ficco_plan_t* p, const void* a, const void* b, void* c, void*
   if (!gi.exec) {
     if ((r = build_graph(p, parity, a, b, c, s))) return r;
   } else if (gi.a != a || gi.b != b || gi.c != c) {
-    if ((r = repoint_graph(p, parity, a, b, c))) return r;
+    if ((r = repoint_graph(p, parity, a, b, c))) return r;  // user-buffer copy nodes (+ kernel node)
   }
   p->comm->runs += 1;
-  CK(cudaGraphLaunch(gi.exec, s));
+  if (p->kernel_in_graph) {
+    CK(cudaGraphLaunch(gi.exec, s));
+    return 0;
+  }
+  ficco_comm* cm = p->comm;
+  cudaStream_t gs = cm->copy[FICCO_MAX_STREAMS - 1];  // graph launch stream (idle between runs)
+  CK(cudaEventRecord(cm->ev_fork, s));
+  CK(cudaStreamWaitEvent(gs, cm->ev_fork, 0));
+  CK(cudaGraphLaunch(gi.exec, gs));
+  if ((r = launch_tiles(p, parity, a, b, c, s))) return r;
+  CK(cudaEventRecord(cm->ev_join[0], gs));
+  CK(cudaStreamWaitEvent(s, cm->ev_join[0], 0));
   return 0;
 }
 

@@ -171,7 +171,7 @@ def _my_gemms(plan: ExecutionPlan, rank: int) -> list[GemmSpec]:
 
 
 def _publish(ops: list, g: int, world: int, row_bytes: int, shard_rows: int, gather_off: int, par: int,
-             src_buf: int) -> None:
+             src_buf: int, inplace: bool = False) -> None:
     """Local shard -> own slot of the gathered buffer (stream 0), then the publish barrier.
 
     The tile kernel reads the local rows in place from the call argument (the
@@ -180,8 +180,10 @@ def _publish(ops: list, g: int, world: int, row_bytes: int, shard_rows: int, gat
     cross-rank barrier (each rank sets its byte in everyone's PUB word and waits
     for all bytes) and records EV_START, which every pull chain waits on.
     """
-    ops.append(_op(OP_COPY, src_buf=src_buf, dst_buf=BUF_WS, src_off=0, dst_off=gather_off + g * shard_rows * row_bytes,
-                   dst_par=par, width=shard_rows * row_bytes, stream=0))
+    if not inplace:  # in-place inputs already sit in the slot (see FiccoGroup.input_slot)
+        ops.append(_op(OP_COPY, src_buf=src_buf, dst_buf=BUF_WS, src_off=0,
+                       dst_off=gather_off + g * shard_rows * row_bytes, dst_par=par,
+                       width=shard_rows * row_bytes, stream=0))
     ops.append(_op(OP_BARRIER, flag=F_PUB, stream=0))
     ops.append(_op(OP_RECORD, value=EV_START, stream=0))
 
@@ -192,7 +194,7 @@ def _peer_stream(p: int, g: int) -> int:
 
 
 def lower_ag(plan: ExecutionPlan, rank: int, gathered: str = "A", alpha: float = 1.0, grid: int = 0,
-             other_rows: int | None = None, cta_group: int = DEFAULT_CTA_GROUP) -> Lowered:
+             other_rows: int | None = None, cta_group: int = DEFAULT_CTA_GROUP, inplace: bool = False) -> Lowered:
     """All-gather -> GEMM family (AG->GEMM and the CP KV-gather -> QK^T).
 
     gathered="A": C[M,N] = A_all[M,K] @ W[N,K]^T; call args (a=A_shard[R,K], b=W, c=C).
@@ -220,7 +222,7 @@ def lower_ag(plan: ExecutionPlan, rank: int, gathered: str = "A", alpha: float =
     src_buf = BUF_A if gathered == "A" else BUF_B
     if G > MAX_WORLD:
         raise PlanError(f"at most {MAX_WORLD} ranks")
-    _publish(ops, g, G, row_bytes, R, low.gather_off, low.gather_par, src_buf)
+    _publish(ops, g, G, row_bytes, R, low.gather_off, low.gather_par, src_buf, inplace)
 
     def pull(p: int, row0: int, nrows: int, stream: int) -> CopyOp:
         off = low.gather_off + row0 * row_bytes
@@ -351,16 +353,18 @@ def lower_ag(plan: ExecutionPlan, rank: int, gathered: str = "A", alpha: float =
         low.tiles[:] = pair_tiles(low.tiles)
     d = low.desc
     gat = _operand(BUF_WS, M, K, low.gather_off, low.gather_par)
+    # local rows: read in place from the call argument, or from the own slot for in-place inputs
+    own = _operand(BUF_WS, R, K, low.gather_off + g * R * row_bytes, low.gather_par) if inplace else None
     if gathered == "A":
         d.a, d.b, d.c = gat, _operand(BUF_B, N, K), _operand(BUF_C, M, N)
-        d.a2, d.b2 = _operand(BUF_A, R, K), _operand(BUF_NONE, 0, 0)
+        d.a2, d.b2 = own or _operand(BUF_A, R, K), _operand(BUF_NONE, 0, 0)
     else:
         d.a, d.b, d.c = _operand(BUF_A, Q, K), gat, _operand(BUF_C, Q, M)
-        d.a2, d.b2 = _operand(BUF_NONE, 0, 0), _operand(BUF_B, R, K)
+        d.a2, d.b2 = _operand(BUF_NONE, 0, 0), own or _operand(BUF_B, R, K)
     d.part = _operand(BUF_NONE, 0, 0)
     d.recv = _operand(BUF_NONE, 0, 0)
     d.k, d.alpha, d.grid, d.tile_n, d.cta_group = K, alpha, grid, tn, cta_group
-    low.notes = {"kind": kind.value, "rank": g, "world": G, "gathered": gathered}
+    low.notes = {"kind": kind.value, "rank": g, "world": G, "gathered": gathered, "inplace": inplace}
     return low
 
 

@@ -103,6 +103,19 @@ class FiccoGroup:
         ptr = self.comm.ws_ptrs[rank] + offset
         return _wrap_device_ptr(ptr, shape, dtype)
 
+    def input_slot(self, rows: int, cols: int, n_out: int, kind=None) -> torch.Tensor:
+        """This rank's slot of the gathered buffer for the NEXT all_gather_matmul call.
+
+        Writing the shard here (e.g. as the producing layer's output) and passing
+        the view as ``a_shard`` skips the local publish copy: peers pull it
+        straight from the slot. The slot alternates between calls (workspace
+        parity), so ask for it before every call.
+        """
+        _, low, _ = prepare_ag(self, rows, cols, n_out, kind)
+        par = self.comm.epoch() & 1
+        off = low.gather_off + par * low.gather_par + self.rank * rows * cols * 2
+        return self.ws_tensor(self.rank, off, (rows, cols))
+
     def close(self) -> None:
         self._plans.clear()
         if self.comm is not None:
@@ -158,13 +171,24 @@ def _default_group(group, world):
     raise ValueError("pass a FiccoGroup (FiccoGroup.distributed(pg) or FiccoGroup.virtual_group(world, rank))")
 
 
-def prepare_ag(grp: FiccoGroup, R: int, K: int, N: int, kind=None):
+def prepare_ag(grp: FiccoGroup, R: int, K: int, N: int, kind=None, inplace: bool = False):
     """Build (or fetch) the lowered AG->GEMM plan for this rank: (plan, lowered, kind)."""
     M = R * grp.world
     sc = _scenario("ag_gemm", M, N, K, grp.world)
     kd = choose_kind(sc, kind)
-    plan, low = grp.plan(("ag", M, N, K, kd), lambda: lower_ag(build_plan(sc, kd), grp.rank, "A"))
+    plan, low = grp.plan(("ag", M, N, K, kd, inplace),
+                         lambda: lower_ag(build_plan(sc, kd), grp.rank, "A", inplace=inplace))
     return plan, low, kd
+
+
+def _is_slot(grp: FiccoGroup, t: torch.Tensor, low) -> bool:
+    """Is ``t`` this rank's slot of the gathered buffer for the next call's parity?"""
+    if grp.comm is None or not t.is_contiguous():
+        return False
+    par = grp.comm.epoch() & 1
+    rows, cols = t.shape
+    want = grp.comm.local_ws + low.gather_off + par * low.gather_par + grp.rank * rows * cols * 2
+    return t.data_ptr() == want
 
 
 def prepare_rs(grp: FiccoGroup, M: int, K: int, N: int, kind=None):
@@ -198,7 +222,9 @@ def all_gather_matmul(a_shard: torch.Tensor, weight: torch.Tensor, kind=None, gr
     R, K = a_shard.shape
     N = weight.shape[0]
     M = R * grp.world
-    plan, low, _ = prepare_ag(grp, R, K, N, kind)
+    plan, low, kd = prepare_ag(grp, R, K, N, kind)
+    if _is_slot(grp, a_shard, low):  # zero-copy publish: the shard already sits in its slot
+        plan, low, _ = prepare_ag(grp, R, K, N, kd, inplace=True)
     if out is None:
         out = torch.empty(M, N, dtype=torch.bfloat16, device=a_shard.device)
     if SERIALIZE:

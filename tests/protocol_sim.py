@@ -165,8 +165,13 @@ class World:
     def on_run_done(self, rank: int, run: int) -> None:  # hook for checks
         pass
 
+    def on_run_start(self, rank: int, run: int) -> None:  # hook: caller work stream-ordered before the call
+        pass
+
     def _start(self, g: int, st: dict) -> None:
         st["run"] += 1
+        if st["run"] < len(self.args):
+            self.on_run_start(g, st["run"])
         low = self.low[g]
         streams: dict[int, list] = {}
         for op in low.ops:

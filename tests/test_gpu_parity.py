@@ -139,3 +139,27 @@ def test_cp_qk_virtual_matches_oracle(lib, kind):
             np.testing.assert_allclose(_np(out), want, rtol=RTOL, atol=ATOL)
     finally:
         grp.close()
+
+
+@pytest.mark.parametrize("kind", ["shard_overlap_p2p", "hetero_unfused_1d", "uniform_fused_2d"])
+def test_ag_input_slot_zero_copy(lib, kind):
+    """Inputs produced directly in the group's symmetric slot skip the publish copy."""
+    from paper_2512_10236_b200 import ops
+    G, rank, R, K, N = 4, 2, 256, 512, 256
+    w = orc.seeded_inputs(0, 99, (N, K), "normal")
+    grp = ops.FiccoGroup.virtual_group(G, rank)
+    try:
+        for call in range(3):
+            shards = [orc.seeded_inputs(call, p, (R, K)) for p in range(G)]
+            _, low, _ = ops.prepare_ag(grp, R, K, N, kind)
+            grp.load_peer_shards(low, [_t(s) for s in shards])
+            slot = grp.input_slot(R, K, N, kind)
+            slot.copy_(_t(shards[rank]))
+            out, gathered = ops.all_gather_matmul(slot, _t(w), kind=kind, group=grp, return_gathered=True)
+            grp.comm.check()
+            assert ("ag", R * G, N, K, ops.ScheduleKind(kind), True) in grp._plans  # the in-place plan ran
+            full = np.concatenate(shards)
+            assert np.array_equal(_np(gathered), full)
+            np.testing.assert_allclose(_np(out), full @ w.T, rtol=RTOL, atol=ATOL)
+    finally:
+        grp.close()

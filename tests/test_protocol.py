@@ -133,3 +133,36 @@ def test_missing_signal_deadlocks():
     lows[1].ops = [op for op in lows[1].ops if op.op != OP_SIGNAL]
     with pytest.raises(Deadlock):
         World(lows, args).run(1)
+
+
+@pytest.mark.parametrize("kind", AG_KINDS)
+def test_ag_inplace_inputs(kind):
+    """Zero-copy publish: each call's shard is written into the rank's own slot (parity of
+    the call) by the caller just before the call; no local copy in the program."""
+    G, R, K, N = 4, 64, 256, 64
+    sc = _scenario("sim", R * G, N, K, G)
+    for seed in range(2):
+        lows = [lower_ag(build_plan(sc, ScheduleKind(kind)), g, "A", inplace=True) for g in range(G)]
+        ws = max(low.ws_bytes for low in lows)
+        for low in lows:
+            low.ws_bytes = ws
+        w = orc.seeded_inputs(seed, 999, (N, K), "normal")
+        args, expect = [], []
+        for run in range(RUNS):
+            shards = [orc.seeded_inputs(seed * 10 + run, g, (R, K)) for g in range(G)]
+            full = np.concatenate(shards)
+            expect.append(full @ w.T)
+            args.append([{"a": bf16_bits(shards[g]), "b": bf16_bits(w),
+                          "c": np.zeros((R * G, N), dtype=np.uint16)} for g in range(G)])
+        world = World(lows, args, seed=seed)
+
+        def on_start(rank, run):
+            low = lows[rank]
+            off = low.gather_off + (low.gather_par if run & 1 else 0) + rank * R * K * 2
+            world.ranks[rank].ws[off: off + R * K * 2] = args[run][rank]["a"].view(np.uint8).reshape(-1)
+
+        def on_done(rank, run):
+            np.testing.assert_allclose(bits_f32(args[run][rank]["c"]), expect[run], rtol=2e-2, atol=2e-2)
+
+        world.on_run_start, world.on_run_done = on_start, on_done
+        world.run(RUNS)
