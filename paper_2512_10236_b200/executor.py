@@ -114,17 +114,20 @@ class MeasuredMakespan:
             kind = plan.schedule
             _, low, _ = ops.prepare_ag(grp, R, K, N, kind)
             grp.load_peer_shards(low, shards)
+            flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
             for _ in range(self.warmup):
                 ops.all_gather_matmul(shards[0], w, kind=kind, group=grp, out=out)
             torch.cuda.synchronize()
-            ts = []
-            for _ in range(self.reps):
-                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(self.reps)]
+            torch.cuda._sleep(100_000_000)  # host enqueues every rep before the GPU gets there
+            for s, e in evs:
+                flush.fill_(1)  # L2 flushed between reps
                 s.record()
                 ops.all_gather_matmul(shards[0], w, kind=kind, group=grp, out=out)
                 e.record()
-                e.synchronize()
-                ts.append(s.elapsed_time(e) * 1e-3)
+            torch.cuda.synchronize()
+            ts = [s.elapsed_time(e) * 1e-3 for s, e in evs]
             grp.comm.check()
         finally:
             grp.close()

@@ -58,6 +58,7 @@ class FiccoGroup:
         self.world, self.rank, self.virtual, self.pg = world, rank, virtual, pg
         self.comm: Communicator | None = None
         self._plans: dict = {}
+        self._fast: dict = {}
         self._ws_bytes = 0
 
     @classmethod
@@ -77,7 +78,10 @@ class FiccoGroup:
         nbytes = 1 << max(20, math.ceil(math.log2(nbytes)))
         if self.comm is not None:
             torch.cuda.synchronize()
+            for plan, _ in self._plans.values():
+                plan.close()
             self._plans.clear()
+            self._fast.clear()
             self.comm.close()
         if self.virtual:
             self.comm = Communicator.virtual(self.world, self.rank, nbytes)
@@ -117,7 +121,10 @@ class FiccoGroup:
         return self.ws_tensor(self.rank, off, (rows, cols))
 
     def close(self) -> None:
+        for plan, _ in self._plans.values():
+            plan.close()
         self._plans.clear()
+        self._fast.clear()
         if self.comm is not None:
             self.comm.close()
             self.comm = None
@@ -171,14 +178,25 @@ def _default_group(group, world):
     raise ValueError("pass a FiccoGroup (FiccoGroup.distributed(pg) or FiccoGroup.virtual_group(world, rank))")
 
 
+def _cached(grp: FiccoGroup, key, make):
+    """Per-call fast path: (plan, lowered, kind) memoised per (op, shape, requested kind)."""
+    hit = grp._fast.get(key)
+    if hit is None or hit[0].handle is None:
+        hit = make()
+        grp._fast[key] = hit
+    return hit
+
+
 def prepare_ag(grp: FiccoGroup, R: int, K: int, N: int, kind=None, inplace: bool = False):
     """Build (or fetch) the lowered AG->GEMM plan for this rank: (plan, lowered, kind)."""
-    M = R * grp.world
-    sc = _scenario("ag_gemm", M, N, K, grp.world)
-    kd = choose_kind(sc, kind)
-    plan, low = grp.plan(("ag", M, N, K, kd, inplace),
-                         lambda: lower_ag(build_plan(sc, kd), grp.rank, "A", inplace=inplace))
-    return plan, low, kd
+    def make():
+        M = R * grp.world
+        sc = _scenario("ag_gemm", M, N, K, grp.world)
+        kd = choose_kind(sc, kind)
+        plan, low = grp.plan(("ag", M, N, K, kd, inplace),
+                             lambda: lower_ag(build_plan(sc, kd), grp.rank, "A", inplace=inplace))
+        return plan, low, kd
+    return _cached(grp, ("ag", R, K, N, kind, inplace), make)
 
 
 def _is_slot(grp: FiccoGroup, t: torch.Tensor, low) -> bool:
@@ -192,23 +210,27 @@ def _is_slot(grp: FiccoGroup, t: torch.Tensor, low) -> bool:
 
 
 def prepare_rs(grp: FiccoGroup, M: int, K: int, N: int, kind=None):
-    sc = _scenario("gemm_rs", M, N, K, grp.world)
-    kd = choose_kind(sc, kind)
-    if kd not in (ScheduleKind.UNIFORM_FUSED_1D, ScheduleKind.HETERO_FUSED_1D, ScheduleKind.HETERO_UNFUSED_1D):
-        kd = ScheduleKind.HETERO_FUSED_1D  # the 2D/serial choices have no RS adjoint on this executor
-    plan, low = grp.plan(("rs", M, N, K, kd), lambda: lower_rs(sc, kd, grp.rank, virtual=grp.virtual))
-    return plan, low, kd
+    def make():
+        sc = _scenario("gemm_rs", M, N, K, grp.world)
+        kd = choose_kind(sc, kind)
+        if kd not in (ScheduleKind.UNIFORM_FUSED_1D, ScheduleKind.HETERO_FUSED_1D, ScheduleKind.HETERO_UNFUSED_1D):
+            kd = ScheduleKind.HETERO_FUSED_1D  # the 2D/serial choices have no RS adjoint on this executor
+        plan, low = grp.plan(("rs", M, N, K, kd), lambda: lower_rs(sc, kd, grp.rank, virtual=grp.virtual))
+        return plan, low, kd
+    return _cached(grp, ("rs", M, K, N, kind), make)
 
 
 def prepare_cp(grp: FiccoGroup, Tq: int, d: int, Tkv: int, kind=None, scale: float | None = None):
-    sc = _scenario("cp_qk", Tkv, Tq, d, grp.world)
-    kd = choose_kind(sc, kind)
-    if kd is ScheduleKind.UNIFORM_FUSED_2D:
-        kd = ScheduleKind.UNIFORM_FUSED_1D  # K=d is a single k-segment; the 2D split does not apply
-    alpha = (1.0 / math.sqrt(d)) if scale is None else scale
-    plan, low = grp.plan(("cp", Tkv, Tq, d, kd, alpha),
-                         lambda: lower_ag(build_plan(sc, kd), grp.rank, "B", alpha=alpha, other_rows=Tq))
-    return plan, low, kd
+    def make():
+        sc = _scenario("cp_qk", Tkv, Tq, d, grp.world)
+        kd = choose_kind(sc, kind)
+        if kd is ScheduleKind.UNIFORM_FUSED_2D:
+            kd = ScheduleKind.UNIFORM_FUSED_1D  # K=d is a single k-segment; the 2D split does not apply
+        alpha = (1.0 / math.sqrt(d)) if scale is None else scale
+        plan, low = grp.plan(("cp", Tkv, Tq, d, kd, alpha),
+                             lambda: lower_ag(build_plan(sc, kd), grp.rank, "B", alpha=alpha, other_rows=Tq))
+        return plan, low, kd
+    return _cached(grp, ("cp", Tq, d, Tkv, kind, scale), make)
 
 
 def all_gather_matmul(a_shard: torch.Tensor, weight: torch.Tensor, kind=None, group: FiccoGroup | None = None,
