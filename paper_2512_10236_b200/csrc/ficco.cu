@@ -774,12 +774,14 @@ int ficco_plan_run(ficco_plan_t* p, const void* a, const void* b, void* c, void*
     CK(cudaGraphLaunch(gi.exec, s));
     return 0;
   }
+  // Kernel first, then the copy graph: the kernel is dispatched before any of the graph's
+  // stream-wait nodes exists, so a blocked wait can never hold back the kernel that satisfies it.
   ficco_comm* cm = p->comm;
   cudaStream_t gs = cm->copy[FICCO_MAX_STREAMS - 1];  // graph launch stream (idle between runs)
   CK(cudaEventRecord(cm->ev_fork, s));
+  if ((r = launch_tiles(p, parity, a, b, c, s))) return r;
   CK(cudaStreamWaitEvent(gs, cm->ev_fork, 0));
   CK(cudaGraphLaunch(gi.exec, gs));
-  if ((r = launch_tiles(p, parity, a, b, c, s))) return r;
   CK(cudaEventRecord(cm->ev_join[0], gs));
   CK(cudaStreamWaitEvent(s, cm->ev_join[0], 0));
   return 0;

@@ -271,13 +271,20 @@ __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfu
 #pragma unroll
       for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]) * scale;
       if (td.mode == FICCO_EPI_REDUCE && row_ok) {
+        // rank-ascending sum of the peers' partial chunks; the next peer's 64 bytes are in
+        // flight while the current ones are added (the loads are latency-, not bandwidth-bound)
+        const int64_t roff = int64_t(td.recv_row + row) * p.ld_recv + td.c_col + cc * 32;
+        uint4 cur[4], nxt[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) cur[q] = __ldcs(reinterpret_cast<const uint4*>(p.recv[0] + roff) + q);
         for (int j = 0; j < p.n_recv; ++j) {
-          const uint4* src = reinterpret_cast<const uint4*>(p.recv[j] + int64_t(td.recv_row + row) * p.ld_recv +
-                                                            td.c_col + cc * 32);
+          if (j + 1 < p.n_recv) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) nxt[q] = __ldcs(reinterpret_cast<const uint4*>(p.recv[j + 1] + roff) + q);
+          }
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            uint4 w = __ldcs(src + q);
-            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&cur[q]);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               float2 x = __bfloat1622float2(h[e]);
@@ -285,6 +292,8 @@ __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfu
               f[q * 8 + 2 * e + 1] += x.y;
             }
           }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) cur[q] = nxt[q];
         }
       }
       uint4 w[4];

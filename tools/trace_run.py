@@ -19,7 +19,8 @@ from paper_2512_10236_b200 import ops, runtime  # noqa: E402
 
 def main():
     cp = "--cp" in sys.argv
-    argv = [a for a in sys.argv[1:] if a != "--cp"]
+    inplace = "--inplace" in sys.argv
+    argv = [a for a in sys.argv[1:] if not a.startswith("--")]
     M, N, K, G = (131072, 16384, 128, 8) if cp else (8192, 3584, 4096, 8)
     if argv:
         M, N, K, G = map(int, argv[:4])
@@ -39,11 +40,16 @@ def main():
         if cp:
             plan, low, _ = ops.prepare_cp(grp, N, K, M, kind)
         else:
-            plan, low, _ = ops.prepare_ag(grp, R, K, N, kind)
+            plan, low, _ = ops.prepare_ag(grp, R, K, N, kind, inplace=inplace)
         grp.load_peer_shards(low, shards)
+        if inplace and not cp:
+            for par in (0, 1):
+                grp.ws_tensor(0, low.gather_off + par * low.gather_par, (R, K)).copy_(shards[0])
         def call(k, plan=plan):
             if cp:
                 ops.cp_kv_all_gather_qk(w, shards[0], kind=k, group=grp, out=out)
+            elif inplace:
+                ops.all_gather_matmul(grp.input_slot(R, K, N, k), w, kind=k, group=grp, out=out)
             else:
                 ops.all_gather_matmul(shards[0], w, kind=k, group=grp, out=out)
         info = plan.info()
