@@ -89,17 +89,19 @@ int get_driver(Driver** out) {
   return 0;
 }
 
-// 32 x 32 bf16 store boxes with 64-byte swizzle (the epilogue's staging layout).
-int encode_store_map(Driver* drv, CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld) {
+// bf16 store boxes of 32 rows x box_cols (64: SWIZZLE_128B, 32: SWIZZLE_64B) — the epilogue's staging layouts.
+int encode_store_map(Driver* drv, CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld,
+                     int box_cols) {
   if (reinterpret_cast<uintptr_t>(base) % 16 != 0 || (ld * 2) % 16 != 0)
     return fail(FICCO_EINVAL, "output not 16-byte aligned");
   cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
   cuuint64_t strides[1] = {cuuint64_t(ld * 2)};
-  cuuint32_t box[2] = {32, 32};
+  cuuint32_t box[2] = {cuuint32_t(box_cols), 32};
   cuuint32_t estr[2] = {1, 1};
   CKD(drv->encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
+                  CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  box_cols == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                  CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
   return 0;
 }
 
@@ -136,7 +138,13 @@ int configure_kernels(int dev) {
   if (configured == dev) return 0;
 #define FICCO_CFG(T, G)                                                                              \
   CK(cudaFuncSetAttribute(ficco::tile_gemm_kernel<T, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                          ficco::TileCfg<T, G>::SMEM_BYTES));
+                          ficco::TileCfg<T, G>::SMEM_BYTES));                          \
+  {                                                                                                  \
+    cudaFuncAttributes fa;                                                                           \
+    CK(cudaFuncGetAttributes(&fa, ficco::tile_gemm_kernel<T, G>));                                   \
+    if (fa.numRegs * ficco::NUM_THREADS > 65536 - ficco::COPY_RESERVE_REGS)                          \
+      return fail(FICCO_ECUDA, "tile kernel register use leaves no room for copy kernels");      \
+  }
   FICCO_FOR_EACH_CFG(FICCO_CFG)
 #undef FICCO_CFG
   configured = dev;
@@ -374,11 +382,13 @@ int make_params(ficco_plan* p, uint32_t parity, const void* a, const void* b, vo
       (r = resolve(cm, parity, d.part.buf, -1, d.part.off, d.part.par, a, b, c, &pp)))
     return r;
   if (po && d.c.rows > 0) {
-    if ((r = encode_store_map(cm->drv, &prm->tmap_out, po, d.c.rows, d.c.ld, d.c.ld))) return r;
+    if ((r = encode_store_map(cm->drv, &prm->tmap_out, po, d.c.rows, d.c.ld, d.c.ld, 64))) return r;
+    if ((r = encode_store_map(cm->drv, &prm->tmap_out32, po, d.c.rows, d.c.ld, d.c.ld, 32))) return r;
     prm->has_out_map = 1;
   }
   if (pp && d.part.rows > 0) {
-    if ((r = encode_store_map(cm->drv, &prm->tmap_part, pp, d.part.rows, d.part.ld, d.part.ld))) return r;
+    if ((r = encode_store_map(cm->drv, &prm->tmap_part, pp, d.part.rows, d.part.ld, d.part.ld, 64))) return r;
+    if ((r = encode_store_map(cm->drv, &prm->tmap_part32, pp, d.part.rows, d.part.ld, d.part.ld, 32))) return r;
     prm->has_part_map = 1;
   }
   prm->tiles = p->d_tiles;

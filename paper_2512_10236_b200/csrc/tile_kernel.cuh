@@ -42,14 +42,22 @@ constexpr int A_STAGE = BM * BK * 2;  // 16 KiB
 constexpr int EPI_WARPS = 8;   // two epilogue warps per TMEM lane quarter (alternating 32-column chunks)
 constexpr int EPI_THREADS = EPI_WARPS * 32;
 constexpr int NUM_THREADS = 64 + EPI_THREADS;
+// Register cap. The persistent kernel occupies every SM for the whole op while the
+// copy program runs beside it; same-device strided copies (the virtual peers' pulls,
+// local publishes) may be executed by the driver as small SM copy kernels, which must
+// still fit next to one tile CTA. At 168 registers/thread the co-resident copy CTA no
+// longer fits and the copy program stalls behind the kernel that waits on it.
+constexpr int MAX_REGS = 128;
+constexpr int COPY_RESERVE_REGS = 65536 - MAX_REGS * NUM_THREADS;
 constexpr uint32_t TMEM_COLS = 512;  // two accumulators of up to 256 fp32 columns
 constexpr int MAX_RECV = 15;
 constexpr uint32_t SPIN_LIMIT = 1u << 25;  // ~4-10 s of polling before declaring a timeout
 constexpr int SMEM_LIMIT = 226 * 1024;  // leaves room for the static smem (seen-flag bitset)
-// Epilogue output staging: per epilogue warp EPI_BUFS buffers of one 32 x 32 bf16 box
-// (64 B rows, TMA SWIZZLE_64B layout), stored with cp.async.bulk.tensor.
-constexpr int EPI_BUF_BYTES = 32 * 64;
-constexpr int EPI_BUFS = 2;
+// Epilogue output staging: per epilogue warp EPI_BUFS buffers of one 32-row x 64-column bf16
+// box (128 B rows, TMA SWIZZLE_128B layout: full-line writes), stored with
+// cp.async.bulk.tensor; a trailing 32-column chunk uses a 32 x 32 box (SWIZZLE_64B).
+constexpr int EPI_BUF_BYTES = 32 * 128;
+constexpr int EPI_BUFS = 1;
 
 // Per (tile width, CTA group) configuration: as many pipeline stages as fit.
 template <int TN, int CG>
@@ -70,8 +78,10 @@ struct alignas(64) TileParams {
   CUtensorMap tmap_b;
   CUtensorMap tmap_a2;  // alternate sources (e.g. the caller's local shard, read in place)
   CUtensorMap tmap_b2;
-  CUtensorMap tmap_out;   // 32 x 32 store boxes, SWIZZLE_64B (STORE / REDUCE destination)
-  CUtensorMap tmap_part;  // same for the STORE_SIGNAL destination
+  CUtensorMap tmap_out;     // 64 x 32 store boxes, SWIZZLE_128B (STORE / REDUCE destination)
+  CUtensorMap tmap_part;    // same for the STORE_SIGNAL destination
+  CUtensorMap tmap_out32;   // 32 x 32 boxes, SWIZZLE_64B (trailing 32-column chunks)
+  CUtensorMap tmap_part32;
   int has_out_map;
   int has_part_map;
   const ficco_tile* tiles;
@@ -222,9 +232,54 @@ __device__ __forceinline__ void mma_loop(const TileParams& p, uint8_t* sA, uint8
   }
 }
 
-// Byte offset of 16-byte chunk j of row t inside a 32-row x 64-byte TMA SWIZZLE_64B box
-// (Swizzle<2,4,3>: address bits [4,5] ^= bits [7,8]).
+// Byte offset of 16-byte chunk j of row t in a TMA SWIZZLE_64B box (64 B rows, Swizzle<2,4,3>)
+// and in a SWIZZLE_128B box (128 B rows, Swizzle<3,4,3>).
 __device__ __forceinline__ uint32_t swz64(uint32_t t, uint32_t j) { return t * 64u + ((j ^ ((t >> 1) & 3u)) << 4); }
+__device__ __forceinline__ uint32_t swz128(uint32_t t, uint32_t j) { return t * 128u + ((j ^ (t & 7u)) << 4); }
+
+// TMEM columns [col, col+32) of this thread's row -> scaled fp32 (+ peers' partials) -> 4 packed uint4.
+__device__ __forceinline__ void epi_chunk(const TileParams& p, const ficco_tile& td, uint32_t taddr, int col,
+                                          float scale, bool reduce_row, int row, uint4 (&w)[4]) {
+  uint32_t v[32];
+  tmem_ld_32x32b_x32(taddr + col, v);
+  tmem_ld_wait();
+  float f[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]) * scale;
+  if (reduce_row) {
+    // rank-ascending sum of the peers' partial chunks; the next peer's 64 bytes are in
+    // flight while the current ones are added (the loads are latency-, not bandwidth-bound)
+    const int64_t roff = int64_t(td.recv_row + row) * p.ld_recv + td.c_col + col;
+    uint4 cur[4], nxt[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) cur[q] = __ldcs(reinterpret_cast<const uint4*>(p.recv[0] + roff) + q);
+    for (int j = 0; j < p.n_recv; ++j) {
+      if (j + 1 < p.n_recv) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) nxt[q] = __ldcs(reinterpret_cast<const uint4*>(p.recv[j + 1] + roff) + q);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&cur[q]);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float2 x = __bfloat1622float2(h[e]);
+          f[q * 8 + 2 * e] += x.x;
+          f[q * 8 + 2 * e + 1] += x.y;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) cur[q] = nxt[q];
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    w[q].x = pack_bf16x2(f[q * 8 + 0], f[q * 8 + 1]);
+    w[q].y = pack_bf16x2(f[q * 8 + 2], f[q * 8 + 3]);
+    w[q].z = pack_bf16x2(f[q * 8 + 4], f[q * 8 + 5]);
+    w[q].w = pack_bf16x2(f[q * 8 + 6], f[q * 8 + 7]);
+  }
+}
 
 template <int TN, int CG>
 __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfull, uint64_t* tempty,
@@ -232,11 +287,11 @@ __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfu
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   const int quarter = warp & 3;           // TMEM lane quarter this warp may access
-  const int half = (warp - 2) / 4;        // which alternate 32-column chunks this warp drains
+  const int half = (warp - 2) / 4;        // which alternate 64-column chunks this warp drains
   const int row = quarter * 32 + lane;
   const uint64_t hint_out = policy_evict_first();  // results stream out; keep operands resident in L2
-  uint8_t* wbuf = stage_smem + (warp - 2) * (EPI_BUFS * EPI_BUF_BYTES);
-  uint32_t nbuf = 0;  // this warp's staging buffers used so far (ring of EPI_BUFS)
+  uint8_t* buf = stage_smem + (warp - 2) * (EPI_BUFS * EPI_BUF_BYTES);
+  bool pending = false;  // a bulk store still reading `buf`
   uint32_t it = 0;
   for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
     const ficco_tile td = p.tiles[t];
@@ -254,73 +309,47 @@ __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfu
     const uint32_t taddr = tmem + (uint32_t(quarter * 32) << 16) + acc * BN_MAX;
     const bool row_ok = row < td.rows;
     const bool signal = td.mode == FICCO_EPI_STORE_SIGNAL;
+    const bool reduce_row = td.mode == FICCO_EPI_REDUCE && row_ok;
     // whole 32-row warp boxes go out through TMA stores; ragged rows use direct stores
     const int warp_rows = td.rows - quarter * 32;
     const bool tma = warp_rows >= 32 && (signal ? p.has_part_map : p.has_out_map);
-    const CUtensorMap* map = signal ? &p.tmap_part : &p.tmap_out;
+    const CUtensorMap* map64 = signal ? &p.tmap_part : &p.tmap_out;
+    const CUtensorMap* map32 = signal ? &p.tmap_part32 : &p.tmap_out32;
     __nv_bfloat16* dst = signal ? p.part + int64_t(td.c_row + row) * p.ld_part + td.c_col
                                 : p.out + int64_t(td.c_row + row) * p.ld_out + td.c_col;
     const float scale = td.mode == FICCO_EPI_STORE ? p.alpha : 1.0f;
 #pragma unroll 1
-    for (int cc = half; cc < TN / 32; cc += 2) {
-      uint32_t v[32];
-      tmem_ld_32x32b_x32(taddr + cc * 32, v);
-      tmem_ld_wait();
-      if (cc * 32 >= td.cols) continue;  // warp-uniform
-      float f[32];
+    for (int c64 = half; c64 * 64 < TN; c64 += 2) {
+      const int col = c64 * 64;
+      const bool live1 = col + 64 <= TN && col + 32 < td.cols;  // warp-uniform
+      if (col >= td.cols) continue;
+      if (tma) {
+        if (lane == 0 && pending) tma_store_wait_read<0>();  // the staging buffer drained
+        __syncwarp();
+      }
+      // the two 32-column halves one after the other: one half's values live at a time
+#pragma unroll 1
+      for (int h = 0; h < (live1 ? 2 : 1); ++h) {
+        uint4 w[4];
+        epi_chunk(p, td, taddr, col + 32 * h, scale, reduce_row, row, w);
+        if (tma) {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]) * scale;
-      if (td.mode == FICCO_EPI_REDUCE && row_ok) {
-        // rank-ascending sum of the peers' partial chunks; the next peer's 64 bytes are in
-        // flight while the current ones are added (the loads are latency-, not bandwidth-bound)
-        const int64_t roff = int64_t(td.recv_row + row) * p.ld_recv + td.c_col + cc * 32;
-        uint4 cur[4], nxt[4];
+          for (int q = 0; q < 4; ++q)
+            *reinterpret_cast<uint4*>(buf + (live1 ? swz128(lane, 4 * h + q) : swz64(lane, q))) = w[q];
+        } else if (row_ok) {
+          uint4* o = reinterpret_cast<uint4*>(dst + col + 32 * h);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) cur[q] = __ldcs(reinterpret_cast<const uint4*>(p.recv[0] + roff) + q);
-        for (int j = 0; j < p.n_recv; ++j) {
-          if (j + 1 < p.n_recv) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) nxt[q] = __ldcs(reinterpret_cast<const uint4*>(p.recv[j + 1] + roff) + q);
-          }
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&cur[q]);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              float2 x = __bfloat1622float2(h[e]);
-              f[q * 8 + 2 * e] += x.x;
-              f[q * 8 + 2 * e + 1] += x.y;
-            }
-          }
-#pragma unroll
-          for (int q = 0; q < 4; ++q) cur[q] = nxt[q];
+          for (int q = 0; q < 4; ++q) o[q] = w[q];
         }
       }
-      uint4 w[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        w[q].x = pack_bf16x2(f[q * 8 + 0], f[q * 8 + 1]);
-        w[q].y = pack_bf16x2(f[q * 8 + 2], f[q * 8 + 3]);
-        w[q].z = pack_bf16x2(f[q * 8 + 4], f[q * 8 + 5]);
-        w[q].w = pack_bf16x2(f[q * 8 + 6], f[q * 8 + 7]);
-      }
       if (tma) {
-        uint8_t* buf = wbuf + (nbuf % EPI_BUFS) * EPI_BUF_BYTES;
-        if (lane == 0 && nbuf >= EPI_BUFS) tma_store_wait_read<EPI_BUFS - 1>();  // buffer drained by its store
-        __syncwarp();
-#pragma unroll
-        for (int q = 0; q < 4; ++q) *reinterpret_cast<uint4*>(buf + swz64(lane, q)) = w[q];
         fence_async_shared();
         __syncwarp();
         if (lane == 0) {
-          tma_store_2d_hint(map, buf, td.c_col + cc * 32, td.c_row + quarter * 32, hint_out);
+          tma_store_2d_hint(live1 ? map64 : map32, buf, td.c_col + col, td.c_row + quarter * 32, hint_out);
           tma_store_commit();
         }
-        ++nbuf;
-      } else if (row_ok) {
-        uint4* o = reinterpret_cast<uint4*>(dst + cc * 32);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) o[q] = w[q];
+        pending = true;
       }
     }
     tc_fence_before();
@@ -342,7 +371,7 @@ __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfu
 }
 
 template <int TN, int CG>
-__global__ void __launch_bounds__(NUM_THREADS, 1) tile_gemm_kernel(const __grid_constant__ TileParams p) {
+__global__ void __maxnreg__(MAX_REGS) tile_gemm_kernel(const __grid_constant__ TileParams p) {
   using Cfg = TileCfg<TN, CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -365,8 +394,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tile_gemm_kernel(const __grid_
     tma_prefetch_desc(&p.tmap_b);
     tma_prefetch_desc(&p.tmap_a2);
     tma_prefetch_desc(&p.tmap_b2);
-    if (p.has_out_map) tma_prefetch_desc(&p.tmap_out);
-    if (p.has_part_map) tma_prefetch_desc(&p.tmap_part);
+    if (p.has_out_map) {
+      tma_prefetch_desc(&p.tmap_out);
+      tma_prefetch_desc(&p.tmap_out32);
+    }
+    if (p.has_part_map) {
+      tma_prefetch_desc(&p.tmap_part);
+      tma_prefetch_desc(&p.tmap_part32);
+    }
     for (int s = 0; s < Cfg::STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);

@@ -87,7 +87,7 @@ def load_library(path: os.PathLike | str | None = None) -> C.CDLL:
     with _lock:
         if _lib is not None:
             return _lib
-        p = pathlib.Path(path) if path else LIB_PATH
+        p = pathlib.Path(path or os.environ.get("FICCO_LIB_PATH") or LIB_PATH)
         if not p.exists():
             raise RuntimeError(f"{p} not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
         lib = C.CDLL(str(p))
