@@ -37,8 +37,9 @@ from .selector import select_schedule
 
 
 # FICCO_SERIALIZE=1: run copy programs to completion before the tile kernel (kernel
-# profilers such as ncu serialise work, which would starve flag-gated tiles).
-SERIALIZE = os.environ.get("FICCO_SERIALIZE", "0") == "1"
+# profilers such as ncu serialise work, which would starve flag-gated tiles). ncu is
+# detected by the environment it injects (NV_COMPUTE_PROFILER_PERFWORKS_DIR) and switches this on by itself.
+SERIALIZE = os.environ.get("FICCO_SERIALIZE", "0") == "1" or bool(os.environ.get("NV_COMPUTE_PROFILER_PERFWORKS_DIR"))
 
 
 def _scenario(name: str, m: int, n: int, k: int, world: int, collective=Collective.ALL_GATHER) -> Scenario:
