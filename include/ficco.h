@@ -64,6 +64,7 @@ extern "C" {
 #define FICCO_FLAG_CONST_ONE 16320                 /* constant 0x01010101: source of flag-setting copies */
 #define FICCO_FLAG_CONST_ZERO 16322                /* constant 8 zero bytes: source of flag resets */
 #define FICCO_FLAG_ABORT (FICCO_WS_FLAG_WORDS - 1) /* kernel-side timeout indicator */
+#define FICCO_WS_IDENTITY_OFF 40960                /* bytes: 64 x 64 bf16 identity (RS reduction operand) */
 #define FICCO_MAX_STREAMS 16                       /* copy streams (parallel copy-engine chains) */
 
 /* copy-program opcodes (executed in order on the copy stream) */
@@ -219,6 +220,10 @@ int ficco_gemm_bf16_cfg(const void* a, const void* b, void* c, int64_t m, int64_
                         int grid, int tile_n, int cta_group, void* stream);
 int ficco_copy_batch(void* const* dsts, const void* const* srcs, const size_t* sizes, size_t count,
                      void* stream);
+/* Occupy every SM (one CTA per SM holding all registers and shared memory) for `ns`
+ * nanoseconds: copies issued meanwhile progress only if a copy engine executes them
+ * (copy-engine vs SM-copy-kernel probe; CIL calibration). */
+int ficco_occupy_sms(int64_t ns, void* stream);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

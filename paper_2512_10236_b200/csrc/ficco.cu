@@ -153,6 +153,17 @@ int configure_kernels(int dev) {
 
 }  // namespace
 
+namespace ficco {
+// Spin for `ns` with every register and shared-memory byte of the SM taken (launch 1 CTA x 1024
+// threads per SM with the opt-in smem maximum): nothing else can be resident meanwhile.
+__global__ void __launch_bounds__(1024, 1) occupy_kernel(int64_t ns) {
+  extern __shared__ uint8_t occ_smem[];
+  const unsigned long long t0 = globaltimer();
+  if (threadIdx.x == 0) occ_smem[0] = 1;
+  while (int64_t(globaltimer() - t0) < ns) __nanosleep(256);
+}
+}  // namespace ficco
+
 struct ficco_comm {
   int rank = 0, world = 1, device = 0, sms = 0;
   bool virt = false;
@@ -406,6 +417,25 @@ int make_params(ficco_plan* p, uint32_t parity, const void* a, const void* b, vo
   }
   prm->ld_recv = d.recv.ld;
   prm->rs_flag0 = d.rs_flag0;
+  {
+    // identity-MMA reduction: the receive slots must tile one [n_recv * rows, N] matrix
+    const char* hint = getenv("FICCO_PART_HINT");
+    prm->part_hint = hint ? atoi(hint) : 0;
+    const char* env = getenv("FICCO_RS_MMA");
+    const int64_t pitch = d.recv.ld * 2;
+    if (d.n_recv > 0 && !(env && env[0] == '0') && pitch > 0 && d.recv_slot % pitch == 0) {
+      uint8_t* pr0;
+      if ((r = resolve(cm, parity, d.recv.buf, -1, d.recv.off, d.recv.par, a, b, c, &pr0))) return r;
+      prm->recv_rows = int(d.recv_slot / pitch);
+      if ((r = encode_bf16_2d(cm->drv, &prm->tmap_recv, pr0, int64_t(d.n_recv) * prm->recv_rows, d.recv.ld,
+                              d.recv.ld, ficco::BM)))
+        return r;
+      if ((r = encode_bf16_2d(cm->drv, &prm->tmap_ident, cm->ws[cm->rank] + FICCO_WS_IDENTITY_OFF, 64, 64, 64,
+                              64 / p->cta_group)))
+        return r;
+      prm->reduce_mma = 1;
+    }
+  }
   prm->flags = cm->block(cm->rank, parity);
   prm->counters = cm->block(cm->rank, parity) + FICCO_FLAG_COUNTERS;
   prm->abort_word = cm->flags(cm->rank) + FICCO_FLAG_ABORT;
@@ -545,6 +575,12 @@ int ficco_ws_alloc(size_t bytes, void** out) {
   CK(cudaMemset(p, 0, FICCO_WS_DATA_OFFSET));
   const uint32_t one = 0x01010101u;
   CK(cudaMemcpy(reinterpret_cast<uint32_t*>(p) + FICCO_FLAG_CONST_ONE, &one, 4, cudaMemcpyHostToDevice));
+  {
+    uint16_t ident[64 * 64] = {};
+    for (int i = 0; i < 64; ++i) ident[i * 64 + i] = 0x3F80;  // bf16 1.0
+    CK(cudaMemcpy(reinterpret_cast<uint8_t*>(p) + FICCO_WS_IDENTITY_OFF, ident, sizeof(ident),
+                  cudaMemcpyHostToDevice));
+  }
   CK(cudaDeviceSynchronize());
   *out = p;
   return 0;
@@ -794,6 +830,17 @@ int ficco_plan_run(ficco_plan_t* p, const void* a, const void* b, void* c, void*
   CK(cudaGraphLaunch(gi.exec, gs));
   CK(cudaEventRecord(cm->ev_join[0], gs));
   CK(cudaStreamWaitEvent(s, cm->ev_join[0], 0));
+  return 0;
+}
+
+int ficco_occupy_sms(int64_t ns, void* stream) {
+  int dev, sms, smem;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  CK(cudaDeviceGetAttribute(&smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  CK(cudaFuncSetAttribute(ficco::occupy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  ficco::occupy_kernel<<<sms, 1024, smem, reinterpret_cast<cudaStream_t>(stream)>>>(ns);
+  CK(cudaGetLastError());
   return 0;
 }
 

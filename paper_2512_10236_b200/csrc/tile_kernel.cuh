@@ -71,6 +71,10 @@ struct TileCfg {
   static constexpr int MAX_STAGES = (SMEM_LIMIT - 1024 - 256 - EPI_STAGE_BYTES) / STAGE;
   static constexpr int STAGES = MAX_STAGES > 8 ? 8 : MAX_STAGES;
   static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE + EPI_STAGE_BYTES + 256;
+  // REDUCE tiles: per peer, RKB extra k-blocks D[:, 64i:64i+64] += P_j[:, 64i:64i+64] * I_64
+  static constexpr int RKB = (TN + 63) / 64;
+  static constexpr int IDENT_ROWS = 64 / CG;  // identity rows (UMMA N split) loaded by each CTA
+  static constexpr int RED_STAGE = A_STAGE + IDENT_ROWS * BK * 2;
 };
 
 struct alignas(64) TileParams {
@@ -82,6 +86,8 @@ struct alignas(64) TileParams {
   CUtensorMap tmap_part;    // same for the STORE_SIGNAL destination
   CUtensorMap tmap_out32;   // 32 x 32 boxes, SWIZZLE_64B (trailing 32-column chunks)
   CUtensorMap tmap_part32;
+  CUtensorMap tmap_recv;    // receive slots as one [n_recv * recv_rows, N] matrix, 128 x 64 boxes (A layout)
+  CUtensorMap tmap_ident;   // 64 x 64 bf16 identity, (64 / CG) x 64 boxes (B layout)
   int has_out_map;
   int has_part_map;
   const ficco_tile* tiles;
@@ -95,6 +101,9 @@ struct alignas(64) TileParams {
   int64_t ld_recv;
   int n_recv;
   int rs_flag0;
+  int reduce_mma;          // REDUCE tiles fold the peers' partials in with identity MMAs (else epilogue loads)
+  int recv_rows;           // rows per receive slot in tmap_recv (slot j starts at row j * recv_rows)
+  int part_hint;           // L2 policy of STORE_SIGNAL (to-be-pushed) stores: 0 evict_first, 1 normal, 2 last
   uint32_t* flags;         // local flag block of this run's parity
   uint32_t* counters;      // local tile counters
   uint32_t* abort_word;
@@ -189,6 +198,33 @@ __device__ __forceinline__ void producer_loop(const TileParams& p, uint8_t* sA, 
         phase ^= 1u;
       }
     }
+    if (p.reduce_mma && td.mode == FICCO_EPI_REDUCE) {
+      // GEMM -> RS owner tile: the peers' partial chunks (copy-engine pushed into our
+      // receive slots) stream through the same ring as A operands against an identity B,
+      // so the reduction rides the TMA/tensor pipeline instead of the epilogue's loads.
+      for (int j = 0; j < p.n_recv; ++j)
+        wait_flag_cached(seen, p.flags, p.rs_flag0 + td.chunk * p.n_recv + j, p.epoch, p.abort_word);
+      for (int j = 0; j < p.n_recv; ++j) {
+        for (int kb = 0; kb < Cfg::RKB; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1u);
+          const int rrow = j * p.recv_rows + td.recv_row;
+          if constexpr (CG == 1) {
+            mbar_arrive_expect_tx(&full[stage], Cfg::RED_STAGE);
+            tma_load_2d(sA + stage * A_STAGE, &p.tmap_recv, &full[stage], td.c_col + kb * 64, rrow, hint_a);
+            tma_load_2d(sB + stage * Cfg::B_STAGE, &p.tmap_ident, &full[stage], 0, 0, hint_b);
+          } else {
+            if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::RED_STAGE);
+            tma_load_2d_pair(sA + stage * A_STAGE, &p.tmap_recv, &full[stage], td.c_col + kb * 64, rrow, hint_a);
+            tma_load_2d_pair(sB + stage * Cfg::B_STAGE, &p.tmap_ident, &full[stage], 0,
+                             int(rank) * Cfg::IDENT_ROWS, hint_b);
+          }
+          if (++stage == Cfg::STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
   }
 }
 
@@ -197,6 +233,7 @@ __device__ __forceinline__ void mma_loop(const TileParams& p, uint8_t* sA, uint8
                                          uint64_t* empty, uint64_t* tfull, uint64_t* tempty, uint32_t tmem) {
   using Cfg = TileCfg<TN, CG>;
   constexpr uint32_t idesc = make_idesc_bf16(BM * CG, TN);
+  constexpr uint32_t idesc64 = make_idesc_bf16(BM * CG, 64);
   uint32_t stage = 0, phase = 0, it = 0;
   for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
     const uint32_t acc = it & 1u;
@@ -223,6 +260,31 @@ __device__ __forceinline__ void mma_loop(const TileParams& p, uint8_t* sA, uint8
       if (++stage == Cfg::STAGES) {
         stage = 0;
         phase ^= 1u;
+      }
+    }
+    if (p.reduce_mma && p.tiles[t].mode == FICCO_EPI_REDUCE) {
+      // D[:, 64i:64i+64] += P_j[:, 64i:64i+64] x I_64 for every peer j (rank-ascending)
+      for (int j = 0; j < p.n_recv * Cfg::RKB; ++j) {
+        const uint32_t col = uint32_t(j % Cfg::RKB) * 64u;
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        const uint64_t ad = make_sdesc_sw128(smem_addr(sA + stage * A_STAGE));
+        const uint64_t bd = make_sdesc_sw128(smem_addr(sB + stage * Cfg::B_STAGE));
+#pragma unroll
+        for (int k = 0; k < BK / UMMA_K; ++k) {
+          if constexpr (CG == 1)
+            umma_bf16(d + col, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc64, 1u);
+          else
+            umma_bf16_pair(d + col, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc64, 1u);
+        }
+        if constexpr (CG == 1)
+          umma_commit(&empty[stage]);
+        else
+          umma_commit_pair(&empty[stage]);
+        if (++stage == Cfg::STAGES) {
+          stage = 0;
+          phase ^= 1u;
+        }
       }
     }
     if constexpr (CG == 1)
@@ -290,13 +352,16 @@ __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfu
   const int half = (warp - 2) / 4;        // which alternate 64-column chunks this warp drains
   const int row = quarter * 32 + lane;
   const uint64_t hint_out = policy_evict_first();  // results stream out; keep operands resident in L2
+  // partial chunks are read back by the push copies right after their unit completes
+  const uint64_t hint_part = p.part_hint == 2 ? policy_evict_last()
+                             : p.part_hint == 1 ? policy_evict_normal() : hint_out;
   uint8_t* buf = stage_smem + (warp - 2) * (EPI_BUFS * EPI_BUF_BYTES);
   bool pending = false;  // a bulk store still reading `buf`
   uint32_t it = 0;
   for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
     const ficco_tile td = p.tiles[t];
     const uint32_t acc = it & 1u;
-    if (td.mode == FICCO_EPI_REDUCE) {
+    if (td.mode == FICCO_EPI_REDUCE && !p.reduce_mma) {
       // peers' partial chunks must have landed in our receive slots
       if (threadIdx.x == 64) {
         for (int j = 0; j < p.n_recv; ++j)
@@ -309,7 +374,7 @@ __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfu
     const uint32_t taddr = tmem + (uint32_t(quarter * 32) << 16) + acc * BN_MAX;
     const bool row_ok = row < td.rows;
     const bool signal = td.mode == FICCO_EPI_STORE_SIGNAL;
-    const bool reduce_row = td.mode == FICCO_EPI_REDUCE && row_ok;
+    const bool reduce_row = td.mode == FICCO_EPI_REDUCE && !p.reduce_mma && row_ok;
     // whole 32-row warp boxes go out through TMA stores; ragged rows use direct stores
     const int warp_rows = td.rows - quarter * 32;
     const bool tma = warp_rows >= 32 && (signal ? p.has_part_map : p.has_out_map);
@@ -346,7 +411,8 @@ __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfu
         fence_async_shared();
         __syncwarp();
         if (lane == 0) {
-          tma_store_2d_hint(live1 ? map64 : map32, buf, td.c_col + col, td.c_row + quarter * 32, hint_out);
+          tma_store_2d_hint(live1 ? map64 : map32, buf, td.c_col + col, td.c_row + quarter * 32,
+                            signal ? hint_part : hint_out);
           tma_store_commit();
         }
         pending = true;
@@ -401,6 +467,10 @@ __global__ void __maxnreg__(MAX_REGS) tile_gemm_kernel(const __grid_constant__ T
     if (p.has_part_map) {
       tma_prefetch_desc(&p.tmap_part);
       tma_prefetch_desc(&p.tmap_part32);
+    }
+    if (p.reduce_mma) {
+      tma_prefetch_desc(&p.tmap_recv);
+      tma_prefetch_desc(&p.tmap_ident);
     }
     for (int s = 0; s < Cfg::STAGES; ++s) {
       mbar_init(&full[s], 1);

@@ -128,7 +128,8 @@ def pair_tiles(tiles: list[Tile]) -> list[Tile]:
     pending: dict[tuple, Tile] = {}
     out: list[Tile] = []
     for t in tiles:
-        key = (t.b_row, t.c_col, t.cols, t.b_src)
+        # REDUCE tiles stream extra (partial x identity) k-blocks: both CTAs must do them
+        key = (t.b_row, t.c_col, t.cols, t.b_src, t.mode == EPI_REDUCE)
         mate = pending.pop(key, None)
         if mate is None:
             pending[key] = t
@@ -138,6 +139,8 @@ def pair_tiles(tiles: list[Tile]) -> list[Tile]:
         # the padding CTA still loads half of B, so it must honour the same gates
         pad = _tile(t.a_row, t.b_row, t.c_row, t.c_col, 0, t.cols, t.flag, t.fmask, t.kseg, t.kstride,
                     a_src=t.a_src, b_src=t.b_src)
+        if t.mode == EPI_REDUCE:  # same k-block stream (and receive-slot gates) as its partner
+            pad.mode, pad.chunk, pad.recv_row = EPI_REDUCE, t.chunk, t.recv_row
         out += [t, pad]
     return out
 

@@ -42,7 +42,7 @@ EXPORTED = (
     "ficco_ipc_handle_size", "ficco_ipc_get_handle", "ficco_ipc_open", "ficco_ipc_close",
     "ficco_comm_create", "ficco_comm_destroy", "ficco_comm_epoch", "ficco_comm_check", "ficco_comm_set_flags",
     "ficco_plan_create", "ficco_plan_destroy", "ficco_plan_run", "ficco_plan_run_parts",
-    "ficco_gemm_bf16", "ficco_copy_batch", "ficco_plan_set_trace", "ficco_plan_info", "ficco_gemm_bf16_cfg",
+    "ficco_gemm_bf16", "ficco_copy_batch", "ficco_plan_set_trace", "ficco_plan_info", "ficco_gemm_bf16_cfg", "ficco_occupy_sms",
 )
 
 
@@ -114,6 +114,7 @@ def load_library(path: os.PathLike | str | None = None) -> C.CDLL:
             "ficco_gemm_bf16": ([vp, vp, vp, i64, i64, i64, C.c_float, i32, vp], i32),
             "ficco_gemm_bf16_cfg": ([vp, vp, vp, i64, i64, i64, C.c_float, i32, i32, i32, vp], i32),
             "ficco_copy_batch": ([C.POINTER(vp), C.POINTER(vp), C.POINTER(sz), sz, vp], i32),
+            "ficco_occupy_sms": ([i64, vp], i32),
             "ficco_plan_set_trace": ([vp, vp], i32),
             "ficco_plan_info": ([vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)], i32),
         }
