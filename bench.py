@@ -139,6 +139,7 @@ class AGWorkload:
     """C2: all-gather -> GEMM (TP/SP up-projection)."""
 
     inplace = False
+    agent = "dma"  # comm_agent: copy engines ("dma") or SM copy kernels ("core")
 
     key = "c2"
     title = "C2 Llama-3-8B TP/SP MLP up-proj AG->GEMM"
@@ -163,7 +164,7 @@ class AGWorkload:
         return {"M": self.M, "N": self.N, "K": self.K, "seq_len": self.M}
 
     def prepare(self, grp, kind):
-        _, low, _ = self.ops.prepare_ag(grp, self.R, self.K, self.N, kind)
+        _, low, _ = self.ops.prepare_ag(grp, self.R, self.K, self.N, kind, comm_agent=self.agent)
         if grp.virtual:
             grp.load_peer_shards(low, self.shards)
         if self.inplace:  # the shard already sits in this rank's workspace slot, both parities
@@ -175,9 +176,10 @@ class AGWorkload:
         if self.inplace:
             def fn():
                 a = grp.input_slot(self.R, self.K, self.N, kind)
-                self.ops.all_gather_matmul(a, self.w, kind=kind, group=grp, out=self.out)
+                self.ops.all_gather_matmul(a, self.w, kind=kind, group=grp, out=self.out, comm_agent=self.agent)
             return fn
-        return lambda: self.ops.all_gather_matmul(self.shards[0], self.w, kind=kind, group=grp, out=self.out)
+        return lambda: self.ops.all_gather_matmul(self.shards[0], self.w, kind=kind, group=grp, out=self.out,
+                                                  comm_agent=self.agent)
 
     def serial(self):
         t = self.t
@@ -262,12 +264,13 @@ class RSWorkload(AGWorkload):
         return {"M": self.M, "N": self.N, "K": self.K, "seq_len": self.M}
 
     def prepare(self, grp, kind):
-        _, low, _ = self.ops.prepare_rs(grp, self.M, self.K, self.N, kind)
+        _, low, _ = self.ops.prepare_rs(grp, self.M, self.K, self.N, kind, comm_agent=self.agent)
         if grp.virtual:
             grp.load_peer_partials(low, self.peer_parts)
 
     def step(self, grp, kind):
-        return lambda: self.ops.matmul_reduce_scatter(self.a, self.w, kind=kind, group=grp, out=self.out)
+        return lambda: self.ops.matmul_reduce_scatter(self.a, self.w, kind=kind, group=grp, out=self.out,
+                                                      comm_agent=self.agent)
 
     def serial(self):
         t = self.t
@@ -345,12 +348,13 @@ class CPWorkload(AGWorkload):
         return {"Tkv": self.Tkv, "Tq": self.Tq, "d": self.d, "seq_len": self.Tkv}
 
     def prepare(self, grp, kind):
-        _, low, _ = self.ops.prepare_cp(grp, self.Tq, self.d, self.Tkv, kind)
+        _, low, _ = self.ops.prepare_cp(grp, self.Tq, self.d, self.Tkv, kind, comm_agent=self.agent)
         if grp.virtual:
             grp.load_peer_shards(low, self.shards)
 
     def step(self, grp, kind):
-        return lambda: self.ops.cp_kv_all_gather_qk(self.q, self.shards[0], kind=kind, group=grp, out=self.out)
+        return lambda: self.ops.cp_kv_all_gather_qk(self.q, self.shards[0], kind=kind, group=grp, out=self.out,
+                                                    comm_agent=self.agent)
 
     def serial(self):
         t = self.t
@@ -452,6 +456,16 @@ def our_arm(args) -> None:
         grp.comm.check()
         sched[kind] = {"us": maxrank(statistics.median(ts)) * 1e3, "mean_us": maxrank(statistics.mean(ts)) * 1e3}
     best = min((k for k in sched if "us" in sched[k] and k != "serial"), key=lambda k: sched[k]["us"])
+    # comm_agent = core (SM copy kernels) for the same schedules: the CE-offload comparison point
+    core = {}
+    if not args.no_core:
+        wl.agent = "core"
+        for kind in [k for k in sched if "us" in sched[k]]:
+            wl.prepare(grp, kind)
+            ts = time_steps(wl.step(grp, kind), args.steps, args.warmup, flush, stream, barrier)
+            grp.comm.check()
+            core[kind] = {"us": round(maxrank(statistics.median(ts)) * 1e3, 2)}
+        wl.agent = "dma"
     wl.prepare(grp, best)
     wl.step(grp, best)()
     grp.comm.check()
@@ -512,6 +526,7 @@ def our_arm(args) -> None:
             "serial_baseline": serial_desc, "cublas_gemm_us": round(cublas_us, 2),
             "ideal_overlap_us": round(t_star, 2), "pct_ideal_overlap": round(t_star / value, 4),
             "schedules": {k: ({"us": round(v["us"], 2)} if "us" in v else v) for k, v in sched.items()},
+            "schedules_comm_agent_core": core,
             "parity_spot_check": parity,
             "roofline": {"bound": bound, "achieved": round(achieved, 1), "peak": peak, "unit": unit,
                          "frac": round(achieved / peak, 4), "traffic": traffic,
@@ -573,6 +588,7 @@ def main() -> None:
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--kinds", default="", help="comma-separated subset of schedules")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
+    ap.add_argument("--no-core", action="store_true", help="skip the comm_agent=core (SM copies) comparison")
     ap.add_argument("--input", default="slot", choices=["slot", "copy"],
                     help="slot: the A shard is produced in the group's symmetric input slot (zero-copy publish, "
                          "FiccoGroup.input_slot); copy: an ordinary tensor copied in by the op")

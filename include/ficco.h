@@ -163,8 +163,13 @@ typedef struct {
   int32_t tile_n;     /* tile width (UMMA N): 128, 160, 192, 224 or 256 (0: 256) */
   int32_t cta_group;  /* 1: one CTA per 128-row tile; 2: CTA pairs, tiles (2p, 2p+1) share b_row/c_col
                          and form one 256-row UMMA (0: 1) */
-  int32_t reserved;
+  int32_t hints;      /* FICCO_HINT_* bits (0: defaults) */
 } ficco_plan_desc;
+
+/* ficco_plan_desc.hints */
+#define FICCO_HINT_A_EVICT_LAST 1 /* A is small and re-read by every column tile: keep it in L2 */
+#define FICCO_HINT_CORE_COPIES 2  /* comm_agent = core: workspace-to-workspace transfers run as SM copy
+                                     kernels (P2P loads/stores) instead of copy-engine memcpys */
 
 int ficco_abi_version(void);
 const char* ficco_last_error(void);

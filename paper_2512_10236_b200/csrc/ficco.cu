@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "../../include/ficco.h"
+#include "copy_kernel.cuh"
 #include "tile_kernel.cuh"
 
 namespace {
@@ -234,13 +235,36 @@ int resolve(ficco_comm* c, uint32_t parity, int buf, int peer, int64_t off, int6
 
 bool is_user(int buf) { return buf == FICCO_BUF_A || buf == FICCO_BUF_B || buf == FICCO_BUF_C; }
 
+int core_copy_ctas() {
+  static const int n = [] {
+    const char* env = getenv("FICCO_CORE_COPY_CTAS");
+    const int v = env ? atoi(env) : 0;
+    return v > 0 ? v : 32;
+  }();
+  return n;
+}
+
 int enqueue_copy(ficco_comm* cm, uint32_t parity, const ficco_copy_op& op, const void* a, const void* b, void* c,
-                 cudaStream_t s) {
+                 cudaStream_t s, bool core) {
   uint8_t *src, *dst;
   int r = resolve(cm, parity, op.src_buf, op.peer, op.src_off, op.src_par, a, b, c, &src);
   if (r) return r;
   r = resolve(cm, parity, op.dst_buf, op.dst_peer, op.dst_off, op.dst_par, a, b, c, &dst);
   if (r) return r;
+  const int64_t height = op.height <= 1 ? 1 : op.height;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst) | uint64_t(op.width) |
+                         (height > 1 ? uint64_t(op.src_pitch | op.dst_pitch) : 0)) & 15) == 0;
+  if (core && op.src_buf == FICCO_BUF_WS && op.dst_buf == FICCO_BUF_WS && aligned) {
+    // comm_agent = core: the transfer runs on SMs (P2P loads / stores), next to the tile kernel
+    const int64_t vecs = op.width / 16 * height;
+    const int64_t need = (vecs + ficco::COPY_THREADS * ficco::COPY_UNROLL - 1) / (ficco::COPY_THREADS * ficco::COPY_UNROLL);
+    const int grid = int(need < core_copy_ctas() ? (need > 0 ? need : 1) : core_copy_ctas());
+    ficco::sm_copy_kernel<<<grid, ficco::COPY_THREADS, 0, s>>>(dst, src, op.width, height,
+                                                               height > 1 ? op.src_pitch : op.width,
+                                                               height > 1 ? op.dst_pitch : op.width);
+    CK(cudaGetLastError());
+    return 0;
+  }
   if (op.height <= 1) {
     CK(cudaMemcpyAsync(dst, src, size_t(op.width), cudaMemcpyDefault, s));
   } else {
@@ -277,7 +301,7 @@ int enqueue_run(ficco_plan* p, uint32_t parity, const void* a, const void* b, vo
       cudaStream_t cs = cm->copy[op.stream];
       switch (op.op) {
         case FICCO_OP_COPY: {
-          int r = enqueue_copy(cm, parity, op, a, b, c, cs);
+          int r = enqueue_copy(cm, parity, op, a, b, c, cs, (p->desc.hints & FICCO_HINT_CORE_COPIES) != 0);
           if (r) return r;
           if (is_user(op.src_buf) || is_user(op.dst_buf)) {  // remember it for graph re-pointing
             cudaStreamCaptureStatus st;
@@ -441,6 +465,7 @@ int make_params(ficco_plan* p, uint32_t parity, const void* a, const void* b, vo
   prm->abort_word = cm->flags(cm->rank) + FICCO_FLAG_ABORT;
   prm->epoch = 1u;  // one-shot flags: wait for != 0
   prm->alpha = d.alpha;
+  prm->a_evict_last = (d.hints & FICCO_HINT_A_EVICT_LAST) != 0;
   prm->trace = p->trace;
   int g = d.grid > 0 ? d.grid : cm->sms;
   if (g > p->n_tiles) g = p->n_tiles;
@@ -932,6 +957,11 @@ int ficco_gemm_bf16_cfg(const void* a, const void* b, void* c, int64_t m, int64_
   p->desc.c = ficco_operand{FICCO_BUF_C, 0, 0, 0, m, n};
   p->desc.k = k;
   p->desc.alpha = alpha;
+  {
+    const char* env = getenv("FICCO_A_EVICT_LAST");  // "0" / "1" override the size rule (A/B experiments)
+    const bool pin = env && env[0] != 'a' ? env[0] == '1' : m * k * 2 <= (int64_t(32) << 20);  // lowering.A_PIN_BYTES
+    p->desc.hints = pin ? FICCO_HINT_A_EVICT_LAST : 0;
+  }
   return ficco_plan_run_parts(p, a, b, c, stream, 0, 1);  // no flags: direct launch
 }
 

@@ -57,7 +57,10 @@ constexpr int SMEM_LIMIT = 226 * 1024;  // leaves room for the static smem (seen
 // box (128 B rows, TMA SWIZZLE_128B layout: full-line writes), stored with
 // cp.async.bulk.tensor; a trailing 32-column chunk uses a 32 x 32 box (SWIZZLE_64B).
 constexpr int EPI_BUF_BYTES = 32 * 128;
-constexpr int EPI_BUFS = 1;
+#ifndef FICCO_EPI_BUFS
+#define FICCO_EPI_BUFS 1
+#endif
+constexpr int EPI_BUFS = FICCO_EPI_BUFS;  // staging buffers per epilogue warp (bulk stores in flight)
 
 // Per (tile width, CTA group) configuration: as many pipeline stages as fit.
 template <int TN, int CG>
@@ -103,6 +106,7 @@ struct alignas(64) TileParams {
   int rs_flag0;
   int reduce_mma;          // REDUCE tiles fold the peers' partials in with identity MMAs (else epilogue loads)
   int recv_rows;           // rows per receive slot in tmap_recv (slot j starts at row j * recv_rows)
+  int a_evict_last;        // FICCO_HINT_A_EVICT_LAST
   int part_hint;           // L2 policy of STORE_SIGNAL (to-be-pushed) stores: 0 evict_first, 1 normal, 2 last
   uint32_t* flags;         // local flag block of this run's parity
   uint32_t* counters;      // local tile counters
@@ -156,7 +160,7 @@ template <int TN, int CG>
 __device__ __forceinline__ void producer_loop(const TileParams& p, uint8_t* sA, uint8_t* sB, uint64_t* full,
                                               uint64_t* empty, uint32_t rank, uint32_t* seen) {
   using Cfg = TileCfg<TN, CG>;
-  const uint64_t hint_a = policy_evict_first();
+  const uint64_t hint_a = p.a_evict_last ? policy_evict_last() : policy_evict_first();
   const uint64_t hint_b = policy_evict_last();
   uint32_t stage = 0, phase = 0;
   for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
@@ -356,7 +360,7 @@ __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfu
   const uint64_t hint_part = p.part_hint == 2 ? policy_evict_last()
                              : p.part_hint == 1 ? policy_evict_normal() : hint_out;
   uint8_t* buf = stage_smem + (warp - 2) * (EPI_BUFS * EPI_BUF_BYTES);
-  bool pending = false;  // a bulk store still reading `buf`
+  uint32_t bi = 0;  // staging buffer of the next bulk store (round robin over EPI_BUFS)
   uint32_t it = 0;
   for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
     const ficco_tile td = p.tiles[t];
@@ -389,7 +393,8 @@ __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfu
       const bool live1 = col + 64 <= TN && col + 32 < td.cols;  // warp-uniform
       if (col >= td.cols) continue;
       if (tma) {
-        if (lane == 0 && pending) tma_store_wait_read<0>();  // the staging buffer drained
+        // the buffer about to be refilled was handed to the store issued EPI_BUFS stores ago
+        if (lane == 0) tma_store_wait_read<EPI_BUFS - 1>();
         __syncwarp();
       }
       // the two 32-column halves one after the other: one half's values live at a time
@@ -400,7 +405,8 @@ __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfu
         if (tma) {
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            *reinterpret_cast<uint4*>(buf + (live1 ? swz128(lane, 4 * h + q) : swz64(lane, q))) = w[q];
+            *reinterpret_cast<uint4*>(buf + bi * EPI_BUF_BYTES + (live1 ? swz128(lane, 4 * h + q) : swz64(lane, q))) =
+                w[q];
         } else if (row_ok) {
           uint4* o = reinterpret_cast<uint4*>(dst + col + 32 * h);
 #pragma unroll
@@ -411,11 +417,11 @@ __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfu
         fence_async_shared();
         __syncwarp();
         if (lane == 0) {
-          tma_store_2d_hint(live1 ? map64 : map32, buf, td.c_col + col, td.c_row + quarter * 32,
-                            signal ? hint_part : hint_out);
+          tma_store_2d_hint(live1 ? map64 : map32, buf + bi * EPI_BUF_BYTES, td.c_col + col,
+                            td.c_row + quarter * 32, signal ? hint_part : hint_out);
           tma_store_commit();
         }
-        pending = true;
+        bi = bi + 1 == EPI_BUFS ? 0 : bi + 1;
       }
     }
     tc_fence_before();

@@ -42,6 +42,7 @@ transposed-operand variants of the same chunk routing (see ``lower_rs`` /
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 
 from .domain import Scenario
@@ -66,6 +67,17 @@ EV_START = 0     # event slot: the cross-rank barrier passed
 MAX_WORLD = 16
 
 ELT = 2  # bf16
+A_PIN_BYTES = 32 << 20  # A operands up to this size are kept in L2 (evict_last) when re-read per column tile
+FICCO_HINT_A_EVICT_LAST = 1  # include/ficco.h
+FICCO_HINT_CORE_COPIES = 2
+
+
+def _agent_hint(comm_agent) -> int:
+    """comm_agent (the reference's CommAgent, machines.py:48): 'dma' = copy engines, 'core' = SM copies."""
+    agent = getattr(comm_agent, "value", comm_agent)
+    if agent not in ("dma", "core"):
+        raise ValueError(f"comm_agent must be 'dma' or 'core', got {comm_agent!r}")
+    return FICCO_HINT_CORE_COPIES if agent == "core" else 0
 
 
 @dataclass
@@ -197,7 +209,8 @@ def _peer_stream(p: int, g: int) -> int:
 
 
 def lower_ag(plan: ExecutionPlan, rank: int, gathered: str = "A", alpha: float = 1.0, grid: int = 0,
-             other_rows: int | None = None, cta_group: int = DEFAULT_CTA_GROUP, inplace: bool = False) -> Lowered:
+             other_rows: int | None = None, cta_group: int = DEFAULT_CTA_GROUP, inplace: bool = False,
+             comm_agent: str = "dma") -> Lowered:
     """All-gather -> GEMM family (AG->GEMM and the CP KV-gather -> QK^T).
 
     gathered="A": C[M,N] = A_all[M,K] @ W[N,K]^T; call args (a=A_shard[R,K], b=W, c=C).
@@ -367,7 +380,15 @@ def lower_ag(plan: ExecutionPlan, rank: int, gathered: str = "A", alpha: float =
     d.part = _operand(BUF_NONE, 0, 0)
     d.recv = _operand(BUF_NONE, 0, 0)
     d.k, d.alpha, d.grid, d.tile_n, d.cta_group = K, alpha, grid, tn, cta_group
-    low.notes = {"kind": kind.value, "rank": g, "world": G, "gathered": gathered, "inplace": inplace}
+    # a small A (CP: Q, a few MiB) is re-read by every column tile while the output streams
+    # through L2 (4 GiB of scores in C4) — pin it (evict_last) instead of the default evict_first
+    a_bytes = (Q if gathered == "B" else M) * K * ELT
+    if os.environ.get("FICCO_A_EVICT_LAST", "auto") == "1" or (
+            os.environ.get("FICCO_A_EVICT_LAST", "auto") == "auto" and a_bytes <= A_PIN_BYTES):
+        d.hints |= FICCO_HINT_A_EVICT_LAST
+    d.hints |= _agent_hint(comm_agent)
+    low.notes = {"kind": kind.value, "rank": g, "world": G, "gathered": gathered, "inplace": inplace,
+                 "comm_agent": comm_agent}
     return low
 
 
@@ -379,7 +400,7 @@ def rs_plan(scenario: Scenario, kind: ScheduleKind) -> ExecutionPlan:
 
 
 def lower_rs(scenario: Scenario, kind: ScheduleKind, rank: int, grid: int = 0, virtual: bool = False,
-             cta_group: int = DEFAULT_CTA_GROUP) -> Lowered:
+             cta_group: int = DEFAULT_CTA_GROUP, comm_agent: str = "dma") -> Lowered:
     """GEMM -> reduce-scatter (not in the reference, parity unpinned).
 
     Rank g holds A_g [M, Kg] and W_g [N, Kg]; P_g = A_g @ W_g^T [M, N]; rank q
@@ -482,10 +503,11 @@ def lower_rs(scenario: Scenario, kind: ScheduleKind, rank: int, grid: int = 0, v
     d.recv_slot, d.n_recv, d.rs_flag0 = low.recv_slot, G - 1, F_RS
     d.n_counters = len(units)
     d.k, d.alpha, d.grid, d.tile_n, d.cta_group = K, 1.0, grid, tn, cta_group
+    d.hints |= _agent_hint(comm_agent)
     if len(units) >= 4096 - 1:
         raise PlanError("too many push units")
     if F_RS + G * (G - 1) >= 4096:
         raise PlanError("too many ranks for the RS flag area")
     low.notes = {"kind": kind.value, "rank": g, "world": G, "op": "rs", "units": len(units),
-                 "tiles_per_chunk": tiles_per_chunk}
+                 "tiles_per_chunk": tiles_per_chunk, "comm_agent": comm_agent}
     return low

@@ -188,16 +188,17 @@ def _cached(grp: FiccoGroup, key, make):
     return hit
 
 
-def prepare_ag(grp: FiccoGroup, R: int, K: int, N: int, kind=None, inplace: bool = False):
+def prepare_ag(grp: FiccoGroup, R: int, K: int, N: int, kind=None, inplace: bool = False, comm_agent: str = "dma"):
     """Build (or fetch) the lowered AG->GEMM plan for this rank: (plan, lowered, kind)."""
     def make():
         M = R * grp.world
         sc = _scenario("ag_gemm", M, N, K, grp.world)
         kd = choose_kind(sc, kind)
-        plan, low = grp.plan(("ag", M, N, K, kd, inplace),
-                             lambda: lower_ag(build_plan(sc, kd), grp.rank, "A", inplace=inplace))
+        plan, low = grp.plan(("ag", M, N, K, kd, inplace, comm_agent),
+                             lambda: lower_ag(build_plan(sc, kd), grp.rank, "A", inplace=inplace,
+                                              comm_agent=comm_agent))
         return plan, low, kd
-    return _cached(grp, ("ag", R, K, N, kind, inplace), make)
+    return _cached(grp, ("ag", R, K, N, kind, inplace, comm_agent), make)
 
 
 def _is_slot(grp: FiccoGroup, t: torch.Tensor, low) -> bool:
@@ -210,44 +211,49 @@ def _is_slot(grp: FiccoGroup, t: torch.Tensor, low) -> bool:
     return t.data_ptr() == want
 
 
-def prepare_rs(grp: FiccoGroup, M: int, K: int, N: int, kind=None):
+def prepare_rs(grp: FiccoGroup, M: int, K: int, N: int, kind=None, comm_agent: str = "dma"):
     def make():
         sc = _scenario("gemm_rs", M, N, K, grp.world)
         kd = choose_kind(sc, kind)
         if kd not in (ScheduleKind.UNIFORM_FUSED_1D, ScheduleKind.HETERO_FUSED_1D, ScheduleKind.HETERO_UNFUSED_1D):
             kd = ScheduleKind.HETERO_FUSED_1D  # the 2D/serial choices have no RS adjoint on this executor
-        plan, low = grp.plan(("rs", M, N, K, kd), lambda: lower_rs(sc, kd, grp.rank, virtual=grp.virtual))
+        plan, low = grp.plan(("rs", M, N, K, kd, comm_agent),
+                             lambda: lower_rs(sc, kd, grp.rank, virtual=grp.virtual, comm_agent=comm_agent))
         return plan, low, kd
-    return _cached(grp, ("rs", M, K, N, kind), make)
+    return _cached(grp, ("rs", M, K, N, kind, comm_agent), make)
 
 
-def prepare_cp(grp: FiccoGroup, Tq: int, d: int, Tkv: int, kind=None, scale: float | None = None):
+def prepare_cp(grp: FiccoGroup, Tq: int, d: int, Tkv: int, kind=None, scale: float | None = None,
+               comm_agent: str = "dma"):
     def make():
         sc = _scenario("cp_qk", Tkv, Tq, d, grp.world)
         kd = choose_kind(sc, kind)
         if kd is ScheduleKind.UNIFORM_FUSED_2D:
             kd = ScheduleKind.UNIFORM_FUSED_1D  # K=d is a single k-segment; the 2D split does not apply
         alpha = (1.0 / math.sqrt(d)) if scale is None else scale
-        plan, low = grp.plan(("cp", Tkv, Tq, d, kd, alpha),
-                             lambda: lower_ag(build_plan(sc, kd), grp.rank, "B", alpha=alpha, other_rows=Tq))
+        plan, low = grp.plan(("cp", Tkv, Tq, d, kd, alpha, comm_agent),
+                             lambda: lower_ag(build_plan(sc, kd), grp.rank, "B", alpha=alpha, other_rows=Tq,
+                                              comm_agent=comm_agent))
         return plan, low, kd
-    return _cached(grp, ("cp", Tq, d, Tkv, kind, scale), make)
+    return _cached(grp, ("cp", Tq, d, Tkv, kind, scale, comm_agent), make)
 
 
 def all_gather_matmul(a_shard: torch.Tensor, weight: torch.Tensor, kind=None, group: FiccoGroup | None = None,
-                      out: torch.Tensor | None = None, stream=None, return_gathered: bool = False):
+                      out: torch.Tensor | None = None, stream=None, return_gathered: bool = False,
+                      comm_agent: str = "dma"):
     """C = all_gather(A_shard) @ W^T with FiCCO overlap. A_shard [R, K], W [N, K] -> C [G*R, N].
 
     ``return_gathered`` also returns the gathered A (a view into the group's
-    double-buffered workspace, valid until the call after next).
+    double-buffered workspace, valid until the call after next). ``comm_agent``
+    'dma' moves chunks with the copy engines, 'core' with SM copy kernels.
     """
     grp = _default_group(group, None)
     R, K = a_shard.shape
     N = weight.shape[0]
     M = R * grp.world
-    plan, low, kd = prepare_ag(grp, R, K, N, kind)
+    plan, low, kd = prepare_ag(grp, R, K, N, kind, comm_agent=comm_agent)
     if _is_slot(grp, a_shard, low):  # zero-copy publish: the shard already sits in its slot
-        plan, low, _ = prepare_ag(grp, R, K, N, kd, inplace=True)
+        plan, low, _ = prepare_ag(grp, R, K, N, kd, inplace=True, comm_agent=comm_agent)
     if out is None:
         out = torch.empty(M, N, dtype=torch.bfloat16, device=a_shard.device)
     if SERIALIZE:
@@ -262,12 +268,12 @@ def all_gather_matmul(a_shard: torch.Tensor, weight: torch.Tensor, kind=None, gr
 
 
 def matmul_reduce_scatter(a: torch.Tensor, weight: torch.Tensor, kind=None, group: FiccoGroup | None = None,
-                          out: torch.Tensor | None = None, stream=None):
+                          out: torch.Tensor | None = None, stream=None, comm_agent: str = "dma"):
     """C_shard = reduce_scatter_rows(A @ W^T). A [M, Kg], W [N, Kg] -> [M/G, N] (this rank's rows)."""
     grp = _default_group(group, None)
     M, K = a.shape
     N = weight.shape[0]
-    plan, _, _ = prepare_rs(grp, M, K, N, kind)
+    plan, _, _ = prepare_rs(grp, M, K, N, kind, comm_agent=comm_agent)
     if out is None:
         out = torch.empty(M // grp.world, N, dtype=torch.bfloat16, device=a.device)
     if SERIALIZE:
@@ -278,7 +284,8 @@ def matmul_reduce_scatter(a: torch.Tensor, weight: torch.Tensor, kind=None, grou
 
 
 def cp_kv_all_gather_qk(q: torch.Tensor, k_shard: torch.Tensor, kind=None, scale: float | None = None,
-                        group: FiccoGroup | None = None, out: torch.Tensor | None = None, stream=None):
+                        group: FiccoGroup | None = None, out: torch.Tensor | None = None, stream=None,
+                        comm_agent: str = "dma"):
     """S = scale * Q @ all_gather(K_shard)^T. Q [Tq, d], K_shard [Tkv/G, d] -> S [Tq, Tkv] (bf16).
 
     Scenario view: M = Tkv (gathered kv tokens), N = Tq, K = d.
@@ -286,7 +293,7 @@ def cp_kv_all_gather_qk(q: torch.Tensor, k_shard: torch.Tensor, kind=None, scale
     grp = _default_group(group, None)
     Tq, d = q.shape
     Tkv = k_shard.shape[0] * grp.world
-    plan, _, _ = prepare_cp(grp, Tq, d, Tkv, kind, scale)
+    plan, _, _ = prepare_cp(grp, Tq, d, Tkv, kind, scale, comm_agent=comm_agent)
     if out is None:
         out = torch.empty(Tq, Tkv, dtype=torch.bfloat16, device=q.device)
     if SERIALIZE:

@@ -72,7 +72,7 @@ class PlanDesc(C.Structure):
                 ("recv", Operand), ("a2", Operand), ("b2", Operand), ("recv_slot", C.c_int64), ("k", C.c_int64),
                 ("n_recv", C.c_int32),
                 ("rs_flag0", C.c_int32), ("n_counters", C.c_int32), ("grid", C.c_int32), ("alpha", C.c_float),
-                ("tile_n", C.c_int32), ("cta_group", C.c_int32), ("reserved", C.c_int32)]
+                ("tile_n", C.c_int32), ("cta_group", C.c_int32), ("hints", C.c_int32)]
 
 
 assert C.sizeof(CopyOp) == 96 and C.sizeof(Tile) == 40 and C.sizeof(Operand) == 40

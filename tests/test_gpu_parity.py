@@ -157,9 +157,80 @@ def test_ag_input_slot_zero_copy(lib, kind):
             slot.copy_(_t(shards[rank]))
             out, gathered = ops.all_gather_matmul(slot, _t(w), kind=kind, group=grp, return_gathered=True)
             grp.comm.check()
-            assert ("ag", R * G, N, K, ops.ScheduleKind(kind), True) in grp._plans  # the in-place plan ran
+            assert ("ag", R * G, N, K, ops.ScheduleKind(kind), True, "dma") in grp._plans  # the in-place plan ran
             full = np.concatenate(shards)
             assert np.array_equal(_np(gathered), full)
             np.testing.assert_allclose(_np(out), full @ w.T, rtol=RTOL, atol=ATOL)
+    finally:
+        grp.close()
+
+
+@pytest.mark.parametrize("kind", AG_KINDS)
+def test_ag_core_agent_matches_oracle(lib, kind):
+    """comm_agent='core': the transfers run as SM copy kernels beside the tile kernel; same results."""
+    from paper_2512_10236_b200 import ops
+    G, rank, R, K, N = 4, 3, 512, 1024, 768
+    shards = [orc.seeded_inputs(2, p, (R, K)) for p in range(G)]
+    w = orc.seeded_inputs(2, 99, (N, K), "normal")
+    gathered_ref, outs = orc.execute_ag(kind, shards, w)
+    grp = ops.FiccoGroup.virtual_group(G, rank)
+    try:
+        _, low, _ = ops.prepare_ag(grp, R, K, N, kind, comm_agent="core")
+        assert low.desc.hints & 2
+        grp.load_peer_shards(low, [_t(s) for s in shards])
+        for it in range(3):
+            out, gathered = ops.all_gather_matmul(_t(shards[rank]), _t(w), kind=kind, group=grp,
+                                                  return_gathered=True, comm_agent="core")
+            grp.comm.check()
+            assert np.array_equal(_np(gathered), gathered_ref[rank]), (kind, it)
+            np.testing.assert_allclose(_np(out), outs[rank], rtol=RTOL, atol=ATOL)
+    finally:
+        grp.close()
+
+
+@pytest.mark.parametrize("kind", ["uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d"])
+def test_rs_core_agent_matches_oracle(lib, kind):
+    from paper_2512_10236_b200 import ops
+    G, rank = 4, 2
+    M, Kg, N = 128 * G * G, 256, 512
+    a = [orc.seeded_inputs(8, p, (M, Kg)) for p in range(G)]
+    w = [orc.seeded_inputs(8, 100 + p, (N, Kg), "normal") for p in range(G)]
+    want = orc.execute_rs(a, w)[rank]
+    R = M // G
+    peers = [orc.bf16_round(a[p] @ w[p].T)[rank * R:(rank + 1) * R] for p in range(G) if p != rank]
+    grp = ops.FiccoGroup.virtual_group(G, rank)
+    try:
+        _, low, _ = ops.prepare_rs(grp, M, Kg, N, kind, comm_agent="core")
+        grp.load_peer_partials(low, [_t(x) for x in peers])
+        for _ in range(2):
+            out = ops.matmul_reduce_scatter(_t(a[rank]), _t(w[rank]), kind=kind, group=grp, comm_agent="core")
+            grp.comm.check()
+            np.testing.assert_allclose(_np(out), want, rtol=RTOL, atol=ATOL * math.sqrt(G))
+        # the pushes really happened: every remote owner's receive slot holds our partial chunks
+        # (GPU-rounded partials: within the GEMM tolerance of the fp32 product, not bit-equal)
+        part = a[rank] @ w[rank].T
+        for q in range(G):
+            if q == rank:
+                continue
+            slot = rank if rank < q else rank - 1
+            got = grp.ws_tensor(q, low.recv_off + slot * low.recv_slot, (R, N))
+            np.testing.assert_allclose(_np(got), part[q * R:(q + 1) * R], rtol=RTOL, atol=ATOL)
+    finally:
+        grp.close()
+
+
+def test_cp_core_agent_matches_oracle(lib):
+    from paper_2512_10236_b200 import ops
+    G, rank, d, Tq, Tkv = 4, 1, 128, 384, 4096
+    q = orc.seeded_inputs(9, 50, (Tq, d), "normal")
+    ks = [orc.seeded_inputs(9, p, (Tkv // G, d), "normal") for p in range(G)]
+    want, _ = orc.execute_cp_qk(q, ks, 1.0 / math.sqrt(d))
+    grp = ops.FiccoGroup.virtual_group(G, rank)
+    try:
+        _, low, _ = ops.prepare_cp(grp, Tq, d, Tkv, "hetero_unfused_1d", comm_agent="core")
+        grp.load_peer_shards(low, [_t(x) for x in ks])
+        out = ops.cp_kv_all_gather_qk(_t(q), _t(ks[rank]), kind="hetero_unfused_1d", group=grp, comm_agent="core")
+        grp.comm.check()
+        np.testing.assert_allclose(_np(out), want, rtol=RTOL, atol=ATOL)
     finally:
         grp.close()
