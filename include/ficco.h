@@ -229,6 +229,9 @@ int ficco_copy_batch(void* const* dsts, const void* const* srcs, const size_t* s
  * nanoseconds: copies issued meanwhile progress only if a copy engine executes them
  * (copy-engine vs SM-copy-kernel probe; CIL calibration). */
 int ficco_occupy_sms(int64_t ns, void* stream);
+/* Write the %globaltimer (ns, same clock as ficco_plan_set_trace stamps) to device u64 *dst,
+ * stream-ordered: marks an op's start/end on the tile kernel's timeline. */
+int ficco_timestamp(void* dst, void* stream);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

@@ -120,14 +120,20 @@ int encode_bf16_2d(Driver* drv, CUtensorMap* map, const void* base, int64_t rows
   return 0;
 }
 
-// Resolve the (tile width, CTA group) instantiation: entry point, dynamic smem, B box rows.
-int kernel_for(int tn, int cg, const void** fn, int* smem, int* b_rows) {
-#define FICCO_CASE(T, G)                                                  \
-  if (tn == T && cg == G) {                                               \
-    *fn = reinterpret_cast<const void*>(ficco::tile_gemm_kernel<T, G>);   \
-    *smem = ficco::TileCfg<T, G>::SMEM_BYTES;                             \
-    *b_rows = ficco::TileCfg<T, G>::B_ROWS;                               \
-    return 0;                                                             \
+// Epilogue staging buffers per warp: short-K tile programs (a handful of k-blocks per tile,
+// e.g. C4's d = 128) are paced by the epilogue's TMEM reads and stores, so they keep 3 bulk
+// stores in flight per warp; long-K programs are MMA-bound and keep the smem for stages.
+int epi_bufs_for(int64_t k) { return k <= 384 ? 3 : 1; }
+
+// Resolve the (tile width, CTA group, staging buffers) instantiation: entry point, dynamic smem,
+// B box rows.
+int kernel_for(int tn, int cg, int eb, const void** fn, int* smem, int* b_rows) {
+#define FICCO_CASE(T, G, E)                                                  \
+  if (tn == T && cg == G && eb == E) {                                       \
+    *fn = reinterpret_cast<const void*>(ficco::tile_gemm_kernel<T, G, E>);   \
+    *smem = ficco::TileCfg<T, G, E>::SMEM_BYTES;                             \
+    *b_rows = ficco::TileCfg<T, G, E>::B_ROWS;                               \
+    return 0;                                                                \
   }
   FICCO_FOR_EACH_CFG(FICCO_CASE)
 #undef FICCO_CASE
@@ -137,12 +143,12 @@ int kernel_for(int tn, int cg, const void** fn, int* smem, int* b_rows) {
 int configure_kernels(int dev) {
   static int configured = -1;
   if (configured == dev) return 0;
-#define FICCO_CFG(T, G)                                                                              \
-  CK(cudaFuncSetAttribute(ficco::tile_gemm_kernel<T, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                          ficco::TileCfg<T, G>::SMEM_BYTES));                          \
-  {                                                                                                  \
-    cudaFuncAttributes fa;                                                                           \
-    CK(cudaFuncGetAttributes(&fa, ficco::tile_gemm_kernel<T, G>));                                   \
+#define FICCO_CFG(T, G, E)                                                                              \
+  CK(cudaFuncSetAttribute(ficco::tile_gemm_kernel<T, G, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                          ficco::TileCfg<T, G, E>::SMEM_BYTES));                                        \
+  {                                                                                                     \
+    cudaFuncAttributes fa;                                                                              \
+    CK(cudaFuncGetAttributes(&fa, ficco::tile_gemm_kernel<T, G, E>));                                   \
     if (fa.numRegs * ficco::NUM_THREADS > 65536 - ficco::COPY_RESERVE_REGS)                          \
       return fail(FICCO_ECUDA, "tile kernel register use leaves no room for copy kernels");      \
   }
@@ -163,6 +169,8 @@ __global__ void __launch_bounds__(1024, 1) occupy_kernel(int64_t ns) {
   if (threadIdx.x == 0) occ_smem[0] = 1;
   while (int64_t(globaltimer() - t0) < ns) __nanosleep(256);
 }
+// One %globaltimer stamp, stream-ordered (op-boundary marks for the tile kernel's trace).
+__global__ void stamp_kernel(unsigned long long* dst) { *dst = globaltimer(); }
 }  // namespace ficco
 
 struct ficco_comm {
@@ -207,6 +215,7 @@ struct ficco_plan {
   // so the kernel that would satisfy the wait never starts.
   bool kernel_in_graph = true;
   int tile_n = 256;                     // tile width (UMMA N)
+  int epi_bufs = 1;                     // epilogue staging buffers per warp (epi_bufs_for)
   int cta_group = 1;                    // 1: one CTA per tile; 2: CTA pair (cluster of 2, UMMA M = 256)
   ficco_plan_desc desc{};
   GraphInst graph[2];
@@ -395,7 +404,7 @@ int make_params(ficco_plan* p, uint32_t parity, const void* a, const void* b, vo
   {
     const void* fn;
     int smem, b_rows;
-    if ((r = kernel_for(p->tile_n, p->cta_group, &fn, &smem, &b_rows))) return r;
+    if ((r = kernel_for(p->tile_n, p->cta_group, p->epi_bufs, &fn, &smem, &b_rows))) return r;
     if ((r = encode_bf16_2d(cm->drv, &prm->tmap_b, pb, d.b.rows, d.k, d.b.ld, b_rows))) return r;
     prm->tmap_a2 = prm->tmap_a;
     prm->tmap_b2 = prm->tmap_b;
@@ -481,7 +490,7 @@ int launch_tiles(ficco_plan* p, uint32_t parity, const void* a, const void* b, v
   ficco::TileParams prm;
   int grid, smem, b_rows;
   const void* fn;
-  if ((r = kernel_for(p->tile_n, p->cta_group, &fn, &smem, &b_rows))) return r;
+  if ((r = kernel_for(p->tile_n, p->cta_group, p->epi_bufs, &fn, &smem, &b_rows))) return r;
   if ((r = make_params(p, parity, a, b, c, &prm, &grid))) return r;
   void* args[] = {&prm};
   cudaLaunchConfig_t cfg{};
@@ -554,7 +563,7 @@ int repoint_graph(ficco_plan* p, uint32_t parity, const void* a, const void* b, 
     void* args[] = {&prm};
     const void* fn;
     int smem, b_rows;
-    if ((r = kernel_for(p->tile_n, p->cta_group, &fn, &smem, &b_rows))) return r;
+    if ((r = kernel_for(p->tile_n, p->cta_group, p->epi_bufs, &fn, &smem, &b_rows))) return r;
     cudaKernelNodeParams kp{};
     kp.func = const_cast<void*>(fn);
     kp.gridDim = dim3(grid);
@@ -724,7 +733,7 @@ int ficco_plan_create(ficco_comm_t* c, const ficco_plan_desc* d, ficco_plan_t** 
   {
     const void* fn;
     int smem, b_rows;
-    int r = kernel_for(tile_n, cta_group, &fn, &smem, &b_rows);
+    int r = kernel_for(tile_n, cta_group, epi_bufs_for(d->k), &fn, &smem, &b_rows);
     if (r) return r;
     if (cta_group == 2 && d->n_tiles % 2) return fail(FICCO_EINVAL, "cta_group 2 needs an even tile list (pairs)");
   }
@@ -766,6 +775,7 @@ int ficco_plan_create(ficco_comm_t* c, const ficco_plan_desc* d, ficco_plan_t** 
   p->n_tiles = d->n_tiles;
   p->tile_n = tile_n;
   p->cta_group = cta_group;
+  p->epi_bufs = epi_bufs_for(d->k);
   {
     const char* env = getenv("FICCO_KERNEL_IN_GRAPH");
     p->kernel_in_graph = !(env && env[0] == '0');
@@ -855,6 +865,12 @@ int ficco_plan_run(ficco_plan_t* p, const void* a, const void* b, void* c, void*
   CK(cudaGraphLaunch(gi.exec, gs));
   CK(cudaEventRecord(cm->ev_join[0], gs));
   CK(cudaStreamWaitEvent(s, cm->ev_join[0], 0));
+  return 0;
+}
+
+int ficco_timestamp(void* dst, void* stream) {
+  ficco::stamp_kernel<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(reinterpret_cast<unsigned long long*>(dst));
+  CK(cudaGetLastError());
   return 0;
 }
 
@@ -956,6 +972,7 @@ int ficco_gemm_bf16_cfg(const void* a, const void* b, void* c, int64_t m, int64_
   p->desc.b = ficco_operand{FICCO_BUF_B, 0, 0, 0, n, k};
   p->desc.c = ficco_operand{FICCO_BUF_C, 0, 0, 0, m, n};
   p->desc.k = k;
+  p->epi_bufs = epi_bufs_for(k);
   p->desc.alpha = alpha;
   {
     const char* env = getenv("FICCO_A_EVICT_LAST");  // "0" / "1" override the size rule (A/B experiments)

@@ -53,24 +53,24 @@ constexpr uint32_t TMEM_COLS = 512;  // two accumulators of up to 256 fp32 colum
 constexpr int MAX_RECV = 15;
 constexpr uint32_t SPIN_LIMIT = 1u << 25;  // ~4-10 s of polling before declaring a timeout
 constexpr int SMEM_LIMIT = 226 * 1024;  // leaves room for the static smem (seen-flag bitset)
-// Epilogue output staging: per epilogue warp EPI_BUFS buffers of one 32-row x 64-column bf16
+// Epilogue output staging: per epilogue warp EB buffers of one 32-row x 64-column bf16
 // box (128 B rows, TMA SWIZZLE_128B layout: full-line writes), stored with
 // cp.async.bulk.tensor; a trailing 32-column chunk uses a 32 x 32 box (SWIZZLE_64B).
+// EB staging buffers per warp keep EB bulk stores in flight: 1 for long-K (MMA-bound) tile
+// programs, where smem is better spent on pipeline stages, 3 for short-K programs (C4's
+// d = 128), whose tiles are store-bound (see lowering.epi_bufs_for / ficco.cu epi_bufs_for).
 constexpr int EPI_BUF_BYTES = 32 * 128;
-#ifndef FICCO_EPI_BUFS
-#define FICCO_EPI_BUFS 1
-#endif
-constexpr int EPI_BUFS = FICCO_EPI_BUFS;  // staging buffers per epilogue warp (bulk stores in flight)
 
 // Per (tile width, CTA group) configuration: as many pipeline stages as fit.
-template <int TN, int CG>
+template <int TN, int CG, int EB = 1>
 struct TileCfg {
   static_assert(TN % 32 == 0 && TN >= 64 && TN <= 256, "tile width");
   static_assert(CG == 1 || CG == 2, "cta group");
   static constexpr int B_ROWS = TN / CG;  // B rows loaded by each CTA
   static constexpr int B_STAGE = B_ROWS * BK * 2;
   static constexpr int STAGE = A_STAGE + B_STAGE;
-  static constexpr int EPI_STAGE_BYTES = EPI_BUFS * EPI_BUF_BYTES * EPI_WARPS;  // TMA-store staging
+  static_assert(EB >= 1 && EB <= 4, "epilogue staging buffers");
+  static constexpr int EPI_STAGE_BYTES = EB * EPI_BUF_BYTES * EPI_WARPS;  // TMA-store staging
   static constexpr int MAX_STAGES = (SMEM_LIMIT - 1024 - 256 - EPI_STAGE_BYTES) / STAGE;
   static constexpr int STAGES = MAX_STAGES > 8 ? 8 : MAX_STAGES;
   static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE + EPI_STAGE_BYTES + 256;
@@ -156,10 +156,10 @@ __device__ __forceinline__ void wait_flag_cached(uint32_t* seen, const uint32_t*
   seen[idx >> 5] |= bit;
 }
 
-template <int TN, int CG>
+template <int TN, int CG, int EB>
 __device__ __forceinline__ void producer_loop(const TileParams& p, uint8_t* sA, uint8_t* sB, uint64_t* full,
                                               uint64_t* empty, uint32_t rank, uint32_t* seen) {
-  using Cfg = TileCfg<TN, CG>;
+  using Cfg = TileCfg<TN, CG, EB>;
   const uint64_t hint_a = p.a_evict_last ? policy_evict_last() : policy_evict_first();
   const uint64_t hint_b = policy_evict_last();
   uint32_t stage = 0, phase = 0;
@@ -232,10 +232,10 @@ __device__ __forceinline__ void producer_loop(const TileParams& p, uint8_t* sA, 
   }
 }
 
-template <int TN, int CG>
+template <int TN, int CG, int EB>
 __device__ __forceinline__ void mma_loop(const TileParams& p, uint8_t* sA, uint8_t* sB, uint64_t* full,
                                          uint64_t* empty, uint64_t* tfull, uint64_t* tempty, uint32_t tmem) {
-  using Cfg = TileCfg<TN, CG>;
+  using Cfg = TileCfg<TN, CG, EB>;
   constexpr uint32_t idesc = make_idesc_bf16(BM * CG, TN);
   constexpr uint32_t idesc64 = make_idesc_bf16(BM * CG, 64);
   uint32_t stage = 0, phase = 0, it = 0;
@@ -311,7 +311,13 @@ __device__ __forceinline__ void epi_chunk(const TileParams& p, const ficco_tile&
   tmem_ld_wait();
   float f[32];
 #pragma unroll
-  for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]) * scale;
+  for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
+  if (scale != 1.0f) {
+    // packed fp32x2 multiplies (FMUL2): short-K epilogues are issue-bound, the scale is half their ALU work
+    const uint64_t s2 = f32x2(scale, scale);
+#pragma unroll
+    for (int i = 0; i < 32; i += 2) fmul2(f[i], f[i + 1], s2);
+  }
   if (reduce_row) {
     // rank-ascending sum of the peers' partial chunks; the next peer's 64 bytes are in
     // flight while the current ones are added (the loads are latency-, not bandwidth-bound)
@@ -347,7 +353,7 @@ __device__ __forceinline__ void epi_chunk(const TileParams& p, const ficco_tile&
   }
 }
 
-template <int TN, int CG>
+template <int TN, int CG, int EB>
 __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfull, uint64_t* tempty,
                                               uint32_t tmem, uint8_t* stage_smem) {
   const int warp = threadIdx.x / 32;
@@ -359,13 +365,14 @@ __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfu
   // partial chunks are read back by the push copies right after their unit completes
   const uint64_t hint_part = p.part_hint == 2 ? policy_evict_last()
                              : p.part_hint == 1 ? policy_evict_normal() : hint_out;
-  uint8_t* buf = stage_smem + (warp - 2) * (EPI_BUFS * EPI_BUF_BYTES);
-  uint32_t bi = 0;  // staging buffer of the next bulk store (round robin over EPI_BUFS)
+  uint8_t* buf = stage_smem + (warp - 2) * (EB * EPI_BUF_BYTES);
+  uint32_t bi = 0;  // staging buffer of the next bulk store (round robin over EB)
   uint32_t it = 0;
   for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
     const ficco_tile td = p.tiles[t];
     const uint32_t acc = it & 1u;
-    if (td.mode == FICCO_EPI_REDUCE && !p.reduce_mma) {
+    const bool epi_reduce = td.mode == FICCO_EPI_REDUCE && !p.reduce_mma;  // partials added from global
+    if (epi_reduce) {
       // peers' partial chunks must have landed in our receive slots
       if (threadIdx.x == 64) {
         for (int j = 0; j < p.n_recv; ++j)
@@ -378,7 +385,7 @@ __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfu
     const uint32_t taddr = tmem + (uint32_t(quarter * 32) << 16) + acc * BN_MAX;
     const bool row_ok = row < td.rows;
     const bool signal = td.mode == FICCO_EPI_STORE_SIGNAL;
-    const bool reduce_row = td.mode == FICCO_EPI_REDUCE && !p.reduce_mma && row_ok;
+    const bool reduce_row = epi_reduce && row_ok;
     // whole 32-row warp boxes go out through TMA stores; ragged rows use direct stores
     const int warp_rows = td.rows - quarter * 32;
     const bool tma = warp_rows >= 32 && (signal ? p.has_part_map : p.has_out_map);
@@ -393,8 +400,8 @@ __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfu
       const bool live1 = col + 64 <= TN && col + 32 < td.cols;  // warp-uniform
       if (col >= td.cols) continue;
       if (tma) {
-        // the buffer about to be refilled was handed to the store issued EPI_BUFS stores ago
-        if (lane == 0) tma_store_wait_read<EPI_BUFS - 1>();
+        // the buffer about to be refilled was handed to the store issued EB stores ago
+        if (lane == 0) tma_store_wait_read<EB - 1>();
         __syncwarp();
       }
       // the two 32-column halves one after the other: one half's values live at a time
@@ -421,7 +428,7 @@ __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfu
                             td.c_row + quarter * 32, signal ? hint_part : hint_out);
           tma_store_commit();
         }
-        bi = bi + 1 == EPI_BUFS ? 0 : bi + 1;
+        bi = bi + 1 == EB ? 0 : bi + 1;
       }
     }
     tc_fence_before();
@@ -442,9 +449,9 @@ __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfu
   if (lane == 0) tma_store_wait_all<0>();  // staging smem must outlive the bulk stores
 }
 
-template <int TN, int CG>
+template <int TN, int CG, int EB>
 __global__ void __maxnreg__(MAX_REGS) tile_gemm_kernel(const __grid_constant__ TileParams p) {
-  using Cfg = TileCfg<TN, CG>;
+  using Cfg = TileCfg<TN, CG, EB>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = base;
@@ -505,12 +512,12 @@ __global__ void __maxnreg__(MAX_REGS) tile_gemm_kernel(const __grid_constant__ T
   if (warp == 0) {
     if (lane == 0) {
       for (int i = 0; i < SEEN_WORDS; ++i) seen_flags[i] = 0;
-      producer_loop<TN, CG>(p, sA, sB, full, empty, rank, seen_flags);
+      producer_loop<TN, CG, EB>(p, sA, sB, full, empty, rank, seen_flags);
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) mma_loop<TN, CG>(p, sA, sB, full, empty, tfull, tempty, tmem);
+    if (lane == 0 && rank == 0) mma_loop<TN, CG, EB>(p, sA, sB, full, empty, tfull, tempty, tmem);
   } else {
-    epilogue_loop<TN, CG>(p, tfull, tempty, tmem, sEpi);
+    epilogue_loop<TN, CG, EB>(p, tfull, tempty, tmem, sEpi);
   }
 
   tc_fence_before();
@@ -528,7 +535,9 @@ __global__ void __maxnreg__(MAX_REGS) tile_gemm_kernel(const __grid_constant__ T
 }
 
 // (tile width, CTA group) instantiations for the per-plan choice (see lowering.choose_tile_n).
-#define FICCO_FOR_EACH_CFG(X) \
-  X(128, 1) X(160, 1) X(192, 1) X(224, 1) X(256, 1) X(128, 2) X(160, 2) X(192, 2) X(224, 2) X(256, 2)
+#define FICCO_FOR_EACH_CFG(X)                                                                        \
+  X(128, 1, 1) X(160, 1, 1) X(192, 1, 1) X(224, 1, 1) X(256, 1, 1) X(128, 2, 1) X(160, 2, 1) X(192, 2, 1) \
+  X(224, 2, 1) X(256, 2, 1) X(128, 1, 3) X(160, 1, 3) X(192, 1, 3) X(224, 1, 3) X(256, 1, 3) X(128, 2, 3) \
+  X(160, 2, 3) X(192, 2, 3) X(224, 2, 3) X(256, 2, 3)
 
 }  // namespace ficco

@@ -43,6 +43,7 @@ EXPORTED = (
     "ficco_comm_create", "ficco_comm_destroy", "ficco_comm_epoch", "ficco_comm_check", "ficco_comm_set_flags",
     "ficco_plan_create", "ficco_plan_destroy", "ficco_plan_run", "ficco_plan_run_parts",
     "ficco_gemm_bf16", "ficco_copy_batch", "ficco_plan_set_trace", "ficco_plan_info", "ficco_gemm_bf16_cfg", "ficco_occupy_sms",
+    "ficco_timestamp",
 )
 
 
@@ -115,6 +116,7 @@ def load_library(path: os.PathLike | str | None = None) -> C.CDLL:
             "ficco_gemm_bf16_cfg": ([vp, vp, vp, i64, i64, i64, C.c_float, i32, i32, i32, vp], i32),
             "ficco_copy_batch": ([C.POINTER(vp), C.POINTER(vp), C.POINTER(sz), sz, vp], i32),
             "ficco_occupy_sms": ([i64, vp], i32),
+            "ficco_timestamp": ([vp, vp], i32),
             "ficco_plan_set_trace": ([vp, vp], i32),
             "ficco_plan_info": ([vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)], i32),
         }
@@ -327,3 +329,10 @@ def gemm_bf16(a, b, out, alpha: float = 1.0, grid: int = 0, stream=None, tile_n:
     check(load_library().ficco_gemm_bf16_cfg(C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()),
                                              C.c_void_p(out.data_ptr()), m, n, k, alpha, grid, tile_n, cta_group,
                                              C.c_void_p(_stream_ptr(stream))))
+
+
+def timestamp(dst, stream=None) -> None:
+    """dst (int64 CUDA tensor, one element) := %globaltimer ns, stream-ordered (trace op boundaries)."""
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    check(load_library().ficco_timestamp(C.c_void_p(dst.data_ptr()), C.c_void_p(s.cuda_stream)))
