@@ -74,7 +74,8 @@ extern "C" {
  * write-value memops, which serialise across chains), so a flag lands right
  * behind the data it covers on the same engine. */
 #define FICCO_OP_COPY 0         /* copy width x height bytes src -> dst (copy engine) */
-#define FICCO_OP_SIGNAL 1       /* local flag[flag] := 1 (after everything before it on the stream) */
+#define FICCO_OP_SIGNAL 1       /* local flag[flag] := 1 (after everything before it on the stream);
+                                   value > 1: words [flag, flag + value) at once (one memset) */
 #define FICCO_OP_NOTIFY 2       /* flag[flag] of rank `peer` := 1 (remote write over NVLink) */
 #define FICCO_OP_WAIT 3         /* wait until local flag[flag] != 0, then reset it (cross-rank flags) */
 #define FICCO_OP_WAIT_COUNTER 4 /* wait until local counter[flag] >= value */
@@ -94,6 +95,9 @@ extern "C" {
 #define FICCO_EPI_STORE 0        /* out[c] = bf16(alpha * acc) */
 #define FICCO_EPI_STORE_SIGNAL 1 /* partial[c] = bf16(acc); counter[chunk] += 1 when the tile is stored */
 #define FICCO_EPI_REDUCE 2       /* out[c] = bf16(acc + sum_j recv_j[...]) after rs flags of `chunk` */
+#define FICCO_EPI_STORE_REMOTE 3 /* comm_agent = core GEMM -> RS: partial[c] = bf16(acc) stored straight into
+                                    rank `chunk`'s receive slot for this rank (peer memory over NVLink, TMA),
+                                    then that rank's flag word `recv_row` += 1 (release, system scope) */
 
 typedef struct ficco_comm ficco_comm_t;
 typedef struct ficco_plan ficco_plan_t;
@@ -164,6 +168,12 @@ typedef struct {
   int32_t cta_group;  /* 1: one CTA per 128-row tile; 2: CTA pairs, tiles (2p, 2p+1) share b_row/c_col
                          and form one 256-row UMMA (0: 1) */
   int32_t hints;      /* FICCO_HINT_* bits (0: defaults) */
+  int32_t rs_target;  /* REDUCE tiles wait flag[rs_flag0 + chunk*n_recv + j] >= rs_target (0: 1, one-shot flags;
+                         STORE_REMOTE senders count their tiles into these words) */
+  int32_t go_flag;    /* STORE_REMOTE tiles store only once local flag[go_flag] is set (the copy program's
+                         DONE barrier: every owner has finished reading the previous run's slots); <= 0: none.
+                         Remote slot of this rank on owner q: ws[q] + recv.off + slot*recv_slot, slot = rank
+                         (rank < q) or rank - 1 (rank > q), recv.rows x recv.ld */
 } ficco_plan_desc;
 
 /* ficco_plan_desc.hints */

@@ -216,6 +216,7 @@ struct ficco_plan {
   bool kernel_in_graph = true;
   int tile_n = 256;                     // tile width (UMMA N)
   int epi_bufs = 1;                     // epilogue staging buffers per warp (epi_bufs_for)
+  bool has_remote = false;              // STORE_REMOTE tiles: peers' receive slots are TMA store targets
   int cta_group = 1;                    // 1: one CTA per tile; 2: CTA pair (cluster of 2, UMMA M = 256)
   ficco_plan_desc desc{};
   GraphInst graph[2];
@@ -327,8 +328,11 @@ int enqueue_run(ficco_plan* p, uint32_t parity, const void* a, const void* b, vo
           break;
         }
         case FICCO_OP_SIGNAL:
-          CK(cudaMemcpyAsync(cm->block(cm->rank, parity) + op.flag, cm->flags(cm->rank) + FICCO_FLAG_CONST_ONE, 4,
-                             cudaMemcpyDeviceToDevice, cs));
+          if (op.value > 1)  // a run of words (e.g. virtual peers' pre-landed partials): 0x01010101 each
+            CK(cudaMemsetAsync(cm->block(cm->rank, parity) + op.flag, 0x01, 4 * size_t(op.value), cs));
+          else
+            CK(cudaMemcpyAsync(cm->block(cm->rank, parity) + op.flag, cm->flags(cm->rank) + FICCO_FLAG_CONST_ONE, 4,
+                               cudaMemcpyDeviceToDevice, cs));
           break;
         case FICCO_OP_NOTIFY:
           if (op.peer < 0 || op.peer >= cm->world) return fail(FICCO_EINVAL, "notify peer out of range");
@@ -469,6 +473,25 @@ int make_params(ficco_plan* p, uint32_t parity, const void* a, const void* b, vo
       prm->reduce_mma = 1;
     }
   }
+  if (p->has_remote) {
+    // this rank's receive slot on every owner q (symmetric workspaces: same offsets everywhere)
+    for (int q = 0; q < cm->world; ++q) {
+      if (q == cm->rank) continue;
+      const int slot = cm->rank < q ? cm->rank : cm->rank - 1;
+      uint8_t* base;
+      if ((r = resolve(cm, parity, d.recv.buf, q, d.recv.off + slot * d.recv_slot, d.recv.par, a, b, c, &base)))
+        return r;
+      if ((r = encode_store_map(cm->drv, &prm->tmap_rem[q], base, d.recv.rows, d.recv.ld, d.recv.ld, 64))) return r;
+      if ((r = encode_store_map(cm->drv, &prm->tmap_rem32[q], base, d.recv.rows, d.recv.ld, d.recv.ld, 32)))
+        return r;
+      prm->rem[q] = reinterpret_cast<__nv_bfloat16*>(base);
+      prm->rem_flags[q] = cm->block(q, parity);
+    }
+    prm->ld_rem = d.recv.ld;
+    prm->has_rem_map = 1;
+  }
+  prm->go_flag = d.go_flag;
+  prm->rs_target = d.rs_target > 0 ? uint32_t(d.rs_target) : 1u;
   prm->flags = cm->block(cm->rank, parity);
   prm->counters = cm->block(cm->rank, parity) + FICCO_FLAG_COUNTERS;
   prm->abort_word = cm->flags(cm->rank) + FICCO_FLAG_ABORT;
@@ -737,13 +760,21 @@ int ficco_plan_create(ficco_comm_t* c, const ficco_plan_desc* d, ficco_plan_t** 
     if (r) return r;
     if (cta_group == 2 && d->n_tiles % 2) return fail(FICCO_EINVAL, "cta_group 2 needs an even tile list (pairs)");
   }
+  bool has_remote = false;
   for (int i = 0; i < d->n_tiles; ++i) {
     const ficco_tile& t = d->tiles[i];
     if (t.rows < 0 || t.rows > ficco::BM || (t.rows == 0 && cta_group == 1) || t.cols < 32 || t.cols > tile_n ||
         t.cols % 32)
       return fail(FICCO_EINVAL, "tile " + std::to_string(i) + ": rows/cols out of range");
-    if (t.mode < FICCO_EPI_STORE || t.mode > FICCO_EPI_REDUCE)
+    if (t.mode < FICCO_EPI_STORE || t.mode > FICCO_EPI_STORE_REMOTE)
       return fail(FICCO_EINVAL, "tile " + std::to_string(i) + ": bad epilogue mode");
+    if (t.mode == FICCO_EPI_STORE_REMOTE) {
+      if (t.chunk < 0 || t.chunk >= c->world || t.chunk == c->rank || c->world > ficco::MAX_PEERS)
+        return fail(FICCO_EINVAL, "tile " + std::to_string(i) + ": STORE_REMOTE owner rank out of range");
+      if (t.recv_row < FICCO_FLAG_RUN_LOCAL || t.recv_row >= FICCO_FLAG_BLOCK)
+        return fail(FICCO_EINVAL, "tile " + std::to_string(i) + ": STORE_REMOTE flag out of the run-local block");
+      has_remote = true;
+    }
     if (t.flag >= 0) {
       int top = 15;
       while (top > 0 && !(t.fmask & (1u << top))) --top;
@@ -763,6 +794,8 @@ int ficco_plan_create(ficco_comm_t* c, const ficco_plan_desc* d, ficco_plan_t** 
     if ((op.op == FICCO_OP_SIGNAL || op.op == FICCO_OP_NOTIFY || op.op == FICCO_OP_WAIT ||
          op.op == FICCO_OP_BARRIER) && (op.flag < 0 || op.flag + 4 > FICCO_FLAG_BLOCK))
       return fail(FICCO_EINVAL, "op flag index out of range");
+    if (op.op == FICCO_OP_SIGNAL && op.value > 1 && op.flag + int64_t(op.value) > FICCO_FLAG_BLOCK)
+      return fail(FICCO_EINVAL, "signal run out of the flag block");
     if (op.op == FICCO_OP_COPY && (is_user(op.src_buf) || is_user(op.dst_buf))) user = true;
     if (op.stream + 1 > n_streams) n_streams = op.stream + 1;
   }
@@ -776,6 +809,9 @@ int ficco_plan_create(ficco_comm_t* c, const ficco_plan_desc* d, ficco_plan_t** 
   p->tile_n = tile_n;
   p->cta_group = cta_group;
   p->epi_bufs = epi_bufs_for(d->k);
+  p->has_remote = has_remote;
+  if (has_remote && (d->recv.rows <= 0 || d->recv.ld <= 0))
+    return fail(FICCO_EINVAL, "STORE_REMOTE tiles need the receive-slot geometry (recv)");
   {
     const char* env = getenv("FICCO_KERNEL_IN_GRAPH");
     p->kernel_in_graph = !(env && env[0] == '0');

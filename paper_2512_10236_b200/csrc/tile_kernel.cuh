@@ -51,6 +51,7 @@ constexpr int MAX_REGS = 128;
 constexpr int COPY_RESERVE_REGS = 65536 - MAX_REGS * NUM_THREADS;
 constexpr uint32_t TMEM_COLS = 512;  // two accumulators of up to 256 fp32 columns
 constexpr int MAX_RECV = 15;
+constexpr int MAX_PEERS = MAX_RECV + 1;
 constexpr uint32_t SPIN_LIMIT = 1u << 25;  // ~4-10 s of polling before declaring a timeout
 constexpr int SMEM_LIMIT = 226 * 1024;  // leaves room for the static smem (seen-flag bitset)
 // Epilogue output staging: per epilogue warp EB buffers of one 32-row x 64-column bf16
@@ -91,6 +92,16 @@ struct alignas(64) TileParams {
   CUtensorMap tmap_part32;
   CUtensorMap tmap_recv;    // receive slots as one [n_recv * recv_rows, N] matrix, 128 x 64 boxes (A layout)
   CUtensorMap tmap_ident;   // 64 x 64 bf16 identity, (64 / CG) x 64 boxes (B layout)
+  // STORE_REMOTE (comm_agent = core GEMM -> RS): per owner rank q, this rank's receive slot in q's
+  // workspace (peer memory), 64- and 32-column store boxes, and q's flag block of this run
+  CUtensorMap tmap_rem[MAX_PEERS];
+  CUtensorMap tmap_rem32[MAX_PEERS];
+  __nv_bfloat16* rem[MAX_PEERS];
+  uint32_t* rem_flags[MAX_PEERS];
+  int64_t ld_rem;
+  int has_rem_map;
+  int go_flag;             // STORE_REMOTE stores wait for local flag[go_flag] (<= 0: none)
+  uint32_t rs_target;      // REDUCE waits its peers' flags >= rs_target
   int has_out_map;
   int has_part_map;
   const ficco_tile* tiles;
@@ -207,7 +218,7 @@ __device__ __forceinline__ void producer_loop(const TileParams& p, uint8_t* sA, 
       // receive slots) stream through the same ring as A operands against an identity B,
       // so the reduction rides the TMA/tensor pipeline instead of the epilogue's loads.
       for (int j = 0; j < p.n_recv; ++j)
-        wait_flag_cached(seen, p.flags, p.rs_flag0 + td.chunk * p.n_recv + j, p.epoch, p.abort_word);
+        wait_flag_cached(seen, p.flags, p.rs_flag0 + td.chunk * p.n_recv + j, p.rs_target, p.abort_word);
       for (int j = 0; j < p.n_recv; ++j) {
         for (int kb = 0; kb < Cfg::RKB; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1u);
@@ -367,6 +378,7 @@ __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfu
                              : p.part_hint == 1 ? policy_evict_normal() : hint_out;
   uint8_t* buf = stage_smem + (warp - 2) * (EB * EPI_BUF_BYTES);
   uint32_t bi = 0;  // staging buffer of the next bulk store (round robin over EB)
+  bool go_seen = false;
   uint32_t it = 0;
   for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
     const ficco_tile td = p.tiles[t];
@@ -376,7 +388,7 @@ __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfu
       // peers' partial chunks must have landed in our receive slots
       if (threadIdx.x == 64) {
         for (int j = 0; j < p.n_recv; ++j)
-          wait_flag(p.flags + p.rs_flag0 + td.chunk * p.n_recv + j, p.epoch, p.abort_word);
+          wait_flag(p.flags + p.rs_flag0 + td.chunk * p.n_recv + j, p.rs_target, p.abort_word);
       }
       named_bar_sync(1, EPI_THREADS);
     }
@@ -385,14 +397,22 @@ __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfu
     const uint32_t taddr = tmem + (uint32_t(quarter * 32) << 16) + acc * BN_MAX;
     const bool row_ok = row < td.rows;
     const bool signal = td.mode == FICCO_EPI_STORE_SIGNAL;
+    const bool remote = td.mode == FICCO_EPI_STORE_REMOTE;  // td.chunk = owner rank
     const bool reduce_row = epi_reduce && row_ok;
+    if (remote && !go_seen) {
+      // the owners' receive slots are free once the DONE barrier of this run passed
+      if (p.go_flag > 0 && lane == 0) wait_flag(p.flags + p.go_flag, p.epoch, p.abort_word);
+      __syncwarp();
+      go_seen = true;
+    }
     // whole 32-row warp boxes go out through TMA stores; ragged rows use direct stores
     const int warp_rows = td.rows - quarter * 32;
-    const bool tma = warp_rows >= 32 && (signal ? p.has_part_map : p.has_out_map);
-    const CUtensorMap* map64 = signal ? &p.tmap_part : &p.tmap_out;
-    const CUtensorMap* map32 = signal ? &p.tmap_part32 : &p.tmap_out32;
-    __nv_bfloat16* dst = signal ? p.part + int64_t(td.c_row + row) * p.ld_part + td.c_col
-                                : p.out + int64_t(td.c_row + row) * p.ld_out + td.c_col;
+    const bool tma = warp_rows >= 32 && (remote ? p.has_rem_map : signal ? p.has_part_map : p.has_out_map);
+    const CUtensorMap* map64 = remote ? &p.tmap_rem[td.chunk] : signal ? &p.tmap_part : &p.tmap_out;
+    const CUtensorMap* map32 = remote ? &p.tmap_rem32[td.chunk] : signal ? &p.tmap_part32 : &p.tmap_out32;
+    __nv_bfloat16* dst = remote ? p.rem[td.chunk] + int64_t(td.c_row + row) * p.ld_rem + td.c_col
+                         : signal ? p.part + int64_t(td.c_row + row) * p.ld_part + td.c_col
+                                  : p.out + int64_t(td.c_row + row) * p.ld_out + td.c_col;
     const float scale = td.mode == FICCO_EPI_STORE ? p.alpha : 1.0f;
 #pragma unroll 1
     for (int c64 = half; c64 * 64 < TN; c64 += 2) {
@@ -437,12 +457,13 @@ __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfu
     else
       mbar_arrive_leader(&tempty[acc]);  // the leader's MMA reuses the pair's accumulator
     if (p.trace && threadIdx.x == 64) p.trace[gridDim.x + 2 * t + 1] = globaltimer();
-    if (signal) {
+    if (signal || remote) {
       if (lane == 0) tma_store_wait_all<0>();  // this warp's bulk stores are complete
       named_bar_sync(1, EPI_THREADS);          // every row of the tile is stored
       if (threadIdx.x == 64) {
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // async-proxy (TMA) writes before the release
         __threadfence_system();
-        red_release_add(p.counters + td.chunk, 1u);
+        red_release_add(remote ? p.rem_flags[td.chunk] + td.recv_row : p.counters + td.chunk, 1u);
       }
     }
   }

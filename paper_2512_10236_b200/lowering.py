@@ -43,15 +43,16 @@ transposed-operand variants of the same chunk routing (see ``lower_rs`` /
 from __future__ import annotations
 
 import os
+from collections import Counter
 from dataclasses import dataclass, field
 
 from .domain import Scenario
 from .routing import (ExecutionPlan, GatherSpec, GemmSpec, PlanError, ScatterSpec, ScheduleKind, TransferSpec,
                       build_plan)
-from .runtime import (BUF_A, BUF_B, BUF_C, BUF_NONE, BUF_WS, EPI_REDUCE, EPI_STORE, EPI_STORE_SIGNAL,
-                      FICCO_WS_DATA_OFFSET, MAX_RECV, OP_BARRIER, OP_COPY, OP_NOTIFY, OP_RECORD, OP_SIGNAL,
-                      OP_STREAM_WAIT, OP_WAIT, OP_WAIT_COUNTER, TILE_K, TILE_M, TILE_WIDTHS, CopyOp, Operand, PlanDesc,
-                      Tile)
+from .runtime import (BUF_A, BUF_B, BUF_C, BUF_NONE, BUF_WS, EPI_REDUCE, EPI_STORE, EPI_STORE_REMOTE,
+                      EPI_STORE_SIGNAL, FICCO_WS_DATA_OFFSET, MAX_RECV, OP_BARRIER, OP_COPY, OP_NOTIFY, OP_RECORD,
+                      OP_SIGNAL, OP_STREAM_WAIT, OP_WAIT, OP_WAIT_COUNTER, TILE_K, TILE_M, TILE_WIDTHS, CopyOp,
+                      Operand, PlanDesc, Tile)
 
 # Flag words, relative to the run's parity block (one-shot words, include/ficco.h).
 # [0, 256): cross-rank words, written by peers and reset by their consumer
@@ -62,7 +63,8 @@ F_RINGN = 64     # + step i: the left neighbour holds the shard we pull at ring 
 F_LOCAL = 256    # the local shard sits in its own slot
 F_XFER = 320     # + c*G + p: chunk c of rank p landed (p = own rank is set with LOCAL)
 F_RING = 704     # + step i: ring step i landed
-F_RS = 1024      # + chunk*(G-1) + slot: a peer's partial chunk landed (RS)
+F_RS = 1024      # + chunk*(G-1) + slot: a peer's partial chunk landed (RS; with comm_agent='core' a tile count)
+F_GO = 258       # RS core: the DONE barrier passed, owners' receive slots may be written (run-local)
 EV_START = 0     # event slot: the cross-rank barrier passed
 MAX_WORLD = 16
 
@@ -414,6 +416,13 @@ def lower_rs(scenario: Scenario, kind: ScheduleKind, rank: int, grid: int = 0, v
     uniform_fused_1d: round c = remote chunks c (rotated owners) then own chunk c.
     hetero_fused_1d:  all remote chunks round by round, own shard last; push per round.
     hetero_unfused_1d: as fused but each chunk is pushed as soon as it is done.
+
+    comm_agent='core' (the SM-driven variant, reference CommAgent.CORE): no
+    partial buffer and no push copies. A remote chunk's tile epilogue TMA-stores
+    the partial straight into the owner's receive slot (peer memory over
+    NVLink) and bumps the owner's per-(chunk, sender) word; the owner reduces
+    once that word reaches the sender's tile count (``rs_target``). Stores wait
+    for the DONE barrier (flag F_GO), as the copy-engine pushes do.
     """
     plan = rs_plan(scenario, kind)  # validates divisibility exactly like the AG schedule
     g, G = rank, scenario.n_gpus
@@ -424,13 +433,15 @@ def lower_rs(scenario: Scenario, kind: ScheduleKind, rank: int, grid: int = 0, v
     R, r = M // G, M // (G * G)
     row_bytes = N * ELT
     low = Lowered()
+    direct = getattr(comm_agent, "value", comm_agent) == "core"
     part_off = FICCO_WS_DATA_OFFSET
-    low.recv_off = part_off + M * row_bytes
+    low.recv_off = part_off + (0 if direct else M * row_bytes)  # direct stores need no partial buffer
     low.recv_slot = R * row_bytes
     low.recv_par = 0  # single buffer: a peer pushes run e only after our DONE(e), i.e. after run e-1 finished
     low.ws_bytes = low.recv_off + (G - 1) * low.recv_slot
     ops, tiles = low.ops, low.tiles
     unfused = kind is ScheduleKind.HETERO_UNFUSED_1D
+    _agent_hint(comm_agent)  # validates the name
 
     def slot_of(src: int, owner: int) -> int:
         return src if src < owner else src - 1
@@ -460,7 +471,10 @@ def lower_rs(scenario: Scenario, kind: ScheduleKind, rank: int, grid: int = 0, v
             rows = min(TILE_M, row0 + r - m0)
             for n0 in range(0, N, tn):
                 cols = min(tn, N - n0)
-                if what == "remote":
+                if what == "remote" and direct:
+                    tiles.append(_tile(m0, n0, m0 - q * R, n0, rows, cols, mode=EPI_STORE_REMOTE, chunk=q,
+                                       recv_row=F_RS + c * (G - 1) + slot_of(g, q)))
+                elif what == "remote":
                     tiles.append(_tile(m0, n0, m0, n0, rows, cols, mode=EPI_STORE_SIGNAL, chunk=unit_of[(q, c)]))
                 else:
                     local = m0 - g * R
@@ -472,15 +486,17 @@ def lower_rs(scenario: Scenario, kind: ScheduleKind, rank: int, grid: int = 0, v
     # copy program. Stream 0: DONE barrier (every peer has started this run, so its
     # receive slots are free), then one counter wait per push unit, each published as
     # an event the owners' push chains (one per peer q) wait on before their copies.
-    if virtual:  # stand-in peers never push: their partials are pre-loaded, mark them landed
-        for c in range(G):
-            for j in range(G - 1):
-                ops.append(_op(OP_SIGNAL, flag=F_RS + c * (G - 1) + j, stream=0))
+    if virtual:  # stand-in peers never push: their partials are pre-loaded, mark them all landed at once
+        ops.append(_op(OP_SIGNAL, flag=F_RS, value=G * (G - 1), stream=0))
     ops.append(_op(OP_BARRIER, flag=F_DONE, stream=0))
-    ops.append(_op(OP_RECORD, value=EV_START, stream=0))
-    for q in range(G):
-        if q != g:
-            ops.append(_op(OP_STREAM_WAIT, value=EV_START, stream=_peer_stream(q, g)))
+    if direct:  # the tile epilogues push: release them, nothing else to copy
+        ops.append(_op(OP_SIGNAL, flag=F_GO, stream=0))
+        units = []
+    else:
+        ops.append(_op(OP_RECORD, value=EV_START, stream=0))
+        for q in range(G):
+            if q != g:
+                ops.append(_op(OP_STREAM_WAIT, value=EV_START, stream=_peer_stream(q, g)))
     for uid, qcs in units:
         slot = 1 + uid % 63
         ops.append(_op(OP_WAIT_COUNTER, flag=uid, value=tiles_per_chunk * len(qcs), stream=0))
@@ -497,13 +513,19 @@ def lower_rs(scenario: Scenario, kind: ScheduleKind, rank: int, grid: int = 0, v
     d = low.desc
     d.a, d.b = _operand(BUF_A, M, K), _operand(BUF_B, N, K)
     d.c = _operand(BUF_C, R, N)
-    d.part = _operand(BUF_WS, M, N, part_off)
+    d.part = _operand(BUF_NONE, 0, 0) if direct else _operand(BUF_WS, M, N, part_off)
+    if direct:
+        per_word = Counter((t.chunk, t.recv_row) for t in tiles if t.mode == EPI_STORE_REMOTE)
+        if len(set(per_word.values())) != 1:
+            raise PlanError("uneven STORE_REMOTE tile counts per (chunk, sender)")
+        d.rs_target, d.go_flag = next(iter(per_word.values())), F_GO
     d.recv = _operand(BUF_WS, R, N, low.recv_off, low.recv_par)
     d.a2, d.b2 = _operand(BUF_NONE, 0, 0), _operand(BUF_NONE, 0, 0)
     d.recv_slot, d.n_recv, d.rs_flag0 = low.recv_slot, G - 1, F_RS
     d.n_counters = len(units)
     d.k, d.alpha, d.grid, d.tile_n, d.cta_group = K, 1.0, grid, tn, cta_group
-    d.hints |= _agent_hint(comm_agent)
+    if not direct:
+        d.hints |= _agent_hint(comm_agent)
     if len(units) >= 4096 - 1:
         raise PlanError("too many push units")
     if F_RS + G * (G - 1) >= 4096:

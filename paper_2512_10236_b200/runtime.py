@@ -32,7 +32,7 @@ FICCO_MAX_STREAMS = 16
 OP_COPY, OP_SIGNAL, OP_NOTIFY, OP_WAIT, OP_WAIT_COUNTER, OP_BARRIER, OP_RECORD, OP_STREAM_WAIT = range(8)
 FICCO_MAX_EVENTS = 64
 BUF_NONE, BUF_A, BUF_B, BUF_C, BUF_WS = 0, 1, 2, 3, 4
-EPI_STORE, EPI_STORE_SIGNAL, EPI_REDUCE = 0, 1, 2
+EPI_STORE, EPI_STORE_SIGNAL, EPI_REDUCE, EPI_STORE_REMOTE = 0, 1, 2, 3
 TILE_M, TILE_N, TILE_K = 128, 256, 64
 TILE_WIDTHS = (256, 224, 192, 160, 128)
 MAX_RECV = 15
@@ -73,7 +73,8 @@ class PlanDesc(C.Structure):
                 ("recv", Operand), ("a2", Operand), ("b2", Operand), ("recv_slot", C.c_int64), ("k", C.c_int64),
                 ("n_recv", C.c_int32),
                 ("rs_flag0", C.c_int32), ("n_counters", C.c_int32), ("grid", C.c_int32), ("alpha", C.c_float),
-                ("tile_n", C.c_int32), ("cta_group", C.c_int32), ("hints", C.c_int32)]
+                ("tile_n", C.c_int32), ("cta_group", C.c_int32), ("hints", C.c_int32), ("rs_target", C.c_int32),
+                ("go_flag", C.c_int32)]
 
 
 assert C.sizeof(CopyOp) == 96 and C.sizeof(Tile) == 40 and C.sizeof(Operand) == 40

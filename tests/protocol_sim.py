@@ -28,7 +28,7 @@ import random
 import numpy as np
 
 from paper_2512_10236_b200.runtime import (BUF_A, BUF_B, BUF_C, BUF_NONE, BUF_WS, EPI_REDUCE, EPI_STORE,
-                                           EPI_STORE_SIGNAL, FICCO_FLAG_BLOCK, FICCO_FLAG_COUNTERS,
+                                           EPI_STORE_REMOTE, EPI_STORE_SIGNAL, FICCO_FLAG_BLOCK, FICCO_FLAG_COUNTERS,
                                            FICCO_FLAG_RUN_LOCAL, OP_BARRIER, OP_COPY, OP_NOTIFY, OP_RECORD,
                                            OP_SIGNAL, OP_STREAM_WAIT, OP_WAIT, OP_WAIT_COUNTER, TILE_K)
 
@@ -122,10 +122,17 @@ class World:
             out = self._operand(rank, run, d.c)
         elif t.mode == EPI_STORE_SIGNAL:
             out = self._operand(rank, run, d.part)
+        elif t.mode == EPI_STORE_REMOTE:  # straight into owner t.chunk's receive slot for this rank
+            q = t.chunk
+            slot = rank if rank < q else rank - 1
+            base = self.ranks[q].ws
+            off = d.recv.off + (d.recv.par if run & 1 else 0) + slot * d.recv_slot
+            out = base[off: off + d.recv.rows * d.recv.ld * 2].view(np.uint16).reshape(d.recv.rows, d.recv.ld)
         else:
             blk = self.ranks[rank].block(run & 1)
             for j in range(d.n_recv):
-                assert blk[d.rs_flag0 + t.chunk * d.n_recv + j] != 0, "REDUCE before its partials landed"
+                assert blk[d.rs_flag0 + t.chunk * d.n_recv + j] >= max(1, d.rs_target), \
+                    "REDUCE before its partials landed"
                 base = self._buf(rank, run, d.recv.buf, -1)
                 off = d.recv.off + (d.recv.par if run & 1 else 0) + j * d.recv_slot
                 slot = base[off: off + d.recv.rows * d.recv.ld * 2].view(np.uint16).reshape(d.recv.rows, d.recv.ld)
@@ -135,6 +142,8 @@ class World:
         if t.mode == EPI_STORE_SIGNAL:
             blk = self.ranks[rank].block(run & 1)
             blk[FICCO_FLAG_COUNTERS + t.chunk] += 1
+        elif t.mode == EPI_STORE_REMOTE:
+            self.ranks[t.chunk].block(run & 1)[t.recv_row] += 1
 
     # ---------------------------------------------------------------- driver
     def run(self, runs: int) -> None:
@@ -209,7 +218,9 @@ class World:
             if op.op == OP_COPY:
                 acts.append(lambda op=op, adv=adv: (self._copy(g, run, op), adv()))
             elif op.op == OP_SIGNAL:
-                acts.append(lambda op=op, blk=blk, adv=adv: (blk.__setitem__(op.flag, 1), adv()))
+                n = max(1, op.value)
+                acts.append(lambda op=op, blk=blk, adv=adv, n=n: (blk.__setitem__(slice(op.flag, op.flag + n),
+                                                                                 0x01010101), adv()))
             elif op.op == OP_NOTIFY:
                 peer_blk = self.ranks[op.peer].block(par)
                 acts.append(lambda op=op, pb=peer_blk, adv=adv: (pb.__setitem__(op.flag, 1), adv()))
@@ -253,10 +264,13 @@ class World:
                 if x["kseg"] + 1 < nseg:
                     acts.append(lambda x=x: x.__setitem__("kseg", x["kseg"] + 1))
                 else:
+                    d = self.low[g].desc
                     if t.mode == EPI_REDUCE:
                         blk = rk.block(par)
-                        d = self.low[g].desc
-                        if not all(blk[d.rs_flag0 + t.chunk * d.n_recv + j] for j in range(d.n_recv)):
+                        if not all(blk[d.rs_flag0 + t.chunk * d.n_recv + j] >= max(1, d.rs_target)
+                                   for j in range(d.n_recv)):
                             continue
+                    if t.mode == EPI_STORE_REMOTE and d.go_flag > 0 and not rk.block(par)[d.go_flag]:
+                        continue  # the epilogue holds its stores until the DONE barrier passed
                     acts.append(lambda x=x, t=t: (self._run_tile(g, run, t), x.__setitem__("done", True)))
         return acts

@@ -16,7 +16,8 @@ from paper_2512_10236_b200.lowering import lower_ag, lower_rs
 from paper_2512_10236_b200.ops import _scenario
 from paper_2512_10236_b200.routing import ScheduleKind, build_plan
 
-from protocol_sim import World, bf16_bits, bits_f32
+from paper_2512_10236_b200.runtime import OP_BARRIER
+from protocol_sim import Deadlock, World, bf16_bits, bits_f32
 
 AG_KINDS = ["serial", "shard_overlap_p2p", "uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d",
             "uniform_fused_2d"]
@@ -68,13 +69,16 @@ def test_ag_protocol(kind, G, cta_group):
 @pytest.mark.parametrize("kind", ["uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d"])
 @pytest.mark.parametrize("G", [2, 3, 4])
 @pytest.mark.parametrize("cta_group", [1, 2])
-def test_rs_protocol(kind, G, cta_group):
+@pytest.mark.parametrize("agent", ["dma", "core"])
+def test_rs_protocol(kind, G, cta_group, agent):
+    """comm_agent 'dma': copy-engine pushes of the partial chunks; 'core': the tile epilogues store
+    the partials straight into the owners' receive slots and count tiles into their flag words."""
     r, Kg, N = 16, 64, 64
     M = r * G * G
     R = M // G
     for seed in range(3):
         sc = _scenario("rs", M, N, Kg, G)
-        lows = [lower_rs(sc, ScheduleKind(kind), g, cta_group=cta_group) for g in range(G)]
+        lows = [lower_rs(sc, ScheduleKind(kind), g, cta_group=cta_group, comm_agent=agent) for g in range(G)]
         ws = max(low.ws_bytes for low in lows)
         for low in lows:
             low.ws_bytes = ws
@@ -166,3 +170,43 @@ def test_ag_inplace_inputs(kind):
 
         world.on_run_start, world.on_run_done = on_start, on_done
         world.run(RUNS)
+
+
+def test_rs_core_without_done_barrier_is_caught():
+    """The direct-store RS relies on the DONE barrier before overwriting a peer's receive slot:
+    dropping it (and the epilogue's go gate) lets a fast rank's next-run partials clobber a slow
+    owner's slot before its reduction read it — the interpreter must see a wrong sum."""
+    G, r, Kg, N = 3, 16, 64, 64
+    M = r * G * G
+    R = M // G
+    bad = 0
+    for seed in range(10):
+        sc = _scenario("rs", M, N, Kg, G)
+        lows = [lower_rs(sc, ScheduleKind.HETERO_FUSED_1D, g, cta_group=1, comm_agent="core") for g in range(G)]
+        for low in lows:
+            low.ops[:] = [op for op in low.ops if op.op != OP_BARRIER]
+            low.desc.go_flag = 0
+        ws = max(low.ws_bytes for low in lows)
+        for low in lows:
+            low.ws_bytes = ws
+        args, expect = [], []
+        for run in range(RUNS):
+            a = [orc.seeded_inputs(seed * 10 + run, g, (M, Kg)) for g in range(G)]
+            w = [orc.seeded_inputs(seed * 10 + run, 50 + g, (N, Kg), "normal") for g in range(G)]
+            expect.append(orc.execute_rs(a, w))
+            args.append([{"a": bf16_bits(a[g]), "b": bf16_bits(w[g]), "c": np.zeros((R, N), dtype=np.uint16)}
+                         for g in range(G)])
+        world = World(lows, args, seed=seed)
+        wrong = []
+
+        def on_done(rank, run):
+            if not np.allclose(bits_f32(args[run][rank]["c"]), expect[run][rank], rtol=2e-2, atol=3e-2):
+                wrong.append((rank, run))
+
+        world.on_run_done = on_done
+        try:
+            world.run(RUNS)
+        except (Deadlock, AssertionError):
+            wrong.append("error")
+        bad += bool(wrong)
+    assert bad > 0
