@@ -172,6 +172,9 @@ class AGWorkload:
                 off = low.gather_off + par * low.gather_par + grp.rank * self.R * self.K * 2
                 grp.ws_tensor(grp.rank, off, (self.R, self.K)).copy_(self.shards[0])
 
+    def lowered(self, grp, kind):
+        return self.ops.prepare_ag(grp, self.R, self.K, self.N, kind, inplace=self.inplace, comm_agent=self.agent)[1]
+
     def step(self, grp, kind):
         if self.inplace:
             def fn():
@@ -263,6 +266,9 @@ class RSWorkload(AGWorkload):
     def config(self):
         return {"M": self.M, "N": self.N, "K": self.K, "seq_len": self.M}
 
+    def lowered(self, grp, kind):
+        return self.ops.prepare_rs(grp, self.M, self.K, self.N, kind, comm_agent=self.agent)[1]
+
     def prepare(self, grp, kind):
         _, low, _ = self.ops.prepare_rs(grp, self.M, self.K, self.N, kind, comm_agent=self.agent)
         if grp.virtual:
@@ -346,6 +352,9 @@ class CPWorkload(AGWorkload):
 
     def config(self):
         return {"Tkv": self.Tkv, "Tq": self.Tq, "d": self.d, "seq_len": self.Tkv}
+
+    def lowered(self, grp, kind):
+        return self.ops.prepare_cp(grp, self.Tq, self.d, self.Tkv, kind, comm_agent=self.agent)[1]
 
     def prepare(self, grp, kind):
         _, low, _ = self.ops.prepare_cp(grp, self.Tq, self.d, self.Tkv, kind, comm_agent=self.agent)
@@ -455,8 +464,8 @@ def our_arm(args) -> None:
         ts = time_steps(wl.step(grp, kind), args.steps, args.warmup, flush, stream, barrier)
         grp.comm.check()
         sched[kind] = {"us": maxrank(statistics.median(ts)) * 1e3, "mean_us": maxrank(statistics.mean(ts)) * 1e3}
-    best = min((k for k in sched if "us" in sched[k] and k != "serial"), key=lambda k: sched[k]["us"])
-    # comm_agent = core (SM copy kernels) for the same schedules: the CE-offload comparison point
+    # comm_agent = core for the same schedules: SM-driven transfers (AG/CP: SM copy kernels beside
+    # the tile kernel; RS: the tile epilogues store partials straight into the owners' slots)
     core = {}
     if not args.no_core:
         wl.agent = "core"
@@ -464,8 +473,12 @@ def our_arm(args) -> None:
             wl.prepare(grp, kind)
             ts = time_steps(wl.step(grp, kind), args.steps, args.warmup, flush, stream, barrier)
             grp.comm.check()
-            core[kind] = {"us": round(maxrank(statistics.median(ts)) * 1e3, 2)}
-        wl.agent = "dma"
+            core[kind] = {"us": maxrank(statistics.median(ts)) * 1e3}
+    # the headline: the fastest (schedule, comm_agent) of the design space (serial excluded)
+    cands = [(sched[k]["us"], k, "dma") for k in sched if "us" in sched[k] and k != "serial"]
+    cands += [(v["us"], k, "core") for k, v in core.items() if k != "serial"]
+    _, best, best_agent = min(cands)
+    wl.agent = best_agent
     wl.prepare(grp, best)
     wl.step(grp, best)()
     grp.comm.check()
@@ -504,7 +517,10 @@ def our_arm(args) -> None:
     b200 = b200_machine()
     sc = ops._scenario(wl.key, *((wl.M, wl.N, wl.K) if hasattr(wl, "M") else (wl.Tkv, wl.Tq, wl.d)), G)
     selector_kind = select_schedule(sc, b200.machine, b200.t_ref).value
-    value = sched[best]["us"]
+    value = (core if best_agent == "core" else sched)[best]["us"]
+    low = wl.lowered(grp, best)
+    core_copies = sum(op.op == runtime.OP_COPY and op.src_buf == runtime.BUF_WS and op.dst_buf == runtime.BUF_WS
+                      for op in low.ops) if low.desc.hints & runtime.FICCO_HINT_CORE_COPIES else 0
     t_star = wl.ideal_us(peaks)
     if rank == 0:
         traffic = None
@@ -519,6 +535,7 @@ def our_arm(args) -> None:
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded uniform/normal inputs of the config's shapes)",
             "config": dict(workload=wl.title, ranks=G, virtual_peers=world == 1, schedule=best,
+                           comm_agent=best_agent,
                            input="symmetric slot (zero-copy publish)" if wl.inplace else "tensor copied in",
                            selector_schedule=selector_kind, l2="flushed (256 MiB write) between timed steps",
                            **wl.config()),
@@ -526,16 +543,16 @@ def our_arm(args) -> None:
             "serial_baseline": serial_desc, "cublas_gemm_us": round(cublas_us, 2),
             "ideal_overlap_us": round(t_star, 2), "pct_ideal_overlap": round(t_star / value, 4),
             "schedules": {k: ({"us": round(v["us"], 2)} if "us" in v else v) for k, v in sched.items()},
-            "schedules_comm_agent_core": core,
+            "schedules_comm_agent_core": {k: {"us": round(v["us"], 2)} for k, v in core.items()},
             "parity_spot_check": parity,
             "roofline": {"bound": bound, "achieved": round(achieved, 1), "peak": peak, "unit": unit,
                          "frac": round(achieved / peak, 4), "traffic": traffic,
-                         "kernel": "ficco::tile_gemm_kernel (flag-free run of the same tile program)",
+                         "kernel": "ficco::tile_gemm_kernel (flag-free plain GEMM of the op's shape, same kernel)",
                          "kernel_us": round(kern_us, 2),
                          "peak_source": f"MEASURED_PEAKS.json ({peaks_src}; burst figure, kernel timed alone)"},
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_us, 2), "unit": "us", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-            "gpu_launches": args.steps,
+            "gpu_launches": args.steps * (1 + core_copies),
             "clocks": clocks,
         }))
     grp.close()

@@ -50,7 +50,8 @@ from .domain import Scenario
 from .routing import (ExecutionPlan, GatherSpec, GemmSpec, PlanError, ScatterSpec, ScheduleKind, TransferSpec,
                       build_plan)
 from .runtime import (BUF_A, BUF_B, BUF_C, BUF_NONE, BUF_WS, EPI_REDUCE, EPI_STORE, EPI_STORE_REMOTE,
-                      EPI_STORE_SIGNAL, FICCO_WS_DATA_OFFSET, MAX_RECV, OP_BARRIER, OP_COPY, OP_NOTIFY, OP_RECORD,
+                      EPI_STORE_SIGNAL, FICCO_HINT_A_EVICT_LAST, FICCO_HINT_CORE_COPIES,
+                      FICCO_WS_DATA_OFFSET, MAX_RECV, OP_BARRIER, OP_COPY, OP_NOTIFY, OP_RECORD,
                       OP_SIGNAL, OP_STREAM_WAIT, OP_WAIT, OP_WAIT_COUNTER, TILE_K, TILE_M, TILE_WIDTHS, CopyOp,
                       Operand, PlanDesc, Tile)
 
@@ -70,8 +71,6 @@ MAX_WORLD = 16
 
 ELT = 2  # bf16
 A_PIN_BYTES = 32 << 20  # A operands up to this size are kept in L2 (evict_last) when re-read per column tile
-FICCO_HINT_A_EVICT_LAST = 1  # include/ficco.h
-FICCO_HINT_CORE_COPIES = 2
 
 
 def _agent_hint(comm_agent) -> int:
