@@ -975,8 +975,14 @@ int ficco_gemm_bf16_cfg(const void* a, const void* b, void* c, int64_t m, int64_
     }
     std::vector<ficco_tile> tiles;
     const int64_t mstep = int64_t(ficco::BM) * cta_group;
-    for (int64_t i = 0; i < m; i += mstep)
+    // Raster: row-major tiles (M outer) for MMA-bound shapes — measured best for operand reuse
+    // in L2; for short-K, store-bound shapes (epi_bufs_for) the whole M extent per column block
+    // (N outer), so each B tile is read from HBM once while the small A stays in L2.
+    const char* genv = getenv("FICCO_GEMM_GROUP_M");  // pair-blocks per raster group (A/B experiments)
+    const int64_t group = genv ? std::max<int64_t>(1, atoll(genv)) * mstep : epi_bufs_for(k) > 1 ? m : mstep;
+    for (int64_t i0 = 0; i0 < m; i0 += group)
       for (int64_t j = 0; j < n; j += tn)
+        for (int64_t i = i0; i < std::min(m, i0 + group); i += mstep)
         for (int h = 0; h < cta_group; ++h) {
           const int64_t row = i + h * ficco::BM;
           ficco_tile t{};

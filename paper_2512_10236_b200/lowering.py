@@ -359,12 +359,11 @@ def lower_ag(plan: ExecutionPlan, rank: int, gathered: str = "A", alpha: float =
             # contiguous row segments of the (HBM-bound) score matrix; 256-row steps keep CTA-pair
             # partners (m0, m0 + 128) adjacent
             step = TILE_M * cta_group
-            for mb in range(0, Q, step):
-                for n0 in range(start, start + count, tn):
-                    cols = min(tn, start + count - n0)
-                    for m0 in range(mb, min(Q, mb + step), TILE_M):
-                        tiles.append(_tile(m0, n0 - shift, m0, n0, min(TILE_M, Q - m0), cols, flag, fmask, ks,
-                                           kstride, b_src=int(local)))
+            for mb, n0 in [(mb, n0) for mb in range(0, Q, step) for n0 in range(start, start + count, tn)]:
+                cols = min(tn, start + count - n0)
+                for m0 in range(mb, min(Q, mb + step), TILE_M):
+                    tiles.append(_tile(m0, n0 - shift, m0, n0, min(TILE_M, Q - m0), cols, flag, fmask, ks,
+                                       kstride, b_src=int(local)))
 
     if cta_group == 2:
         low.tiles[:] = pair_tiles(low.tiles)
@@ -464,20 +463,21 @@ def lower_rs(scenario: Scenario, kind: ScheduleKind, rank: int, grid: int = 0, v
 
     tn = choose_tile_n(lambda w: -(-(G * G * (-(-r // TILE_M))) // cta_group) * (-(-N // w)), B200_SMS // cta_group)
     tiles_per_chunk = ((r + TILE_M - 1) // TILE_M) * ((N + tn - 1) // tn)
-    for what, q, c in order:
-        row0 = q * R + c * r
-        for m0 in range(row0, row0 + r, TILE_M):
-            rows = min(TILE_M, row0 + r - m0)
+    def emit(what, q, c, m0, n0):
+        rows, cols = min(TILE_M, q * R + c * r + r - m0), min(tn, N - n0)
+        if what == "remote" and direct:
+            tiles.append(_tile(m0, n0, m0 - q * R, n0, rows, cols, mode=EPI_STORE_REMOTE, chunk=q,
+                               recv_row=F_RS + c * (G - 1) + slot_of(g, q)))
+        elif what == "remote":
+            tiles.append(_tile(m0, n0, m0, n0, rows, cols, mode=EPI_STORE_SIGNAL, chunk=unit_of[(q, c)]))
+        else:
+            local = m0 - g * R
+            tiles.append(_tile(m0, n0, local, n0, rows, cols, mode=EPI_REDUCE, chunk=c, recv_row=local))
+
+    for what, q, c in order:  # chunk-major (row-major inside a chunk: measured best for W reuse)
+        for m0 in range(q * R + c * r, q * R + c * r + r, TILE_M):
             for n0 in range(0, N, tn):
-                cols = min(tn, N - n0)
-                if what == "remote" and direct:
-                    tiles.append(_tile(m0, n0, m0 - q * R, n0, rows, cols, mode=EPI_STORE_REMOTE, chunk=q,
-                                       recv_row=F_RS + c * (G - 1) + slot_of(g, q)))
-                elif what == "remote":
-                    tiles.append(_tile(m0, n0, m0, n0, rows, cols, mode=EPI_STORE_SIGNAL, chunk=unit_of[(q, c)]))
-                else:
-                    local = m0 - g * R
-                    tiles.append(_tile(m0, n0, local, n0, rows, cols, mode=EPI_REDUCE, chunk=c, recv_row=local))
+                emit(what, q, c, m0, n0)
 
     if cta_group == 2:
         tiles[:] = pair_tiles(tiles)

@@ -59,16 +59,17 @@ def _worker(rank, world, port, q):
                 if not np.allclose(out.float().cpu().numpy(), full @ w.T, rtol=1.6e-2, atol=1e-2):
                     errors.append(f"AG {kind} call {call}: output differs")
         M, Kg, N2 = 64 * world * world, 256, 256
-        for kind in RS_KINDS:
-            print(f"rank {rank}: RS {kind}", flush=True)
-            for call in range(3):
-                a = [orc.seeded_inputs(20 + call, g, (M, Kg)) for g in range(world)]
-                ws = [orc.seeded_inputs(30 + call, g, (N2, Kg), "normal") for g in range(world)]
-                want = orc.execute_rs(a, ws)[rank]
-                out = ops.matmul_reduce_scatter(t(a[rank]), t(ws[rank]), kind=kind, group=grp)
-                grp.comm.check()
-                if not np.allclose(out.float().cpu().numpy(), want, rtol=1.6e-2, atol=1e-2 * math.sqrt(world)):
-                    errors.append(f"RS {kind} call {call}: output differs")
+        for agent in ("dma", "core"):  # core: epilogue TMA stores into the peers' IPC-mapped slots
+            for kind in RS_KINDS:
+                print(f"rank {rank}: RS {kind} {agent}", flush=True)
+                for call in range(3):
+                    a = [orc.seeded_inputs(20 + call, g, (M, Kg)) for g in range(world)]
+                    ws = [orc.seeded_inputs(30 + call, g, (N2, Kg), "normal") for g in range(world)]
+                    want = orc.execute_rs(a, ws)[rank]
+                    out = ops.matmul_reduce_scatter(t(a[rank]), t(ws[rank]), kind=kind, group=grp, comm_agent=agent)
+                    grp.comm.check()
+                    if not np.allclose(out.float().cpu().numpy(), want, rtol=1.6e-2, atol=1e-2 * math.sqrt(world)):
+                        errors.append(f"RS {kind} {agent} call {call}: output differs")
         d, Tq, Tkv = 128, 256, 512 * world
         qm = orc.seeded_inputs(40, 7, (Tq, d), "normal")
         for kind in ["hetero_unfused_1d", "shard_overlap_p2p"]:
