@@ -426,10 +426,17 @@ WORKLOADS = {"c2": AGWorkload, "c3": RSWorkload, "c4": CPWorkload}
 def our_arm(args) -> None:
     import torch
     world, rank, local = dist_env()
+    # FICCO_BENCH_SHARED_GPU=1: every rank on cuda:0 over gloo — exercises the N>1 code path
+    # (IPC workspaces, cross-rank protocol, max-over-ranks timing) on a one-GPU box; not a bench number
+    shared = os.environ.get("FICCO_BENCH_SHARED_GPU") == "1"
+    local = 0 if shared else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        torch.distributed.init_process_group("nccl", device_id=dev)
+        if shared:
+            torch.distributed.init_process_group("gloo")
+        else:
+            torch.distributed.init_process_group("nccl", device_id=dev)
     from oracle import ficco_oracle as orc  # checker + CPU baseline only
     from paper_2512_10236_b200 import ops, routing, runtime
     from paper_2512_10236_b200.machines import b200_machine
