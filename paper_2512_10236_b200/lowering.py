@@ -46,7 +46,7 @@ import os
 from collections import Counter
 from dataclasses import dataclass, field
 
-from .domain import Scenario
+from .domain import Collective, Scenario
 from .routing import (ExecutionPlan, GatherSpec, GemmSpec, PlanError, ScatterSpec, ScheduleKind, TransferSpec,
                       build_plan)
 from .runtime import (BUF_A, BUF_B, BUF_C, BUF_NONE, BUF_WS, EPI_REDUCE, EPI_STORE, EPI_STORE_REMOTE,
@@ -91,6 +91,8 @@ class Lowered:
     ws_bytes: int = FICCO_WS_DATA_OFFSET
     gather_off: int = 0      # byte offset of parity-0 gathered buffer in the workspace
     gather_par: int = 0      # parity stride
+    send_off: int = 0        # all-to-all: parity-0 send area (G blocks, block d addressed to rank d)
+    send_par: int = 0
     recv_off: int = 0
     recv_par: int = 0
     recv_slot: int = 0
@@ -217,6 +219,15 @@ def lower_ag(plan: ExecutionPlan, rank: int, gathered: str = "A", alpha: float =
     gathered="A": C[M,N] = A_all[M,K] @ W[N,K]^T; call args (a=A_shard[R,K], b=W, c=C).
     gathered="B": S[Q,M] = alpha * Q[Q,K] @ K_all[M,K]^T; call args (a=Q, b=K_shard[R,K], c=S);
                   the plan's M rows (kv tokens) become output columns; ``other_rows`` = Q.
+
+    A scenario whose collective is ``all_to_all`` (EP dispatch -> expert GEMM; the
+    reference plans it exactly like all-gather, core.py:31-33) lowers
+    the same routing with per-destination sources: the call argument a is this
+    rank's send buffer [M, K] = G blocks of R rows, block d addressed to rank d;
+    rank g's gathered rows p*R.. are peer p's block g. The ring schedule pulls each
+    step's block straight from its origin (a block is addressed to one rank, so the
+    plan's store-and-forward through the left neighbour becomes a direct NVSwitch
+    pull with the same step order).
     """
     sc = plan.scenario
     kind = plan.schedule
@@ -231,25 +242,53 @@ def lower_ag(plan: ExecutionPlan, rank: int, gathered: str = "A", alpha: float =
     _check_shape(M, N, K)
     R = M // G
     row_bytes = K * ELT
+    a2a = sc.collective is Collective.ALL_TO_ALL
+    if a2a and (gathered != "A" or inplace):
+        raise PlanError("all_to_all lowers the gathered-A form from a call-argument send buffer")
     low = Lowered()
     low.gather_off = FICCO_WS_DATA_OFFSET
     low.gather_par = M * row_bytes
     low.ws_bytes = FICCO_WS_DATA_OFFSET + 2 * low.gather_par
+    if a2a:  # send area (both parities): the peers pull their blocks from it
+        low.send_off, low.send_par = low.ws_bytes, M * row_bytes
+        low.ws_bytes += 2 * low.send_par
     ops = low.ops
     src_buf = BUF_A if gathered == "A" else BUF_B
     if G > MAX_WORLD:
         raise PlanError(f"at most {MAX_WORLD} ranks")
-    _publish(ops, g, G, row_bytes, R, low.gather_off, low.gather_par, src_buf, inplace)
+    if a2a:
+        ops.append(_op(OP_COPY, src_buf=BUF_A, dst_buf=BUF_WS, dst_off=low.send_off, dst_par=low.send_par,
+                       width=M * row_bytes, stream=0))
+        ops.append(_op(OP_BARRIER, flag=F_PUB, stream=0))
+        ops.append(_op(OP_RECORD, value=EV_START, stream=0))
+        # own block -> own slot of the gathered (dispatched) buffer; tiles read it in place
+        ops.append(_op(OP_COPY, src_buf=BUF_A, dst_buf=BUF_WS, src_off=g * R * row_bytes,
+                       dst_off=low.gather_off + g * R * row_bytes, dst_par=low.gather_par, width=R * row_bytes,
+                       stream=0))
+    else:
+        _publish(ops, g, G, row_bytes, R, low.gather_off, low.gather_par, src_buf, inplace)
 
     def pull(p: int, row0: int, nrows: int, stream: int) -> CopyOp:
         off = low.gather_off + row0 * row_bytes
+        if a2a:  # peer p's block for this rank, same row offset inside the block
+            src = low.send_off + (g * R + row0 - p * R) * row_bytes
+            return _op(OP_COPY, peer=p, src_buf=BUF_WS, dst_buf=BUF_WS, src_off=src, dst_off=off,
+                       src_par=low.send_par, dst_par=low.gather_par, width=nrows * row_bytes, stream=stream)
         return _op(OP_COPY, peer=p, src_buf=BUF_WS, dst_buf=BUF_WS, src_off=off, dst_off=off,
                    src_par=low.gather_par, dst_par=low.gather_par, width=nrows * row_bytes, stream=stream)
 
     # ---- copy program: the plan's TransferSpecs arriving at this rank, one pull chain per source peer
     xfers = [t.kind for t in plan.tasks if isinstance(t.kind, TransferSpec) and t.kind.dst == g]
     kseg = 0
-    if kind is ScheduleKind.SHARD_OVERLAP_P2P:
+    if kind is ScheduleKind.SHARD_OVERLAP_P2P and a2a:
+        # ring step order, each step's block pulled directly from its origin rank (g - i)
+        ops.append(_op(OP_STREAM_WAIT, value=EV_START, stream=1))
+        for x in xfers:
+            i = x.round_idx + 1
+            src = (g - i) % G
+            ops.append(pull(src, src * R, R, 1))
+            ops.append(_op(OP_SIGNAL, flag=F_RING + i, stream=1))
+    elif kind is ScheduleKind.SHARD_OVERLAP_P2P:
         # store-and-forward ring on one chain: step i pulls shard (g-i) from the left neighbour
         right = (g + 1) % G
         ops.append(_op(OP_STREAM_WAIT, value=EV_START, stream=1))
@@ -280,8 +319,10 @@ def lower_ag(plan: ExecutionPlan, rank: int, gathered: str = "A", alpha: float =
             elif kind is ScheduleKind.UNIFORM_FUSED_2D:
                 b = K // G
                 off = low.gather_off + x.src * R * row_bytes + c * b * ELT
-                ops.append(_op(OP_COPY, peer=x.src, src_buf=BUF_WS, dst_buf=BUF_WS, src_off=off, dst_off=off,
-                               src_par=low.gather_par, dst_par=low.gather_par, width=b * ELT, height=R,
+                src, spar = (low.send_off + g * R * row_bytes + c * b * ELT, low.send_par) if a2a else \
+                    (off, low.gather_par)
+                ops.append(_op(OP_COPY, peer=x.src, src_buf=BUF_WS, dst_buf=BUF_WS, src_off=src, dst_off=off,
+                               src_par=spar, dst_par=low.gather_par, width=b * ELT, height=R,
                                src_pitch=row_bytes, dst_pitch=row_bytes, stream=st))
             else:
                 r = M // (G * G)
@@ -373,7 +414,9 @@ def lower_ag(plan: ExecutionPlan, rank: int, gathered: str = "A", alpha: float =
     own = _operand(BUF_WS, R, K, low.gather_off + g * R * row_bytes, low.gather_par) if inplace else None
     if gathered == "A":
         d.a, d.b, d.c = gat, _operand(BUF_B, N, K), _operand(BUF_C, M, N)
-        d.a2, d.b2 = own or _operand(BUF_A, R, K), _operand(BUF_NONE, 0, 0)
+        # local rows: the own shard (all-gather) or the own block g of the send buffer (all-to-all)
+        local_a = _operand(BUF_A, R, K, g * R * row_bytes if a2a else 0)
+        d.a2, d.b2 = own or local_a, _operand(BUF_NONE, 0, 0)
     else:
         d.a, d.b, d.c = _operand(BUF_A, Q, K), gat, _operand(BUF_C, Q, M)
         d.a2, d.b2 = _operand(BUF_NONE, 0, 0), own or _operand(BUF_B, R, K)
@@ -388,7 +431,7 @@ def lower_ag(plan: ExecutionPlan, rank: int, gathered: str = "A", alpha: float =
         d.hints |= FICCO_HINT_A_EVICT_LAST
     d.hints |= _agent_hint(comm_agent)
     low.notes = {"kind": kind.value, "rank": g, "world": G, "gathered": gathered, "inplace": inplace,
-                 "comm_agent": comm_agent}
+                 "comm_agent": comm_agent, "collective": sc.collective.value}
     return low
 
 

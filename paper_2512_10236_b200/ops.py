@@ -43,7 +43,8 @@ SERIALIZE = os.environ.get("FICCO_SERIALIZE", "0") == "1" or bool(os.environ.get
 
 
 def _scenario(name: str, m: int, n: int, k: int, world: int, collective=Collective.ALL_GATHER) -> Scenario:
-    return Scenario(name=name, parallelism=Parallelism.SP_TP, model="ficco-op", gemm=GemmShape(m, n, k, 2),
+    par = Parallelism.EP if collective is Collective.ALL_TO_ALL else Parallelism.SP_TP
+    return Scenario(name=name, parallelism=par, model="ficco-op", gemm=GemmShape(m, n, k, 2),
                     collective=collective, n_gpus=world)
 
 
@@ -149,6 +150,18 @@ class FiccoGroup:
                     off = low.gather_off + par * low.gather_par + p * rows * cols * 2
                     self.ws_tensor(peer, off, (rows, cols)).copy_(sh)
 
+    def load_peer_sends(self, low: Lowered, blocks: list[torch.Tensor]) -> None:
+        """Virtual mode (all-to-all): ``blocks[p]`` = peer p's [R, K] block addressed to this rank,
+        placed in p's send area (both parities) where this rank's pulls read it."""
+        assert self.virtual
+        rows, cols = blocks[0].shape
+        for p, blk in enumerate(blocks):
+            if p == self.rank:
+                continue
+            for par in (0, 1):
+                off = low.send_off + par * low.send_par + self.rank * rows * cols * 2
+                self.ws_tensor(p, off, (rows, cols)).copy_(blk)
+
     def load_peer_partials(self, low: Lowered, partials: list[torch.Tensor]) -> None:
         """Virtual mode (RS): ``partials[j]`` = peer slot j's [R, N] contribution to this rank's shard."""
         assert self.virtual
@@ -199,6 +212,18 @@ def prepare_ag(grp: FiccoGroup, R: int, K: int, N: int, kind=None, inplace: bool
                                               comm_agent=comm_agent))
         return plan, low, kd
     return _cached(grp, ("ag", R, K, N, kind, inplace, comm_agent), make)
+
+
+def prepare_a2a(grp: FiccoGroup, R: int, K: int, N: int, kind=None, comm_agent: str = "dma"):
+    """All-to-all (EP dispatch) -> expert GEMM plan for this rank: (plan, lowered, kind)."""
+    def make():
+        M = R * grp.world
+        sc = _scenario("a2a_gemm", M, N, K, grp.world, Collective.ALL_TO_ALL)
+        kd = choose_kind(sc, kind)
+        plan, low = grp.plan(("a2a", M, N, K, kd, comm_agent),
+                             lambda: lower_ag(build_plan(sc, kd), grp.rank, "A", comm_agent=comm_agent))
+        return plan, low, kd
+    return _cached(grp, ("a2a", R, K, N, kind, comm_agent), make)
 
 
 def _is_slot(grp: FiccoGroup, t: torch.Tensor, low) -> bool:
@@ -264,6 +289,34 @@ def all_gather_matmul(a_shard: torch.Tensor, weight: torch.Tensor, kind=None, gr
         par = (grp.comm.epoch() - 1) & 1  # parity of the run just enqueued
         gathered = grp.ws_tensor(grp.rank, low.gather_off + par * low.gather_par, (M, K))
         return out, gathered
+    return out
+
+
+def all_to_all_matmul(a_send: torch.Tensor, weight: torch.Tensor, kind=None, group: FiccoGroup | None = None,
+                      out: torch.Tensor | None = None, stream=None, return_gathered: bool = False,
+                      comm_agent: str = "dma"):
+    """EP dispatch -> expert GEMM with FiCCO overlap: C = all_to_all(A_send) @ W^T.
+
+    ``a_send`` [G*R, K] holds G blocks of R token rows, block d addressed to rank d (uniform
+    counts, as the reference's plans assume); W [N, K] is this rank's expert weight. Rows
+    p*R.. of the result come from peer p's block for this rank. ``return_gathered`` also
+    returns the dispatched tokens (a view into the group's double-buffered workspace).
+    """
+    grp = _default_group(group, None)
+    M, K = a_send.shape
+    if M % grp.world:
+        raise PlanError(f"send rows {M} must split into {grp.world} equal blocks")
+    R, N = M // grp.world, weight.shape[0]
+    plan, low, _ = prepare_a2a(grp, R, K, N, kind, comm_agent=comm_agent)
+    if out is None:
+        out = torch.empty(M, N, dtype=torch.bfloat16, device=a_send.device)
+    if SERIALIZE:
+        plan.run_parts(a_send, weight, out, stream, tiles=2)
+    else:
+        plan.run(a_send, weight, out, stream)
+    if return_gathered:
+        par = (grp.comm.epoch() - 1) & 1
+        return out, grp.ws_tensor(grp.rank, low.gather_off + par * low.gather_par, (M, K))
     return out
 
 

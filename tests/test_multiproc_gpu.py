@@ -70,6 +70,19 @@ def _worker(rank, world, port, q):
                     grp.comm.check()
                     if not np.allclose(out.float().cpu().numpy(), want, rtol=1.6e-2, atol=1e-2 * math.sqrt(world)):
                         errors.append(f"RS {kind} {agent} call {call}: output differs")
+        for kind in ["shard_overlap_p2p", "hetero_unfused_1d", "uniform_fused_2d"]:
+            print(f"rank {rank}: A2A {kind}", flush=True)
+            for call in range(2):
+                sends = [orc.seeded_inputs(50 + call, g, (R * world, K)) for g in range(world)]
+                wl = [orc.seeded_inputs(60 + call, g, (N, K), "normal") for g in range(world)]
+                disp, outs = orc.execute_a2a(kind, sends, wl)
+                out, got = ops.all_to_all_matmul(t(sends[rank]), t(wl[rank]), kind=kind, group=grp,
+                                                 return_gathered=True)
+                grp.comm.check()
+                if not np.array_equal(got.float().cpu().numpy(), disp[rank]):
+                    errors.append(f"A2A {kind} call {call}: dispatched tokens differ")
+                if not np.allclose(out.float().cpu().numpy(), outs[rank], rtol=1.6e-2, atol=1e-2):
+                    errors.append(f"A2A {kind} call {call}: output differs")
         d, Tq, Tkv = 128, 256, 512 * world
         qm = orc.seeded_inputs(40, 7, (Tq, d), "normal")
         for kind in ["hetero_unfused_1d", "shard_overlap_p2p"]:

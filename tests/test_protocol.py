@@ -12,6 +12,7 @@ import numpy as np
 import pytest
 
 from oracle import ficco_oracle as orc
+from paper_2512_10236_b200.domain import Collective
 from paper_2512_10236_b200.lowering import lower_ag, lower_rs
 from paper_2512_10236_b200.ops import _scenario
 from paper_2512_10236_b200.routing import ScheduleKind, build_plan
@@ -59,6 +60,44 @@ def test_ag_protocol(kind, G, cta_group):
             assert np.array_equal(bits_f32(gat), full), (kind, rank, run, "gathered")
             c = bits_f32(args[run][rank]["c"])
             np.testing.assert_allclose(c, c_ref, rtol=2e-2, atol=2e-2, err_msg=f"{kind} rank {rank} run {run}")
+            checked.append((rank, run))
+
+        world.on_run_done = on_done
+        world.run(RUNS)
+        assert len(checked) == G * RUNS
+
+
+@pytest.mark.parametrize("kind", AG_KINDS)
+@pytest.mark.parametrize("G", [2, 4])
+@pytest.mark.parametrize("cta_group", [1, 2])
+def test_a2a_protocol(kind, G, cta_group):
+    """EP all-to-all -> expert GEMM: same plans as all-gather, per-destination payloads."""
+    R, K, N = 64, 256, 64
+    for seed in range(2):
+        sc = _scenario("a2a", R * G, N, K, G, Collective.ALL_TO_ALL)
+        lows = [lower_ag(build_plan(sc, ScheduleKind(kind)), g, "A", cta_group=cta_group) for g in range(G)]
+        ws = max(low.ws_bytes for low in lows)
+        for low in lows:
+            low.ws_bytes = ws
+        args, expect = [], []
+        for run in range(RUNS):
+            sends = [orc.seeded_inputs(seed * 10 + run, g, (R * G, K)) for g in range(G)]
+            wl = [orc.seeded_inputs(seed * 10 + run, 50 + g, (N, K), "normal") for g in range(G)]
+            expect.append(orc.execute_a2a(kind, sends, wl))
+            args.append([{"a": bf16_bits(sends[g]), "b": bf16_bits(wl[g]),
+                          "c": np.zeros((R * G, N), dtype=np.uint16)} for g in range(G)])
+        world = World(lows, args, seed=seed)
+        checked = []
+
+        def on_done(rank, run, world=world):
+            disp, outs = expect[run]
+            low = lows[rank]
+            off = low.gather_off + (low.gather_par if run & 1 else 0)
+            full = disp[rank]
+            gat = world.ranks[rank].ws[off: off + full.size * 2].view(np.uint16).reshape(full.shape)
+            assert np.array_equal(bits_f32(gat), full), (kind, rank, run, "dispatched")
+            np.testing.assert_allclose(bits_f32(args[run][rank]["c"]), outs[rank], rtol=2e-2, atol=2e-2,
+                                       err_msg=f"{kind} rank {rank} run {run}")
             checked.append((rank, run))
 
         world.on_run_done = on_done
