@@ -420,7 +420,92 @@ class CPWorkload(AGWorkload):
         return per_op, f"numpy fp32 scores for 512 of {self.Tq} queries, scaled linearly"
 
 
-WORKLOADS = {"c2": AGWorkload, "c3": RSWorkload, "c4": CPWorkload}
+class EPWorkload(AGWorkload):
+    """EP all-to-all (token dispatch) -> expert GEMM: the reference corpus row g14 (Mixtral,
+    data/scenarios_corpus.csv:17): per-GPU post-dispatch GEMM (M, N, K) = (147456, 28672, 4096), G = 8.
+    Not a BASELINE.json config; same metric and method."""
+
+    key = "ep"
+    title = "EP Mixtral all-to-all -> expert GEMM (corpus g14)"
+    inplace = False
+
+    def __init__(self, torch, dev, G, rank, world, ops):
+        self.t, self.dev, self.G, self.rank, self.world, self.ops = torch, dev, G, rank, world, ops
+        self.M, self.N, self.K = 147456, 28672, 4096
+        self.R = self.M // G
+        gen = torch.Generator(device=dev).manual_seed(rank)
+        self.send = (torch.rand(self.M, self.K, generator=gen, device=dev) * 2 - 1).to(torch.bfloat16)
+        # virtual peers' blocks addressed to this rank (peer p's block `rank`)
+        self.blocks = [(torch.rand(self.R, self.K, generator=gen, device=dev) * 2 - 1).to(torch.bfloat16)
+                       if p != rank else self.send[rank * self.R:(rank + 1) * self.R] for p in range(G)]
+        wgen = torch.Generator(device=dev).manual_seed(100 + rank)
+        self.w = (torch.randn(self.N, self.K, generator=wgen, device=dev) / math.sqrt(self.K)).to(torch.bfloat16)
+        self.out = torch.empty(self.M, self.N, dtype=torch.bfloat16, device=dev)
+        self.gathered = torch.empty(self.M, self.K, dtype=torch.bfloat16, device=dev)
+        self.flops = 2.0 * self.M * self.N * self.K
+        self.comm_bytes = (G - 1) * self.R * self.K * 2
+
+    def lowered(self, grp, kind):
+        return self.ops.prepare_a2a(grp, self.R, self.K, self.N, kind, comm_agent=self.agent)[1]
+
+    def prepare(self, grp, kind):
+        _, low, _ = self.ops.prepare_a2a(grp, self.R, self.K, self.N, kind, comm_agent=self.agent)
+        if grp.virtual:
+            grp.load_peer_sends(low, self.blocks)
+
+    def step(self, grp, kind):
+        return lambda: self.ops.all_to_all_matmul(self.send, self.w, kind=kind, group=grp, out=self.out,
+                                                  comm_agent=self.agent)
+
+    def serial(self):
+        t = self.t
+        if self.world > 1:
+            def fn():
+                t.distributed.all_to_all_single(self.gathered, self.send)
+                t.matmul(self.gathered, self.w.T, out=self.out)
+            return fn, "NCCL all_to_all_single + cuBLAS"
+
+        def fn():
+            for p in range(self.G):
+                self.gathered[p * self.R:(p + 1) * self.R].copy_(self.blocks[p], non_blocking=True)
+            t.matmul(self.gathered, self.w.T, out=self.out)
+        return fn, "copy-engine dispatch of the 7 peer blocks + cuBLAS (virtual peers)"
+
+    def cublas(self):
+        a = self.t.cat(self.blocks)
+        return lambda: self.t.matmul(a, self.w.T, out=self.out)
+
+    def kernel(self, runtime):
+        a = self.t.cat(self.blocks)
+        return lambda: runtime.gemm_bf16(a, self.w, self.out), "tensor", self.flops
+
+    def check(self):
+        rows = slice(self.R, self.R + 256)  # peer 1's block for this rank
+        ref = self.t.cat(self.blocks)[rows].float() @ self.w.float().T
+        return bool(self.t.allclose(self.out[rows].float(), ref, rtol=1.6e-2, atol=1e-2))
+
+    def e2e(self, grp, kind):
+        t = self.t
+        host_a = self.send.cpu().pin_memory()
+        host_c = t.empty(self.M, self.N, dtype=t.bfloat16).pin_memory()
+        dev_a = t.empty_like(self.send)
+
+        def fn():
+            dev_a.copy_(host_a, non_blocking=True)
+            self.ops.all_to_all_matmul(dev_a, self.w, kind=kind, group=grp, out=self.out)
+            host_c.copy_(self.out, non_blocking=True)
+        return fn, self.M * self.K * 2, self.M * self.N * 2
+
+    def cpu_sample(self, orc, kind):
+        a = self.blocks[1][:1024].float().cpu().numpy()
+        w = self.w.float().cpu().numpy()
+        t0 = time.perf_counter()
+        a @ w.T
+        per_op = (time.perf_counter() - t0) * (self.M / 1024)
+        return per_op, f"numpy fp32 expert GEMM of 1024 of {self.M} dispatched rows, scaled linearly"
+
+
+WORKLOADS = {"c2": AGWorkload, "c3": RSWorkload, "c4": CPWorkload, "ep": EPWorkload}
 
 
 def our_arm(args) -> None:

@@ -180,6 +180,8 @@ typedef struct {
 #define FICCO_HINT_A_EVICT_LAST 1 /* A is small and re-read by every column tile: keep it in L2 */
 #define FICCO_HINT_CORE_COPIES 2  /* comm_agent = core: workspace-to-workspace transfers run as SM copy
                                      kernels (P2P loads/stores) instead of copy-engine memcpys */
+#define FICCO_HINT_B_EVICT_FIRST 4 /* B is streamed once per tile column (column-major raster over row groups
+                                      whose A slice is kept in L2): don't let it displace A */
 
 int ficco_abi_version(void);
 const char* ficco_last_error(void);

@@ -125,6 +125,17 @@ int encode_bf16_2d(Driver* drv, CUtensorMap* map, const void* base, int64_t rows
 // stores in flight per warp; long-K programs are MMA-bound and keep the smem for stages.
 int epi_bufs_for(int64_t k) { return k <= 384 ? 3 : 1; }
 
+// Rows per raster group of the plain GEMM (lowering.raster for the ops): row-major tiles
+// (M outer) while B [N, K] fits in L2 — every B tile then comes from L2; short-K, store-bound
+// shapes sweep the whole M extent per column block (each B tile read from HBM once, the small A
+// stays in L2); a B too large for L2 goes column-major over row groups whose A slice fits.
+int64_t raster_rows(int64_t m, int64_t n, int64_t k, int64_t mstep) {
+  if (epi_bufs_for(k) > 1) return m;
+  if (n * k * 2 <= (int64_t(64) << 20)) return mstep;
+  const int64_t rows = (int64_t(32) << 20) / (k * 2);
+  return std::max<int64_t>(mstep, rows / mstep * mstep);
+}
+
 // Resolve the (tile width, CTA group, staging buffers) instantiation: entry point, dynamic smem,
 // B box rows.
 int kernel_for(int tn, int cg, int eb, const void** fn, int* smem, int* b_rows) {
@@ -498,6 +509,7 @@ int make_params(ficco_plan* p, uint32_t parity, const void* a, const void* b, vo
   prm->epoch = 1u;  // one-shot flags: wait for != 0
   prm->alpha = d.alpha;
   prm->a_evict_last = (d.hints & FICCO_HINT_A_EVICT_LAST) != 0;
+  prm->b_evict_first = (d.hints & FICCO_HINT_B_EVICT_FIRST) != 0;
   prm->trace = p->trace;
   int g = d.grid > 0 ? d.grid : cm->sms;
   if (g > p->n_tiles) g = p->n_tiles;
@@ -975,11 +987,8 @@ int ficco_gemm_bf16_cfg(const void* a, const void* b, void* c, int64_t m, int64_
     }
     std::vector<ficco_tile> tiles;
     const int64_t mstep = int64_t(ficco::BM) * cta_group;
-    // Raster: row-major tiles (M outer) for MMA-bound shapes — measured best for operand reuse
-    // in L2; for short-K, store-bound shapes (epi_bufs_for) the whole M extent per column block
-    // (N outer), so each B tile is read from HBM once while the small A stays in L2.
     const char* genv = getenv("FICCO_GEMM_GROUP_M");  // pair-blocks per raster group (A/B experiments)
-    const int64_t group = genv ? std::max<int64_t>(1, atoll(genv)) * mstep : epi_bufs_for(k) > 1 ? m : mstep;
+    const int64_t group = genv ? std::max<int64_t>(1, atoll(genv)) * mstep : raster_rows(m, n, k, mstep);
     for (int64_t i0 = 0; i0 < m; i0 += group)
       for (int64_t j = 0; j < n; j += tn)
         for (int64_t i = i0; i < std::min(m, i0 + group); i += mstep)
@@ -1018,8 +1027,11 @@ int ficco_gemm_bf16_cfg(const void* a, const void* b, void* c, int64_t m, int64_
   p->desc.alpha = alpha;
   {
     const char* env = getenv("FICCO_A_EVICT_LAST");  // "0" / "1" override the size rule (A/B experiments)
-    const bool pin = env && env[0] != 'a' ? env[0] == '1' : m * k * 2 <= (int64_t(32) << 20);  // lowering.A_PIN_BYTES
-    p->desc.hints = pin ? FICCO_HINT_A_EVICT_LAST : 0;
+    // column-major rasters (row groups, see raster_rows) keep the group's A slice in L2 and stream B
+    const bool grouped = raster_rows(m, n, k, int64_t(ficco::BM) * cta_group) > int64_t(ficco::BM) * cta_group &&
+                         epi_bufs_for(k) == 1;
+    const bool pin = env && env[0] != 'a' ? env[0] == '1' : (m * k * 2 <= (int64_t(32) << 20) || grouped);
+    p->desc.hints = (pin ? FICCO_HINT_A_EVICT_LAST : 0) | (grouped ? FICCO_HINT_B_EVICT_FIRST : 0);
   }
   return ficco_plan_run_parts(p, a, b, c, stream, 0, 1);  // no flags: direct launch
 }

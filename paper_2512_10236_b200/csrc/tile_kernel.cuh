@@ -118,6 +118,7 @@ struct alignas(64) TileParams {
   int reduce_mma;          // REDUCE tiles fold the peers' partials in with identity MMAs (else epilogue loads)
   int recv_rows;           // rows per receive slot in tmap_recv (slot j starts at row j * recv_rows)
   int a_evict_last;        // FICCO_HINT_A_EVICT_LAST
+  int b_evict_first;       // FICCO_HINT_B_EVICT_FIRST
   int part_hint;           // L2 policy of STORE_SIGNAL (to-be-pushed) stores: 0 evict_first, 1 normal, 2 last
   uint32_t* flags;         // local flag block of this run's parity
   uint32_t* counters;      // local tile counters
@@ -172,7 +173,7 @@ __device__ __forceinline__ void producer_loop(const TileParams& p, uint8_t* sA, 
                                               uint64_t* empty, uint32_t rank, uint32_t* seen) {
   using Cfg = TileCfg<TN, CG, EB>;
   const uint64_t hint_a = p.a_evict_last ? policy_evict_last() : policy_evict_first();
-  const uint64_t hint_b = policy_evict_last();
+  const uint64_t hint_b = p.b_evict_first ? policy_evict_first() : policy_evict_last();
   uint32_t stage = 0, phase = 0;
   for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
     const ficco_tile td = p.tiles[t];

@@ -50,7 +50,8 @@ from .domain import Collective, Scenario
 from .routing import (ExecutionPlan, GatherSpec, GemmSpec, PlanError, ScatterSpec, ScheduleKind, TransferSpec,
                       build_plan)
 from .runtime import (BUF_A, BUF_B, BUF_C, BUF_NONE, BUF_WS, EPI_REDUCE, EPI_STORE, EPI_STORE_REMOTE,
-                      EPI_STORE_SIGNAL, FICCO_HINT_A_EVICT_LAST, FICCO_HINT_CORE_COPIES,
+                      EPI_STORE_SIGNAL, FICCO_HINT_A_EVICT_LAST, FICCO_HINT_B_EVICT_FIRST,
+                      FICCO_HINT_CORE_COPIES,
                       FICCO_WS_DATA_OFFSET, MAX_RECV, OP_BARRIER, OP_COPY, OP_NOTIFY, OP_RECORD,
                       OP_SIGNAL, OP_STREAM_WAIT, OP_WAIT, OP_WAIT_COUNTER, TILE_K, TILE_M, TILE_WIDTHS, CopyOp,
                       Operand, PlanDesc, Tile)
@@ -175,6 +176,29 @@ def choose_tile_n(tiles_for_width, sms: int = B200_SMS) -> int:
         if best is None or cost < best - 1e-9:
             best, best_w = cost, w
     return best_w
+
+
+W_L2_BYTES = 64 << 20     # a weight up to this size stays L2-resident under a row-major raster
+A_GROUP_BYTES = 32 << 20  # otherwise rows are rastered in groups whose A slice stays in L2
+
+
+def raster(frags: list[tuple[int, int]], N: int, K: int, tn: int) -> list[tuple[int, int, int]]:
+    """Tiles (m0, n0, rows) covering the row fragments ``frags`` x [0, N).
+
+    Row-major while W [N, K] fits in L2 (each W tile then comes from L2 for every row block:
+    C2/C3). A larger W would be streamed from HBM once per 128-row block (EP g14: 235 MB x 576),
+    so the 128-row blocks go in groups of A_GROUP_BYTES and each group sweeps N column-major:
+    W is read once per group, the group's A rows stay in L2 (pinned evict_last, W evict_first;
+    the plain GEMM uses the same raster, ficco.cu raster_rows).
+    """
+    blocks = [(m0, min(TILE_M, s + c - m0)) for s, c in frags for m0 in range(s, s + c, TILE_M)]
+    if N * K * ELT <= W_L2_BYTES:
+        return [(m0, n0, rows) for m0, rows in blocks for n0 in range(0, N, tn)]
+    per = max(2, (A_GROUP_BYTES // (K * ELT)) // TILE_M // 2 * 2)  # whole CTA pairs per group
+    out = []
+    for i in range(0, len(blocks), per):
+        out += [(m0, n0, rows) for n0 in range(0, N, tn) for m0, rows in blocks[i:i + per]]
+    return out
 
 
 def _check_shape(m: int, n: int, k: int) -> None:
@@ -383,28 +407,36 @@ def lower_ag(plan: ExecutionPlan, rank: int, gathered: str = "A", alpha: float =
         tn = choose_tile_n(lambda w: sum(cdiv(c, w) for _, c in frag_lists) * cdiv(cdiv(Q, TILE_M), cta_group),
                            units)
     tiles = low.tiles
-    for start, count in frag_lists:
+    if gathered == "A":
+        # consecutive fragments behind the same gate (one fused step, the serial gather) are one
+        # raster: a large W is then streamed once per row group, not once per fragment
+        runs: list[tuple[tuple, list[tuple[int, int]]]] = []
+        for start, count in frag_lists:
+            key = (gate(start), start // R == g)
+            if runs and runs[-1][0] == key:
+                runs[-1][1].append((start, count))
+            else:
+                runs.append((key, [(start, count)]))
+        for ((flag, fmask, ks, kstride), local), frags in runs:
+            shift = g * R if local else 0  # own-shard rows come from the call argument (alternate map)
+            for m0, n0, rows in raster(frags, N, K, tn):
+                tiles.append(_tile(m0 - shift, n0, m0, n0, rows, min(tn, N - n0), flag, fmask, ks, kstride,
+                                   a_src=int(local)))
+    for start, count in (frag_lists if gathered == "B" else []):
         flag, fmask, ks, kstride = gate(start)
         local = start // R == g  # rows of the own shard come from the call argument (alternate map)
         shift = g * R if local else 0
-        if gathered == "A":
-            for m0 in range(start, start + count, TILE_M):
-                rows = min(TILE_M, start + count - m0)
-                for n0 in range(0, N, tn):
-                    tiles.append(_tile(m0 - shift, n0, m0, n0, rows, min(tn, N - n0), flag, fmask, ks, kstride,
-                                       a_src=int(local)))
-        else:
-            if count % 32:
-                raise PlanError(f"gathered-B fragments must be multiples of 32 rows, got {count}")
-            # query-row-major inside the fragment: concurrently running tiles then write long
-            # contiguous row segments of the (HBM-bound) score matrix; 256-row steps keep CTA-pair
-            # partners (m0, m0 + 128) adjacent
-            step = TILE_M * cta_group
-            for mb, n0 in [(mb, n0) for mb in range(0, Q, step) for n0 in range(start, start + count, tn)]:
-                cols = min(tn, start + count - n0)
-                for m0 in range(mb, min(Q, mb + step), TILE_M):
-                    tiles.append(_tile(m0, n0 - shift, m0, n0, min(TILE_M, Q - m0), cols, flag, fmask, ks,
-                                       kstride, b_src=int(local)))
+        if count % 32:
+            raise PlanError(f"gathered-B fragments must be multiples of 32 rows, got {count}")
+        # query-row-major inside the fragment: concurrently running tiles then write long
+        # contiguous row segments of the (HBM-bound) score matrix; 256-row steps keep CTA-pair
+        # partners (m0, m0 + 128) adjacent
+        step = TILE_M * cta_group
+        for mb, n0 in [(mb, n0) for mb in range(0, Q, step) for n0 in range(start, start + count, tn)]:
+            cols = min(tn, start + count - n0)
+            for m0 in range(mb, min(Q, mb + step), TILE_M):
+                tiles.append(_tile(m0, n0 - shift, m0, n0, min(TILE_M, Q - m0), cols, flag, fmask, ks,
+                                   kstride, b_src=int(local)))
 
     if cta_group == 2:
         low.tiles[:] = pair_tiles(low.tiles)
@@ -426,9 +458,12 @@ def lower_ag(plan: ExecutionPlan, rank: int, gathered: str = "A", alpha: float =
     # a small A (CP: Q, a few MiB) is re-read by every column tile while the output streams
     # through L2 (4 GiB of scores in C4) — pin it (evict_last) instead of the default evict_first
     a_bytes = (Q if gathered == "B" else M) * K * ELT
+    grouped = gathered == "A" and N * K * ELT > W_L2_BYTES  # column-major raster (see raster)
     if os.environ.get("FICCO_A_EVICT_LAST", "auto") == "1" or (
-            os.environ.get("FICCO_A_EVICT_LAST", "auto") == "auto" and a_bytes <= A_PIN_BYTES):
+            os.environ.get("FICCO_A_EVICT_LAST", "auto") == "auto" and (a_bytes <= A_PIN_BYTES or grouped)):
         d.hints |= FICCO_HINT_A_EVICT_LAST
+    if grouped:
+        d.hints |= FICCO_HINT_B_EVICT_FIRST
     d.hints |= _agent_hint(comm_agent)
     low.notes = {"kind": kind.value, "rank": g, "world": G, "gathered": gathered, "inplace": inplace,
                  "comm_agent": comm_agent, "collective": sc.collective.value}

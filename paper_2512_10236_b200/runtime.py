@@ -32,7 +32,7 @@ FICCO_MAX_STREAMS = 16
 OP_COPY, OP_SIGNAL, OP_NOTIFY, OP_WAIT, OP_WAIT_COUNTER, OP_BARRIER, OP_RECORD, OP_STREAM_WAIT = range(8)
 FICCO_MAX_EVENTS = 64
 BUF_NONE, BUF_A, BUF_B, BUF_C, BUF_WS = 0, 1, 2, 3, 4
-FICCO_HINT_A_EVICT_LAST, FICCO_HINT_CORE_COPIES = 1, 2  # ficco_plan_desc.hints
+FICCO_HINT_A_EVICT_LAST, FICCO_HINT_CORE_COPIES, FICCO_HINT_B_EVICT_FIRST = 1, 2, 4  # ficco_plan_desc.hints
 EPI_STORE, EPI_STORE_SIGNAL, EPI_REDUCE, EPI_STORE_REMOTE = 0, 1, 2, 3
 TILE_M, TILE_N, TILE_K = 128, 256, 64
 TILE_WIDTHS = (256, 224, 192, 160, 128)
