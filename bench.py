@@ -287,14 +287,16 @@ class RSWorkload(AGWorkload):
             return fn, "cuBLAS + NCCL reduce_scatter_tensor"
         R = self.R
 
+        peers = t.stack(self.peer_parts)  # the received partials, contiguous like an NCCL receive buffer
+
         def fn():
             t.matmul(self.a, self.w.T, out=self.part)
             self.sink.copy_(self.part[R:], non_blocking=True)  # the 7 remote shards leave (copy engine)
-            acc = self.part[:R].float()
-            for p in self.peer_parts:
-                acc += p.float()
-            self.out.copy_(acc)
-        return fn, "cuBLAS + copy-engine egress of 7 shards + reduction of 8 partials (virtual peers)"
+            # one pass over the received partials (fp32 sum), then the own partial and one rounding
+            acc = t.sum(peers, dim=0, dtype=t.float32)
+            self.out.copy_(acc.add_(self.part[:R]))
+        return fn, ("cuBLAS + copy-engine egress of 7 shards + fused fp32 reduction of the 7 received partials "
+                    "and the own one (virtual peers)")
 
     def cublas(self):
         return lambda: self.t.matmul(self.a, self.w.T, out=self.part)
