@@ -483,6 +483,8 @@ int make_params(ficco_plan* p, uint32_t parity, const void* a, const void* b, vo
       if ((r = encode_bf16_2d(cm->drv, &prm->tmap_ident, cm->ws[cm->rank] + FICCO_WS_IDENTITY_OFF, 64, 64, 64,
                               64 / p->cta_group)))
         return r;
+      const char* alias = getenv("FICCO_RS_ALIAS");  // timing experiments only: every peer reads slot 0
+      if (alias && alias[0] == '1') prm->recv_rows = 0;
       prm->reduce_mma = 1;
     }
   }

@@ -6,6 +6,7 @@ Variants of the SAME lowered plan, each timed with CUDA events (L2 flushed):
   no_push       push copies dropped (counter waits / virtual flags kept)
   store_only    no copies, every tile a plain STORE (the RS tile ORDER with GEMM epilogues)
   no_reduce     no copies, REDUCE tiles as plain STORE (STORE_SIGNAL kept)
+  core_alias    core, but every peer slot read from slot 0 (timing only: partial reads L2-resident)
   gemm          ficco_gemm_bf16 of the same M x N x K (row-major tile order)
 Usage: python tools/rs_decomp.py [kind] [reps]
 """
@@ -63,6 +64,12 @@ def main():
         "store_only": variant(True, {EPI_REDUCE: EPI_STORE, EPI_STORE_SIGNAL: EPI_STORE}),
     }
     fns = {k: (lambda p=p: p.run(a, w, out)) for k, p in plans.items()}
+
+    def aliased():  # core, every REDUCE reads the peers' partials from slot 0 (wrong sums; L2-resident)
+        os.environ["FICCO_RS_ALIAS"] = "1"
+        plans["core"].run(a, w, out)
+        os.environ.pop("FICCO_RS_ALIAS")
+    fns["core_alias"] = aliased
     fns["gemm"] = lambda: runtime.gemm_bf16(a, w, full_out)
     res = {k: [] for k in fns}
     for _ in range(3):
