@@ -485,7 +485,7 @@ int make_params(ficco_plan* p, uint32_t parity, const void* a, const void* b, vo
         return r;
       const char* alias = getenv("FICCO_RS_ALIAS");  // timing experiments only: every peer reads slot 0
       if (alias && alias[0] == '1') prm->recv_rows = 0;
-      prm->reduce_mma = 1;
+      prm->reduce_mma = env && env[0] == '2' ? 2 : 1;  // 2: loads without the identity MMAs (timing only)
     }
   }
   if (p->has_remote) {

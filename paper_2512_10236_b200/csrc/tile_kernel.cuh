@@ -115,7 +115,8 @@ struct alignas(64) TileParams {
   int64_t ld_recv;
   int n_recv;
   int rs_flag0;
-  int reduce_mma;          // REDUCE tiles fold the peers' partials in with identity MMAs (else epilogue loads)
+  int reduce_mma;          // REDUCE tiles fold the peers' partials in with identity MMAs (else epilogue loads;
+                           // 2: boxes streamed through the ring without the MMAs, timing experiments only)
   int recv_rows;           // rows per receive slot in tmap_recv (slot j starts at row j * recv_rows)
   int a_evict_last;        // FICCO_HINT_A_EVICT_LAST
   int b_evict_first;       // FICCO_HINT_B_EVICT_FIRST
@@ -287,7 +288,7 @@ __device__ __forceinline__ void mma_loop(const TileParams& p, uint8_t* sA, uint8
         const uint64_t ad = make_sdesc_sw128(smem_addr(sA + stage * A_STAGE));
         const uint64_t bd = make_sdesc_sw128(smem_addr(sB + stage * Cfg::B_STAGE));
 #pragma unroll
-        for (int k = 0; k < BK / UMMA_K; ++k) {
+        for (int k = 0; k < BK / UMMA_K && p.reduce_mma == 1; ++k) {  // 2: timing only, loads without adds
           if constexpr (CG == 1)
             umma_bf16(d + col, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc64, 1u);
           else

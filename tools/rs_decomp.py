@@ -7,6 +7,7 @@ Variants of the SAME lowered plan, each timed with CUDA events (L2 flushed):
   store_only    no copies, every tile a plain STORE (the RS tile ORDER with GEMM epilogues)
   no_reduce     no copies, REDUCE tiles as plain STORE (STORE_SIGNAL kept)
   core_alias    core, but every peer slot read from slot 0 (timing only: partial reads L2-resident)
+  core_noadd    core, partial boxes loaded through the ring but no identity MMAs (timing only)
   gemm          ficco_gemm_bf16 of the same M x N x K (row-major tile order)
 Usage: python tools/rs_decomp.py [kind] [reps]
 """
@@ -70,6 +71,12 @@ def main():
         plans["core"].run(a, w, out)
         os.environ.pop("FICCO_RS_ALIAS")
     fns["core_alias"] = aliased
+
+    def no_add():  # core, partials streamed through the ring but not added (wrong sums; timing only)
+        os.environ["FICCO_RS_MMA"] = "2"
+        plans["core"].run(a, w, out)
+        os.environ.pop("FICCO_RS_MMA")
+    fns["core_noadd"] = no_add
     fns["gemm"] = lambda: runtime.gemm_bf16(a, w, full_out)
     res = {k: [] for k in fns}
     for _ in range(3):
