@@ -15,7 +15,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2512_10236_b200 import ops, runtime  # noqa: E402
-from paper_2512_10236_b200.runtime import EPI_REDUCE, EPI_STORE_SIGNAL  # noqa: E402
+from paper_2512_10236_b200.runtime import EPI_REDUCE, EPI_STORE_REMOTE, EPI_STORE_SIGNAL  # noqa: E402
 
 
 def main():
@@ -30,19 +30,20 @@ def main():
     grp = ops.FiccoGroup.virtual_group(G, 0)
     res = {}
     for kind in sys.argv[1:] or ["hetero_fused_1d", "uniform_fused_1d"]:
-        plan, low, _ = ops.prepare_rs(grp, M, K, N, kind)
+        agent = os.environ.get("RS_AGENT", "dma")
+        plan, low, _ = ops.prepare_rs(grp, M, K, N, kind, comm_agent=agent)
         info = plan.info()
         trace = torch.zeros(info["grid"] + 2 * info["tiles"], dtype=torch.int64, device="cuda")
         plan.set_trace(trace)
         for _ in range(3):
-            ops.matmul_reduce_scatter(a, w, kind=kind, group=grp, out=out)
+            ops.matmul_reduce_scatter(a, w, kind=kind, group=grp, out=out, comm_agent=agent)
         torch.cuda.synchronize()
         ts = []
         for _ in range(10):
             flush.fill_(1)
             x, y = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             x.record()
-            ops.matmul_reduce_scatter(a, w, kind=kind, group=grp, out=out)
+            ops.matmul_reduce_scatter(a, w, kind=kind, group=grp, out=out, comm_agent=agent)
             y.record()
             y.synchronize()
             ts.append(x.elapsed_time(y) * 1e3)
@@ -55,7 +56,8 @@ def main():
         modes = {}
         # CTA-pair tile lists interleave the two halves; group by the epilogue mode
         tiles = low.tiles
-        for name, mode in (("store_signal", EPI_STORE_SIGNAL), ("reduce", EPI_REDUCE)):
+        for name, mode in (("store_signal", EPI_STORE_SIGNAL), ("store_remote", EPI_STORE_REMOTE),
+                           ("reduce", EPI_REDUCE)):
             idx = [i for i, t in enumerate(tiles) if t.mode == mode]
             if not idx:
                 continue
