@@ -223,6 +223,18 @@ int ficco_plan_run(ficco_plan_t* plan, const void* a, const void* b, void* c, vo
 int ficco_plan_run_parts(ficco_plan_t* plan, const void* a, const void* b, void* c, void* stream,
                          int run_copies, int run_tiles);
 
+/* Typed op entry points (the overlapped-op boundary of SURVEY.md §8b): ficco_plan_run with the
+ * call arguments named for the op, after checking that the plan was lowered for that op
+ * (FICCO_EINVAL otherwise). bf16 row-major operands; W in nn.Linear layout [N, K].
+ *   ficco_ag_gemm   C [G*R, N] = all_gather(A_shard [R, K]) @ W^T
+ *   ficco_a2a_gemm  C [G*R, N] = all_to_all(A_send [G*R, K]) @ W^T   (block d of A_send -> rank d)
+ *   ficco_gemm_rs   C_shard [M/G, N] = reduce_scatter_rows(A [M, Kg] @ W^T)
+ *   ficco_cp_qk     S [Tq, Tkv] = alpha * Q [Tq, d] @ all_gather(K_shard [Tkv/G, d])^T */
+int ficco_ag_gemm(ficco_plan_t* plan, const void* a_shard, const void* w, void* c, void* stream);
+int ficco_a2a_gemm(ficco_plan_t* plan, const void* a_send, const void* w, void* c, void* stream);
+int ficco_gemm_rs(ficco_plan_t* plan, const void* a, const void* w, void* c_shard, void* stream);
+int ficco_cp_qk(ficco_plan_t* plan, const void* q, const void* k_shard, void* scores, void* stream);
+
 /* Optional measured timeline: buf (device, u64) receives %globaltimer ns stamps —
  * [0, grid) CTA start, then per tile t {2t: flags satisfied / loads start,
  * 2t+1: tile stored} at offset grid. NULL disables. Rebuilds the plan's graphs. */

@@ -125,6 +125,18 @@ int encode_bf16_2d(Driver* drv, CUtensorMap* map, const void* base, int64_t rows
 // stores in flight per warp; long-K programs are MMA-bound and keep the smem for stages.
 int epi_bufs_for(int64_t k) { return k <= 384 ? 3 : 1; }
 
+// What a lowered program computes, from its structure: GEMM -> RS programs carry partial /
+// reduce tiles; gather programs read a workspace operand (A: AG and all-to-all dispatch; B: the
+// CP KV gather); anything else is a plain GEMM.
+enum { ROLE_PLAIN = 0, ROLE_GATHER_A = 1, ROLE_GATHER_B = 2, ROLE_REDUCE_SCATTER = 3 };
+int plan_role(const ficco_plan_desc& d) {
+  for (int i = 0; i < d.n_tiles; ++i)
+    if (d.tiles[i].mode != FICCO_EPI_STORE) return ROLE_REDUCE_SCATTER;
+  if (d.b.buf == FICCO_BUF_WS) return ROLE_GATHER_B;
+  if (d.a.buf == FICCO_BUF_WS) return ROLE_GATHER_A;
+  return ROLE_PLAIN;
+}
+
 // Rows per raster group of the plain GEMM (lowering.raster for the ops): row-major tiles
 // (M outer) while B [N, K] fits in L2 — every B tile then comes from L2; short-K, store-bound
 // shapes sweep the whole M extent per column block (each B tile read from HBM once, the small A
@@ -230,6 +242,7 @@ struct ficco_plan {
   int tile_n = 256;                     // tile width (UMMA N)
   int epi_bufs = 1;                     // epilogue staging buffers per warp (epi_bufs_for)
   bool has_remote = false;              // STORE_REMOTE tiles: peers' receive slots are TMA store targets
+  int role = 0;                         // ROLE_* (which typed entry point may run it)
   int cta_group = 1;                    // 1: one CTA per tile; 2: CTA pair (cluster of 2, UMMA M = 256)
   ficco_plan_desc desc{};
   GraphInst graph[2];
@@ -826,6 +839,7 @@ int ficco_plan_create(ficco_comm_t* c, const ficco_plan_desc* d, ficco_plan_t** 
   p->cta_group = cta_group;
   p->epi_bufs = epi_bufs_for(d->k);
   p->has_remote = has_remote;
+  p->role = plan_role(*d);
   if (has_remote && (d->recv.rows <= 0 || d->recv.ld <= 0))
     return fail(FICCO_EINVAL, "STORE_REMOTE tiles need the receive-slot geometry (recv)");
   {
@@ -918,6 +932,27 @@ int ficco_plan_run(ficco_plan_t* p, const void* a, const void* b, void* c, void*
   CK(cudaEventRecord(cm->ev_join[0], gs));
   CK(cudaStreamWaitEvent(s, cm->ev_join[0], 0));
   return 0;
+}
+
+namespace {
+int run_as(ficco_plan_t* p, int role, const char* op, const void* a, const void* b, void* c, void* stream) {
+  if (!p) return fail(FICCO_EINVAL, "null plan");
+  if (p->role != role) return fail(FICCO_EINVAL, std::string(op) + ": the plan was not lowered for this op");
+  return ficco_plan_run(p, a, b, c, stream);
+}
+}  // namespace
+
+int ficco_ag_gemm(ficco_plan_t* plan, const void* a_shard, const void* w, void* c, void* stream) {
+  return run_as(plan, ROLE_GATHER_A, "ficco_ag_gemm", a_shard, w, c, stream);
+}
+int ficco_a2a_gemm(ficco_plan_t* plan, const void* a_send, const void* w, void* c, void* stream) {
+  return run_as(plan, ROLE_GATHER_A, "ficco_a2a_gemm", a_send, w, c, stream);
+}
+int ficco_gemm_rs(ficco_plan_t* plan, const void* a, const void* w, void* c_shard, void* stream) {
+  return run_as(plan, ROLE_REDUCE_SCATTER, "ficco_gemm_rs", a, w, c_shard, stream);
+}
+int ficco_cp_qk(ficco_plan_t* plan, const void* q, const void* k_shard, void* scores, void* stream) {
+  return run_as(plan, ROLE_GATHER_B, "ficco_cp_qk", q, k_shard, scores, stream);
 }
 
 int ficco_timestamp(void* dst, void* stream) {

@@ -284,7 +284,7 @@ def all_gather_matmul(a_shard: torch.Tensor, weight: torch.Tensor, kind=None, gr
     if SERIALIZE:
         plan.run_parts(a_shard, weight, out, stream, tiles=2)
     else:
-        plan.run(a_shard, weight, out, stream)
+        plan.run_op("ag_gemm", a_shard, weight, out, stream)
     if return_gathered:
         par = (grp.comm.epoch() - 1) & 1  # parity of the run just enqueued
         gathered = grp.ws_tensor(grp.rank, low.gather_off + par * low.gather_par, (M, K))
@@ -313,7 +313,7 @@ def all_to_all_matmul(a_send: torch.Tensor, weight: torch.Tensor, kind=None, gro
     if SERIALIZE:
         plan.run_parts(a_send, weight, out, stream, tiles=2)
     else:
-        plan.run(a_send, weight, out, stream)
+        plan.run_op("a2a_gemm", a_send, weight, out, stream)
     if return_gathered:
         par = (grp.comm.epoch() - 1) & 1
         return out, grp.ws_tensor(grp.rank, low.gather_off + par * low.gather_par, (M, K))
@@ -332,7 +332,7 @@ def matmul_reduce_scatter(a: torch.Tensor, weight: torch.Tensor, kind=None, grou
     if SERIALIZE:
         plan.run_parts(a, weight, out, stream, tiles=2)
     else:
-        plan.run(a, weight, out, stream)
+        plan.run_op("gemm_rs", a, weight, out, stream)
     return out
 
 
@@ -352,5 +352,5 @@ def cp_kv_all_gather_qk(q: torch.Tensor, k_shard: torch.Tensor, kind=None, scale
     if SERIALIZE:
         plan.run_parts(q, k_shard, out, stream, tiles=2)
     else:
-        plan.run(q, k_shard, out, stream)
+        plan.run_op("cp_qk", q, k_shard, out, stream)
     return out

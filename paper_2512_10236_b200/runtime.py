@@ -44,7 +44,7 @@ EXPORTED = (
     "ficco_comm_create", "ficco_comm_destroy", "ficco_comm_epoch", "ficco_comm_check", "ficco_comm_set_flags",
     "ficco_plan_create", "ficco_plan_destroy", "ficco_plan_run", "ficco_plan_run_parts",
     "ficco_gemm_bf16", "ficco_copy_batch", "ficco_plan_set_trace", "ficco_plan_info", "ficco_gemm_bf16_cfg", "ficco_occupy_sms",
-    "ficco_timestamp",
+    "ficco_timestamp", "ficco_ag_gemm", "ficco_a2a_gemm", "ficco_gemm_rs", "ficco_cp_qk",
 )
 
 
@@ -114,6 +114,10 @@ def load_library(path: os.PathLike | str | None = None) -> C.CDLL:
             "ficco_plan_destroy": ([vp], i32),
             "ficco_plan_run": ([vp, vp, vp, vp, vp], i32),
             "ficco_plan_run_parts": ([vp, vp, vp, vp, vp, i32, i32], i32),
+            "ficco_ag_gemm": ([vp, vp, vp, vp, vp], i32),
+            "ficco_a2a_gemm": ([vp, vp, vp, vp, vp], i32),
+            "ficco_gemm_rs": ([vp, vp, vp, vp, vp], i32),
+            "ficco_cp_qk": ([vp, vp, vp, vp, vp], i32),
             "ficco_gemm_bf16": ([vp, vp, vp, i64, i64, i64, C.c_float, i32, vp], i32),
             "ficco_gemm_bf16_cfg": ([vp, vp, vp, i64, i64, i64, C.c_float, i32, i32, i32, vp], i32),
             "ficco_copy_batch": ([C.POINTER(vp), C.POINTER(vp), C.POINTER(sz), sz, vp], i32),
@@ -290,6 +294,13 @@ class Plan:
         ptr = lambda t: C.c_void_p(0 if t is None else t.data_ptr())  # noqa: E731
         check(load_library().ficco_plan_run(C.c_void_p(self.handle), ptr(a), ptr(b), ptr(c),
                                             C.c_void_p(_stream_ptr(stream))))
+
+    def run_op(self, op: str, a, b, c, stream=None) -> None:
+        """The typed op entry point (ficco_ag_gemm / _a2a_gemm / _gemm_rs / _cp_qk): ficco_plan_run
+        after the library checked that this plan was lowered for `op`."""
+        ptr = lambda t: C.c_void_p(0 if t is None else t.data_ptr())  # noqa: E731
+        check(getattr(load_library(), f"ficco_{op}")(C.c_void_p(self.handle), ptr(a), ptr(b), ptr(c),
+                                                     C.c_void_p(_stream_ptr(stream))))
 
     def run_parts(self, a, b, c, stream=None, copies: bool = True, tiles: bool | int = True) -> None:
         """The same run enqueued directly on streams (no graph); halves selectable;

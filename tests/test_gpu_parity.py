@@ -258,3 +258,24 @@ def test_a2a_virtual_matches_oracle(lib, kind, G, rank, R, K, N, agent):
             np.testing.assert_allclose(_np(out), outs[rank], rtol=RTOL, atol=ATOL)
     finally:
         grp.close()
+
+
+def test_typed_entry_points_check_the_plan_role(lib):
+    """ficco_ag_gemm / _gemm_rs / _cp_qk / _a2a_gemm refuse a plan lowered for another op."""
+    from paper_2512_10236_b200 import ops
+    G, R, K, N = 4, 256, 256, 256
+    grp = ops.FiccoGroup.virtual_group(G, 0)
+    try:
+        ag, _, _ = ops.prepare_ag(grp, R, K, N, "hetero_fused_1d")
+        rs, _, _ = ops.prepare_rs(grp, G * R, K, N, "hetero_fused_1d")
+        cp, _, _ = ops.prepare_cp(grp, R, 128, G * R, "uniform_fused_1d")
+        a = torch.zeros(G * R, K, dtype=torch.bfloat16, device="cuda")
+        w = torch.zeros(N, K, dtype=torch.bfloat16, device="cuda")
+        c = torch.zeros(G * R, max(N, G * R), dtype=torch.bfloat16, device="cuda")
+        for plan, wrong in ((ag, "gemm_rs"), (ag, "cp_qk"), (rs, "ag_gemm"), (rs, "a2a_gemm"), (cp, "ag_gemm"),
+                            (cp, "gemm_rs")):
+            with pytest.raises(ValueError, match="not lowered for this op"):  # FICCO_EINVAL
+                plan.run_op(wrong, a, w, c)
+        grp.comm.check()
+    finally:
+        grp.close()
