@@ -8,9 +8,9 @@ measurement:
 * ``makespan`` — CUDA-event time of the whole op on the compute stream;
 * ``timeline`` — one ``TaskSpan`` per GemmSpec task of this rank (first tile
   load start -> last tile stored, from the kernel's %globaltimer trace) and per
-  arriving TransferSpec (end = first time a tile observed its readiness flag
-  set; start = op start), so measured and simulated runs diff with
-  ``export_trace_csv`` (engine.py:310-318).
+  arriving TransferSpec (start = kernel start; end = when the first tile gated
+  on its readiness flag started loading, an upper bound on the arrival), so
+  measured and simulated runs diff with ``export_trace_csv`` (engine.py:310-318).
 
 ``measured_makespan(kind_scenario)`` is the ``makespan_fn`` hook of
 ``selector.validate_heuristic``: exhaustive search over measured makespans
@@ -24,7 +24,7 @@ import statistics
 import torch
 
 from . import ops
-from .lowering import lower_ag
+from .lowering import F_RING, F_XFER, lower_ag
 from .routing import ExecutionPlan, GemmSpec, ScheduleKind, TransferSpec, build_plan
 from .simulator import SimResult, TaskSpan
 
@@ -45,6 +45,19 @@ def _gemm_tile_groups(plan: ExecutionPlan, rank: int, low) -> list[tuple[int, li
                    if tl.rows > 0 and any(s <= tl.c_row < s + c for s, c in t.kind.rows)]
         groups.append((t.id, idx))
     return groups
+
+
+def _first_gate(tile) -> list[int]:
+    """Readiness flags a tile waits for before its first k-block (segment 0 for k-segmented tiles)."""
+    return [tile.flag + b for b in range(16) if tile.fmask >> b & 1]
+
+
+def _transfer_flag(plan: ExecutionPlan, x: TransferSpec, rank: int) -> int:
+    """The flag the lowered copy program sets when transfer ``x`` has landed (lowering.lower_ag)."""
+    G = plan.scenario.n_gpus
+    if plan.schedule is ScheduleKind.SHARD_OVERLAP_P2P:
+        return F_RING + x.round_idx + 1
+    return F_XFER + x.round_idx * G + x.src
 
 
 def execute(plan: ExecutionPlan, a_shard: torch.Tensor, weight: torch.Tensor, group: "ops.FiccoGroup",
@@ -84,9 +97,18 @@ def execute(plan: ExecutionPlan, a_shard: torch.Tensor, weight: torch.Tensor, gr
     for tid, idx in _gemm_tile_groups(plan, rank, low):
         if idx:
             spans.append(TaskSpan(tid, rank, "gemm", min(ready[i] for i in idx), max(done[i] for i in idx), 0.0))
+    # a transfer has landed no later than the first tile gated on its readiness flag started
+    # its loads (the tile producer's stamp is taken right after its first gate is satisfied)
+    first_gated: dict[int, float] = {}
+    for i, tl in enumerate(low.tiles):
+        if tl.rows > 0 and tl.flag >= 0:
+            for f in _first_gate(tl):
+                first_gated[f] = min(first_gated.get(f, ready[i]), ready[i])
     for t in plan.tasks:
         if isinstance(t.kind, TransferSpec) and t.kind.dst == rank:
-            spans.append(TaskSpan(t.id, rank, f"transfer[{t.kind.src}->{t.kind.dst}]", 0.0, 0.0, 0.0))
+            end = first_gated.get(_transfer_flag(plan, t.kind, rank))
+            if end is not None:
+                spans.append(TaskSpan(t.id, rank, f"transfer[{t.kind.src}->{t.kind.dst}]", 0.0, end, 0.0))
     spans.sort(key=lambda s: s.task_id)
     res = SimResult(sc.name, plan.schedule, statistics.median(times), tuple(spans), {}, 0.0)
     return out, res

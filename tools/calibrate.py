@@ -1,10 +1,10 @@
 """Re-calibrate the selector and loss model on this B200 (north star (4)).
 
 Measures, on one GPU:
-  gemm_dil.{row8,row64,col8,col64}: one shard of a degree-way row (M/d) / column (K/d) split,
-      run as its own launch of the tile kernel, vs proportional scaling of the full GEMM,
-      over parents of increasing arithmetic intensity (lookup x = parent OTB, lossmodel.py:85-93);
-  comm_dil: single copy-engine copy of s bytes vs the large-copy rate (x = bytes);
+  gemm_dil.{row8,row64,col8,col64}: a plan's whole persistent tile program with its copies
+      dropped (every gate open) vs one plain GEMM of the parent shape, over parents of
+      increasing arithmetic intensity (lookup x = parent OTB, lossmodel.py:85-93);
+  comm_dil: a plan's copy program alone vs bytes / nic_bw (x = transfer bytes);
   gemm_cil.dma / comm_cil.dma: GEMM slowdown while copy-engine copies run, and copy slowdown
       while the GEMM runs (x = GEMM memory traffic, lossmodel.py:101-108);
   gemm_cil.core / comm_cil.core: same with an SM copy kernel (the comm_agent=core comparison);
@@ -30,10 +30,11 @@ import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-from paper_2512_10236_b200 import machines, pricing, runtime, selector  # noqa: E402
+from paper_2512_10236_b200 import machines, ops, pricing, runtime, selector  # noqa: E402
 from paper_2512_10236_b200.cli_data import synthetic_grid  # noqa: E402,F401
 from paper_2512_10236_b200.domain import GemmShape, gemm_mt, gemm_otb  # noqa: E402
 from paper_2512_10236_b200.executor import MeasuredMakespan  # noqa: E402
+from paper_2512_10236_b200.lowering import lower_ag  # noqa: E402
 from paper_2512_10236_b200.ops import _scenario  # noqa: E402
 from paper_2512_10236_b200.routing import FINE_GRAIN_KINDS, build_plan, ScheduleKind  # noqa: E402
 
@@ -86,53 +87,87 @@ def monotone(points, increasing: bool):
     return [[x, round(m, 4)] for x, m in zip(xs, ms)]
 
 
+def _virtual_plan(m, n, k, kind, drop_copies):
+    """(plan, A shard, W, C) for rank 0 of a virtual 8-rank AG->GEMM, optionally without its copies:
+    the copy program's flag writes stay, so every tile gate opens at once (decomposition only)."""
+    G, R = 8, m // 8
+    grp = ops.FiccoGroup.virtual_group(G, 0)
+    low = lower_ag(build_plan(_scenario("cal", m, n, k, G), ScheduleKind(kind)), 0, "A")
+    grp.ensure_workspace(low.ws_bytes)
+    prog = [op for op in low.ops if not (drop_copies and op.op == runtime.OP_COPY)]
+    plan = runtime.Plan(grp.comm, low.desc, prog, list(low.tiles))
+    shards = [(torch.rand(R, k, device="cuda") - 0.5).to(torch.bfloat16) for _ in range(G)]
+    grp.load_peer_shards(low, shards)  # real operand values everywhere (zeros would draw less power)
+    for par in (0, 1):  # ... including our own gathered buffer, which the dropped copies would fill
+        grp.ws_tensor(0, low.gather_off + par * low.gather_par, (m, k)).copy_(torch.cat(shards))
+    a = shards[0]
+    w = (torch.randn(n, k, device="cuda") / math.sqrt(k)).to(torch.bfloat16)
+    c = torch.empty(m, n, dtype=torch.bfloat16, device="cuda")
+    return grp, plan, a, w, c
+
+
+DIL_KINDS = {"row8": "uniform_fused_1d", "row64": "hetero_unfused_1d", "col8": "uniform_fused_2d"}
+
+
 def measure_gemm_dil(quick: bool):
-    # parents spanning OTB ~ 400 .. 6000 (square-ish bf16 GEMMs: OTB ~ n/3)
+    """Decomposition inefficiency of THIS executor (the 1-GPU DIL experiment): the
+    plan's whole tile program, copies dropped, vs one plain GEMM of the parent shape. The
+    reference prices every GemmSpec as its own kernel (engine.py:86-93); here every chunk GEMM of
+    a plan runs in one persistent kernel, so the tables measure that, per decomposition:
+    row8 = uniform_fused_1d steps (M/8 rows), row64 = hetero_unfused_1d chunks (M/64 rows),
+    col8 = uniform_fused_2d K segments (K/8). col64 has no executable schedule at G = 8 and
+    is set to col8 (the reference requires *64 >= *8)."""
     parents = [(2048, 2048, 2048), (4096, 4096, 4096), (8192, 8192, 8192), (16384, 16384, 8192)]
     if not quick:
         parents.insert(1, (4096, 2048, 4096))
         parents.append((16384, 16384, 16384))
-    out = {"row8": [], "row64": [], "col8": [], "col64": []}
+    out = {"row8": [], "row64": [], "col8": []}
     raw = []
     for m, n, k in parents:
         full = gemm_time(m, n, k)
         otb = gemm_otb(GemmShape(m, n, k, 2))
         rec = {"shape": [m, n, k], "otb": otb, "full_s": full}
-        for axis in ("row", "col"):
-            for d in (8, 64):
-                mm, kk = (m // d, k) if axis == "row" else (m, k // d)
-                if mm < 128 or kk < 64:
-                    continue
-                shard = gemm_time(mm, n, kk, launches=4)
-                dil = shard / (full / d)
-                rec[f"{axis}{d}"] = dil
-                out[f"{axis}{d}"].append([otb, dil])
+        for key, kind in DIL_KINDS.items():
+            grp, plan, a, w, c = _virtual_plan(m, n, k, kind, drop_copies=True)
+            try:
+                t = timed(lambda: plan.run(a, w, c))
+                grp.comm.check()
+            finally:
+                plan.close()
+                grp.close()
+            rec[key] = t / full
+            out[key].append([otb, t / full])
         raw.append(rec)
-    tables = {}
-    for key, pts in out.items():
-        pts = sorted(pts)
-        tables[key] = monotone(pts, increasing=False) if pts else None
-    for ax in ("row", "col"):  # *64 >= *8 at shared knots (lossmodel.py:186-190)
-        t8, t64 = tables[f"{ax}8"], tables[f"{ax}64"]
-        if t8 and t64:
-            at8 = dict((x, m) for x, m in t8)
-            tables[f"{ax}64"] = [[x, max(m, at8.get(x, m))] for x, m in t64]
+    tables = {key: monotone(sorted(pts), increasing=False) for key, pts in out.items()}
+    at8 = dict((x, mm) for x, mm in tables["row8"])
+    tables["row64"] = [[x, max(mm, at8.get(x, mm))] for x, mm in tables["row64"]]
+    tables["col64"] = [list(p) for p in tables["col8"]]
     return tables, raw
 
 
-def measure_comm_dil():
-    big = 512 << 20
-    src = torch.empty(big, dtype=torch.uint8, device="cuda").fill_(1)
-    dst = torch.empty(big, dtype=torch.uint8, device="cuda")
-    t_big = timed(lambda: dst.copy_(src), flush=False)
-    rate = big / t_big
+def measure_comm_dil(nic_bw: float):
+    """Copy-engine transfer inefficiency as the executor issues transfers: a plan's whole copy
+    program alone (run_copies only), per chunk size, vs the switch model's bytes / nic_bw
+    (topology.py:50-87; lookup x = transfer bytes). On one GPU the peers are local HBM, which the
+    copy engines outrun NVLink with, so the ratio is a lower bound and clamps to 1 (>= 1 rule)."""
     pts, raw = [], []
-    for s in (1 << 20, 4 << 20, 16 << 20, 64 << 20, 256 << 20):
-        t = timed(lambda s=s: dst[:s].copy_(src[:s]), flush=False)
-        dil = (t * rate) / s
-        pts.append([float(s), dil])
-        raw.append({"bytes": s, "s": t, "dil": dil})
-    return monotone(pts, increasing=False), {"large_copy_GBps": rate / 1e9, "points": raw}
+    for m, kind in ((8192, "uniform_fused_1d"), (8192, "shard_overlap_p2p"), (32768, "uniform_fused_1d"),
+                    (32768, "shard_overlap_p2p")):
+        n, k, G = 1024, 4096, 8
+        grp, plan, a, w, c = _virtual_plan(m, n, k, kind, drop_copies=False)
+        try:
+            t = timed(lambda: plan.run_parts(a, w, c, copies=True, tiles=False), flush=False)
+            grp.comm.check()
+        finally:
+            plan.close()
+            grp.close()
+        ingress = (G - 1) * (m // G) * k * 2
+        chunk = ingress // ((G - 1) * (G if kind != "shard_overlap_p2p" else 1))
+        ratio = t / (ingress / nic_bw)
+        pts.append([float(chunk), ratio])
+        raw.append({"kind": kind, "m": m, "chunk_bytes": chunk, "ingress_bytes": ingress, "copy_program_s": t,
+                    "ratio_vs_nic": ratio, "effective_GBps": ingress / t / 1e9})
+    return monotone(sorted(pts), increasing=False), {"nic_bw": nic_bw, "points": raw}
 
 
 def measure_cil():
@@ -249,7 +284,7 @@ def main():
     dil, dil_raw = measure_gemm_dil(args.quick)
     print(json.dumps(dil), flush=True)
     print("comm DIL ...", flush=True)
-    cdil, cdil_raw = measure_comm_dil()
+    cdil, cdil_raw = measure_comm_dil(machines.b200_machine().topo.nic_bw)
     print(json.dumps(cdil), flush=True)
     print("CIL ...", flush=True)
     cil, cil_raw = measure_cil()
@@ -260,10 +295,12 @@ def main():
 
     base = json.loads(open(os.path.join(DATA, "calibration_default.json")).read())
     doc = {
-        "_comment": ("B200 calibration measured by tools/calibrate.py (tile kernel chunk GEMMs, copy-engine "
-                     "copies, contention with CE (dma) and SM (core) copies); tables the measurement does "
-                     "not cover keep the reference defaults."),
-        "gemm_dil": {k: (v if v else base["gemm_dil"][k]) for k, v in dil.items()},
+        "_comment": ("B200 calibration measured by tools/calibrate.py on THIS executor: gemm_dil = a plan's "
+                     "persistent tile program without its copies vs the plain GEMM (row8 uniform_fused_1d, "
+                     "row64 hetero_unfused_1d, col8 uniform_fused_2d; col64 = col8); comm_dil = the copy "
+                     "program alone vs bytes / nic_bw (local peers on one GPU: clamped at 1); CIL = GEMM "
+                     "with concurrent copy-engine (dma) / SM (core) copies."),
+        "gemm_dil": dil,
         "comm_dil": cdil,
         "gemm_cil": {"dma": cil["gemm_cil.dma"], "core": cil["gemm_cil.core"]},
         "comm_cil": {"dma": cil["comm_cil.dma"], "core": cil["comm_cil.core"]},
@@ -276,9 +313,17 @@ def main():
     mpath = os.path.join(DATA, "machine_b200.json")
     m = json.load(open(mpath))
     m["t_ref"] = float(f"{t_ref:.4g}")
+    m["peak_flops"] = peak  # the selector's budget is peak_flops * t_ref: keep it the peak t_ref was fitted on
+    m["mem_bw"] = peaks["hbm_gbs"] * 1e9
+    if "bf16_tflops_sustained" in peaks:
+        m["gemm_efficiency"] = round(peaks["bf16_tflops_sustained"] / peaks["bf16_tflops"], 4)
     m["nic_bw"] = m.get("nic_bw", 770e9)
-    m["_comment"] = (m["_comment"].split(" t_ref")[0] +
-                     f" t_ref fitted by tools/calibrate.py ({ok}/{total} measured-best agreement).")
+    m["_comment"] = ("8x NVIDIA B200 over NVSwitch (NVLink 5). Switch topology: every GPU has one NIC of nic_bw "
+                     "per direction (770 GB/s measured peer copy, B200_PROFILING.md; 900 GB/s nominal). "
+                     f"peak_flops = measured cuBLAS bf16 burst (MEASURED_PEAKS.json {peaks['bf16_tflops']} TF); "
+                     "gemm_efficiency = sustained/burst; "
+                     f"mem_bw = measured HBM copy {peaks['hbm_gbs']} GB/s. t_ref fitted by tools/calibrate.py "
+                     f"({ok}/{total} measured-best agreement).")
     json.dump(m, open(mpath, "w"), indent=1, sort_keys=True)
     machines.load_machine(open(mpath).read())
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
