@@ -147,7 +147,7 @@ def measure_gemm_dil(quick: bool):
 
 def measure_comm_dil(nic_bw: float):
     """Copy-engine transfer inefficiency as the executor issues transfers: a plan's whole copy
-    program alone (run_copies only), per chunk size, vs the switch model's bytes / nic_bw
+    program alone (graph replay, no tiles), per chunk size, vs the switch model's bytes / nic_bw
     (topology.py:50-87; lookup x = transfer bytes). On one GPU the peers are local HBM, which the
     copy engines outrun NVLink with, so the ratio is a lower bound and clamps to 1 (>= 1 rule)."""
     pts, raw = [], []
@@ -155,8 +155,13 @@ def measure_comm_dil(nic_bw: float):
                     (32768, "shard_overlap_p2p")):
         n, k, G = 1024, 4096, 8
         grp, plan, a, w, c = _virtual_plan(m, n, k, kind, drop_copies=False)
+        # the copy program alone, replayed from its CUDA graph like in the op (an empty tile list:
+        # direct stream enqueue, ficco_plan_run_parts, is ~3x slower for 100+ small ops)
+        plan.close()
+        low = lower_ag(build_plan(_scenario("cal", m, n, k, G), ScheduleKind(kind)), 0, "A")
+        plan = runtime.Plan(grp.comm, low.desc, list(low.ops), [])
         try:
-            t = timed(lambda: plan.run_parts(a, w, c, copies=True, tiles=False), flush=False)
+            t = timed(lambda: plan.run(a, w, c), flush=False)
             grp.comm.check()
         finally:
             plan.close()
