@@ -175,6 +175,10 @@ class AGWorkload:
     def lowered(self, grp, kind):
         return self.ops.prepare_ag(grp, self.R, self.K, self.N, kind, inplace=self.inplace, comm_agent=self.agent)[1]
 
+    def run_plan(self, plan):
+        """A raw lowered plan with this workload's call arguments (copy-program timing)."""
+        plan.run(self.shards[0], self.w, self.out)
+
     def step(self, grp, kind):
         if self.inplace:
             def fn():
@@ -223,8 +227,12 @@ class AGWorkload:
             host_c.copy_(self.out, non_blocking=True)
         return fn, self.R * self.K * 2, self.M * self.N * 2
 
+    def ideal_parts(self, peaks):
+        """(T_gemm, T_comm) in µs: GEMM at the measured bf16 peak, bytes at nominal NVLink."""
+        return self.flops / (peaks["bf16_tflops"] * 1e12) * 1e6, self.comm_bytes / NVLINK_NOMINAL * 1e6
+
     def ideal_us(self, peaks):
-        return max(self.flops / (peaks["bf16_tflops"] * 1e12), self.comm_bytes / NVLINK_NOMINAL) * 1e6
+        return max(self.ideal_parts(peaks))
 
     def cpu_sample(self, orc, kind):
         sh = [s.float().cpu().numpy() for s in self.shards]
@@ -273,6 +281,8 @@ class RSWorkload(AGWorkload):
         _, low, _ = self.ops.prepare_rs(grp, self.M, self.K, self.N, kind, comm_agent=self.agent)
         if grp.virtual:
             grp.load_peer_partials(low, self.peer_parts)
+
+    run_plan = None  # the RS pushes wait on tile counters: no copy program runs without its tiles
 
     def step(self, grp, kind):
         return lambda: self.ops.matmul_reduce_scatter(self.a, self.w, kind=kind, group=grp, out=self.out,
@@ -363,6 +373,9 @@ class CPWorkload(AGWorkload):
         if grp.virtual:
             grp.load_peer_shards(low, self.shards)
 
+    def run_plan(self, plan):
+        plan.run(self.q, self.shards[0], self.out)
+
     def step(self, grp, kind):
         return lambda: self.ops.cp_kv_all_gather_qk(self.q, self.shards[0], kind=kind, group=grp, out=self.out,
                                                     comm_agent=self.agent)
@@ -408,10 +421,10 @@ class CPWorkload(AGWorkload):
             host_s.copy_(self.out, non_blocking=True)
         return fn, (self.Tq + self.R) * self.d * 2, self.out_bytes
 
-    def ideal_us(self, peaks):
+    def ideal_parts(self, peaks):
         t_hbm = (self.out_bytes + (self.Tq + self.Tkv) * self.d * 2) / (peaks["hbm_gbs"] * 1e9)
         t_gemm = max(self.flops / (peaks["bf16_tflops"] * 1e12), t_hbm)
-        return max(t_gemm, self.comm_bytes / NVLINK_NOMINAL) * 1e6
+        return t_gemm * 1e6, self.comm_bytes / NVLINK_NOMINAL * 1e6
 
     def cpu_sample(self, orc, kind):
         q = self.q[:512].float().cpu().numpy()
@@ -454,6 +467,9 @@ class EPWorkload(AGWorkload):
         _, low, _ = self.ops.prepare_a2a(grp, self.R, self.K, self.N, kind, comm_agent=self.agent)
         if grp.virtual:
             grp.load_peer_sends(low, self.blocks)
+
+    def run_plan(self, plan):
+        plan.run(self.send, self.w, self.out)
 
     def step(self, grp, kind):
         return lambda: self.ops.all_to_all_matmul(self.send, self.w, kind=kind, group=grp, out=self.out,
@@ -616,6 +632,18 @@ def our_arm(args) -> None:
     core_copies = sum(op.op == runtime.OP_COPY and op.src_buf == runtime.BUF_WS and op.dst_buf == runtime.BUF_WS
                       for op in low.ops) if low.desc.hints & runtime.FICCO_HINT_CORE_COPIES else 0
     t_star = wl.ideal_us(peaks)
+    t_fill = max(wl.ideal_parts(peaks)) + min(wl.ideal_parts(peaks)) / G  # the reference's pipelined ideal
+    # the copy program alone, replayed from its CUDA graph (empty tile list): measured transfer rate
+    copy_gbps = None
+    if world == 1 and wl.run_plan is not None:
+        copy_low = wl.lowered(grp, best)
+        copy_plan = runtime.Plan(grp.comm, copy_low.desc, list(copy_low.ops), [])
+        try:
+            copy_us = statistics.median(time_steps(lambda: wl.run_plan(copy_plan), args.steps, args.warmup, flush,
+                                                   stream)) * 1e3
+            copy_gbps = round(wl.comm_bytes / (copy_us * 1e-6) / 1e9, 1)
+        finally:
+            copy_plan.close()
     if rank == 0:
         traffic = None
         try:
@@ -636,11 +664,15 @@ def our_arm(args) -> None:
             "speedup_vs_serial": round(serial_us / value, 4), "serial_us": round(serial_us, 2),
             "serial_baseline": serial_desc, "cublas_gemm_us": round(cublas_us, 2),
             "ideal_overlap_us": round(t_star, 2), "pct_ideal_overlap": round(t_star / value, 4),
+            "ideal_overlap_fill_us": round(t_fill, 2), "pct_ideal_overlap_fill": round(t_fill / value, 4),
+            "copy_program_GBps": copy_gbps,
             "schedules": {k: ({"us": round(v["us"], 2)} if "us" in v else v) for k, v in sched.items()},
             "schedules_comm_agent_core": {k: {"us": round(v["us"], 2)} for k, v in core.items()},
             "parity_spot_check": parity,
             "roofline": {"bound": bound, "achieved": round(achieved, 1), "peak": peak, "unit": unit,
                          "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "frac_sustained": (round(achieved / peaks["bf16_tflops_sustained"], 4)
+                                            if bound == "tensor" and "bf16_tflops_sustained" in peaks else None),
                          "kernel": "ficco::tile_gemm_kernel (flag-free plain GEMM of the op's shape, same kernel)",
                          "kernel_us": round(kern_us, 2),
                          "peak_source": f"MEASURED_PEAKS.json ({peaks_src}; burst figure, kernel timed alone)"},
