@@ -696,7 +696,9 @@ def our_arm(args) -> None:
                            selector_schedule=selector_kind, l2="flushed (256 MiB write) between timed steps",
                            **wl.config()),
             "speedup_vs_serial": round(serial_us / value, 4), "serial_us": round(serial_us, 2),
-            "timing": "value and serial_us: interleaved step by step (time_interleaved); schedules: one run each",
+            "timing": "value and serial_us: interleaved step by step (time_interleaved); schedules: one steady-state "
+                      "run each (interleaving 10+ different plans step by step costs 5-11 % per call, not "
+                      "representative of an op called repeatedly)",
             "value_sequential": round(value_sequential, 2),
             "serial_baseline": serial_desc, "cublas_gemm_us": round(cublas_us, 2),
             "ideal_overlap_us": round(t_star, 2), "pct_ideal_overlap": round(t_star / value, 4),
