@@ -41,6 +41,7 @@ def _worker(rank, world, port, q):
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     errors = []
+    calls = 3 if world < 8 else 2  # 8 processes time-slice one GPU: keep both parities, fewer repeats
     try:
         grp = ops.FiccoGroup.distributed()
         t = lambda x: torch.from_numpy(x).to(torch.bfloat16).cuda()  # noqa: E731
@@ -48,7 +49,7 @@ def _worker(rank, world, port, q):
         w = orc.seeded_inputs(1, 99, (N, K), "normal")
         for kind in AG_KINDS:
             print(f"rank {rank}: AG {kind}", flush=True)
-            for call in range(3):  # consecutive calls: both parities, flag reuse
+            for call in range(calls):  # consecutive calls: both parities, flag reuse
                 shards = [orc.seeded_inputs(10 * call + 1, g, (R, K)) for g in range(world)]
                 out, gathered = ops.all_gather_matmul(t(shards[rank]), t(w), kind=kind, group=grp,
                                                       return_gathered=True)
@@ -62,7 +63,7 @@ def _worker(rank, world, port, q):
         for agent in ("dma", "core"):  # core: epilogue TMA stores into the peers' IPC-mapped slots
             for kind in RS_KINDS:
                 print(f"rank {rank}: RS {kind} {agent}", flush=True)
-                for call in range(3):
+                for call in range(calls):
                     a = [orc.seeded_inputs(20 + call, g, (M, Kg)) for g in range(world)]
                     ws = [orc.seeded_inputs(30 + call, g, (N2, Kg), "normal") for g in range(world)]
                     want = orc.execute_rs(a, ws)[rank]
@@ -101,7 +102,7 @@ def _worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_ranks_sharing_one_gpu(world):
     port = _free_port()
     ctx = mp.get_context("spawn")
@@ -112,7 +113,7 @@ def test_ranks_sharing_one_gpu(world):
     results = {}
     try:
         for _ in range(world):
-            r, errs = q.get(timeout=240)
+            r, errs = q.get(timeout=600)
             results[r] = errs
     finally:
         for p in procs:
