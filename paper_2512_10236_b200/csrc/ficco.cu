@@ -524,6 +524,13 @@ int make_params(ficco_plan* p, uint32_t parity, const void* a, const void* b, vo
   prm->counters = cm->block(cm->rank, parity) + FICCO_FLAG_COUNTERS;
   prm->abort_word = cm->flags(cm->rank) + FICCO_FLAG_ABORT;
   prm->epoch = 1u;  // one-shot flags: wait for != 0
+  {
+    // a flag wait longer than this is a protocol failure (FICCO_ETIMEOUT -> DeadlockError); ops of
+    // many seconds (the reference's largest grid shapes) may need more via FICCO_FLAG_TIMEOUT_S
+    const char* t = getenv("FICCO_FLAG_TIMEOUT_S");
+    const double sec = t ? atof(t) : 30.0;
+    prm->timeout_ns = static_cast<unsigned long long>((sec > 0 ? sec : 30.0) * 1e9);
+  }
   prm->alpha = d.alpha;
   prm->a_evict_last = (d.hints & FICCO_HINT_A_EVICT_LAST) != 0;
   prm->b_evict_first = (d.hints & FICCO_HINT_B_EVICT_FIRST) != 0;

@@ -52,7 +52,6 @@ constexpr int COPY_RESERVE_REGS = 65536 - MAX_REGS * NUM_THREADS;
 constexpr uint32_t TMEM_COLS = 512;  // two accumulators of up to 256 fp32 columns
 constexpr int MAX_RECV = 15;
 constexpr int MAX_PEERS = MAX_RECV + 1;
-constexpr uint32_t SPIN_LIMIT = 1u << 25;  // ~4-10 s of polling before declaring a timeout
 constexpr int SMEM_LIMIT = 226 * 1024;  // leaves room for the static smem (seen-flag bitset)
 // Epilogue output staging: per epilogue warp EB buffers of one 32-row x 64-column bf16
 // box (128 B rows, TMA SWIZZLE_128B layout: full-line writes), stored with
@@ -125,6 +124,7 @@ struct alignas(64) TileParams {
   uint32_t* counters;      // local tile counters
   uint32_t* abort_word;
   uint32_t epoch;          // value a flag must reach (1: one-shot flags)
+  unsigned long long timeout_ns;  // flag waits abort after this long (FICCO_FLAG_TIMEOUT_S, default 30 s)
   float alpha;
   // optional timeline (ns, %globaltimer): [0, gridDim) CTA start; then per tile
   // {loads may start (flags satisfied), accumulator stored}
@@ -139,17 +139,24 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 
 // Poll a flag written by another agent (copy engine, peer GPU) until it reaches
 // `epoch` (wrap-safe) with acquire loads (a sys-scope fence per flag would cost
-// microseconds; the acquire load itself orders the following reads). On
-// timeout raise the abort word and give up so the kernel drains instead of
-// hanging the device.
-__device__ __forceinline__ void wait_flag(const uint32_t* f, uint32_t epoch, uint32_t* abort_word) {
+// microseconds; the acquire load itself orders the following reads). After
+// `timeout_ns` of waiting (%globaltimer; TileParams.timeout_ns) raise the abort word
+// and give up so the kernel drains instead of hanging the device.
+__device__ __forceinline__ void wait_flag(const uint32_t* f, uint32_t epoch, uint32_t* abort_word,
+                                          unsigned long long timeout_ns) {
   uint32_t spins = 0;
+  unsigned long long t0 = 0;
   while (static_cast<int32_t>(ld_acquire_sys(f) - epoch) < 0) {
-    if (++spins >= SPIN_LIMIT) {
-      atomicExch(abort_word, 1u);
-      break;
+    if ((++spins & 1023u) == 0) {
+      const unsigned long long now = globaltimer();
+      if (t0 == 0) {
+        t0 = now;
+      } else if (now - t0 > timeout_ns) {
+        atomicExch(abort_word, 1u);
+        break;
+      }
+      if (*reinterpret_cast<volatile uint32_t*>(abort_word)) break;
     }
-    if ((spins & 1023u) == 0 && *reinterpret_cast<volatile uint32_t*>(abort_word)) break;
     __nanosleep(64);
   }
   // make the copy-engine-written bytes visible to the async (TMA) proxy
@@ -162,10 +169,10 @@ __device__ __forceinline__ void wait_flag(const uint32_t* f, uint32_t epoch, uin
 constexpr int SEEN_WORDS = FICCO_FLAG_BLOCK / 32;
 
 __device__ __forceinline__ void wait_flag_cached(uint32_t* seen, const uint32_t* flags, int idx, uint32_t epoch,
-                                                 uint32_t* abort_word) {
+                                                 uint32_t* abort_word, unsigned long long timeout_ns) {
   const uint32_t bit = 1u << (idx & 31);
   if (seen[idx >> 5] & bit) return;
-  wait_flag(flags + idx, epoch, abort_word);
+  wait_flag(flags + idx, epoch, abort_word, timeout_ns);
   seen[idx >> 5] |= bit;
 }
 
@@ -195,7 +202,7 @@ __device__ __forceinline__ void producer_loop(const TileParams& p, uint8_t* sA, 
           const uint32_t window = uint32_t(((uint64_t(w1) << 32) | w0) >> (base & 31));
           if ((window & td.fmask) != td.fmask)
             for (uint32_t m = td.fmask; m; m &= m - 1)
-              wait_flag_cached(seen, p.flags, base + (__ffs(m) - 1), p.epoch, p.abort_word);
+              wait_flag_cached(seen, p.flags, base + (__ffs(m) - 1), p.epoch, p.abort_word, p.timeout_ns);
         }
       }
       if (kb == 0 && p.trace) p.trace[gridDim.x + 2 * t] = globaltimer();
@@ -220,7 +227,8 @@ __device__ __forceinline__ void producer_loop(const TileParams& p, uint8_t* sA, 
       // receive slots) stream through the same ring as A operands against an identity B,
       // so the reduction rides the TMA/tensor pipeline instead of the epilogue's loads.
       for (int j = 0; j < p.n_recv; ++j)
-        wait_flag_cached(seen, p.flags, p.rs_flag0 + td.chunk * p.n_recv + j, p.rs_target, p.abort_word);
+        wait_flag_cached(seen, p.flags, p.rs_flag0 + td.chunk * p.n_recv + j, p.rs_target, p.abort_word,
+                         p.timeout_ns);
       for (int j = 0; j < p.n_recv; ++j) {
         for (int kb = 0; kb < Cfg::RKB; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1u);
@@ -390,7 +398,7 @@ __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfu
       // peers' partial chunks must have landed in our receive slots
       if (threadIdx.x == 64) {
         for (int j = 0; j < p.n_recv; ++j)
-          wait_flag(p.flags + p.rs_flag0 + td.chunk * p.n_recv + j, p.rs_target, p.abort_word);
+          wait_flag(p.flags + p.rs_flag0 + td.chunk * p.n_recv + j, p.rs_target, p.abort_word, p.timeout_ns);
       }
       named_bar_sync(1, EPI_THREADS);
     }
@@ -403,7 +411,7 @@ __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfu
     const bool reduce_row = epi_reduce && row_ok;
     if (remote && !go_seen) {
       // the owners' receive slots are free once the DONE barrier of this run passed
-      if (p.go_flag > 0 && lane == 0) wait_flag(p.flags + p.go_flag, p.epoch, p.abort_word);
+      if (p.go_flag > 0 && lane == 0) wait_flag(p.flags + p.go_flag, p.epoch, p.abort_word, p.timeout_ns);
       __syncwarp();
       go_seen = true;
     }

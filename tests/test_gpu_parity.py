@@ -279,3 +279,31 @@ def test_typed_entry_points_check_the_plan_role(lib):
         grp.comm.check()
     finally:
         grp.close()
+
+
+def test_missing_transfer_times_out_as_deadlock_error(lib, monkeypatch):
+    """A tile program whose readiness flags are never set (copy program dropped) aborts after
+    FICCO_FLAG_TIMEOUT_S and surfaces as the reference's engine.DeadlockError."""
+    import time
+    from paper_2512_10236_b200 import ops
+    from paper_2512_10236_b200.lowering import lower_ag
+    from paper_2512_10236_b200.routing import ScheduleKind, build_plan
+    from paper_2512_10236_b200.simulator import DeadlockError
+    G, R, K, N = 4, 256, 256, 256
+    grp = ops.FiccoGroup.virtual_group(G, 0)
+    try:
+        low = lower_ag(build_plan(ops._scenario("t", G * R, N, K, G), ScheduleKind.HETERO_UNFUSED_1D), 0, "A")
+        grp.ensure_workspace(low.ws_bytes)
+        plan = lib.Plan(grp.comm, low.desc, [], list(low.tiles))  # no copies: XFER flags never set
+        a = torch.zeros(R, K, dtype=torch.bfloat16, device="cuda")
+        w = torch.zeros(N, K, dtype=torch.bfloat16, device="cuda")
+        c = torch.empty(G * R, N, dtype=torch.bfloat16, device="cuda")
+        monkeypatch.setenv("FICCO_FLAG_TIMEOUT_S", "1")
+        t0 = time.time()
+        plan.run(a, w, c)
+        with pytest.raises(DeadlockError):
+            grp.comm.check()
+        assert time.time() - t0 < 30
+        plan.close()
+    finally:
+        grp.close()
