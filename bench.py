@@ -580,7 +580,7 @@ def our_arm(args) -> None:
     from paper_2512_10236_b200.selector import select_schedule
     runtime.load_library()
 
-    G = G_VIRTUAL if world == 1 else world
+    G = args.virtual_ranks if world == 1 else world
     peaks, peaks_src = load_peaks()
     wl = WORKLOADS[args.workload](torch, dev, G, rank, world, ops)
     wl.inplace = args.input == "slot" and hasattr(wl, "shards") and args.workload == "c2"
@@ -773,6 +773,8 @@ def main() -> None:
     ap.add_argument("--impl", default="ficco", choices=["ficco", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--kinds", default="", help="comma-separated subset of schedules")
+    ap.add_argument("--virtual-ranks", type=int, default=G_VIRTUAL,
+                    help="N=1 only: the job size G this GPU plays rank 0 of (C3 is quoted at G = 2, 4 and 8)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
     ap.add_argument("--no-core", action="store_true", help="skip the comm_agent=core (SM copies) comparison")
     ap.add_argument("--input", default="slot", choices=["slot", "copy"],
