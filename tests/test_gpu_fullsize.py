@@ -1,4 +1,4 @@
-"""GPU parity at BASELINE.json's full sizes (C2, C3, C4 and the EP corpus case at G = 8, virtual peers
+"""GPU parity at BASELINE.json's full sizes (C2, C4 and the EP corpus case at G = 8, C3 at G = 2, 4, 8; virtual peers
 on one B200).
 
 The CPU oracle cannot run these shapes in seconds, so the checks are the size-independent
@@ -92,9 +92,11 @@ def test_c2_full_size_all_kinds_bit_identical(ops, rank):
     np.testing.assert_allclose(_np(plain[rows]), want, rtol=RTOL, atol=ATOL)
 
 
-def test_c3_full_size_all_kinds_bit_identical(ops):
-    """C3: Llama-3-70B down-proj GEMM->RS, (M, N, K/G) = (16384, 8192, 3584), G = 8, rank 0."""
-    rank, M, Kg, N = 0, 16384, 3584, 8192
+@pytest.mark.parametrize("world", [8, 4, 2])
+def test_c3_full_size_all_kinds_bit_identical(ops, world):
+    """C3: Llama-3-70B down-proj GEMM->RS, (M, N, K/G) = (16384, 8192, 28672 / G) at G = 2, 4, 8, rank 0."""
+    G = world
+    rank, M, Kg, N = 0, 16384, 28672 // G, 8192
     R = M // G
     a = _rand((M, Kg), 200)
     w = _rand((N, Kg), 201, "normal")
