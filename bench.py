@@ -176,9 +176,14 @@ class AGWorkload:
     kinds = ["uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d", "uniform_fused_2d", "shard_overlap_p2p",
              "serial"]
 
+    @staticmethod
+    def shape(G):
+        """Per-GPU post-gather GEMM (M, N, K): seq 8192, N = gate||up of 14336 / G (3584 at G = 8), d 4096."""
+        return 8192, 2 * 14336 // G, 4096
+
     def __init__(self, torch, dev, G, rank, world, ops):
         self.t, self.dev, self.G, self.rank, self.world, self.ops = torch, dev, G, rank, world, ops
-        self.M, self.N, self.K = 8192, 3584, 4096
+        self.M, self.N, self.K = self.shape(G)
         self.R = self.M // G
         gen = torch.Generator(device=dev).manual_seed(rank)
         self.shards = [(torch.rand(self.R, self.K, generator=gen, device=dev) * 2 - 1).to(torch.bfloat16)
@@ -557,7 +562,19 @@ class EPWorkload(AGWorkload):
         return per_op, f"numpy fp32 expert GEMM of 1024 of {self.M} dispatched rows, scaled linearly"
 
 
-WORKLOADS = {"c2": AGWorkload, "c3": RSWorkload, "c4": CPWorkload, "ep": EPWorkload}
+class AG70Workload(AGWorkload):
+    """C3': Llama-3-70B TP/SP MLP up-projection all-gather -> GEMM (the north star's 70B AG target):
+    seq 16384, N = gate||up of 28672 / G (7168 at G = 8), d 8192."""
+
+    key = "c3p"
+    title = "C3' Llama-3-70B TP/SP MLP up-proj AG->GEMM"
+
+    @staticmethod
+    def shape(G):
+        return 16384, 2 * 28672 // G, 8192
+
+
+WORKLOADS = {"c2": AGWorkload, "c3": RSWorkload, "c4": CPWorkload, "ep": EPWorkload, "c3p": AG70Workload}
 
 
 def our_arm(args) -> None:
@@ -583,7 +600,7 @@ def our_arm(args) -> None:
     G = args.virtual_ranks if world == 1 else world
     peaks, peaks_src = load_peaks()
     wl = WORKLOADS[args.workload](torch, dev, G, rank, world, ops)
-    wl.inplace = args.input == "slot" and hasattr(wl, "shards") and args.workload == "c2"
+    wl.inplace = args.input == "slot" and hasattr(wl, "shards") and args.workload in ("c2", "c3p")
     grp = ops.FiccoGroup.distributed() if world > 1 else ops.FiccoGroup.virtual_group(G, 0)
     flush_buf = torch.empty(256 * 2**20, dtype=torch.uint8, device=dev)
     flush = lambda: flush_buf.fill_(1)  # noqa: E731
