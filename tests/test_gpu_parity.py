@@ -307,3 +307,46 @@ def test_missing_transfer_times_out_as_deadlock_error(lib, monkeypatch):
         plan.close()
     finally:
         grp.close()
+
+
+@pytest.mark.parametrize("agent", ["dma", "core"])
+@pytest.mark.parametrize("kind", ["uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d"])
+def test_rs_ragged_chunks(lib, kind, agent):
+    """GEMM -> RS with 96-row fine chunks (REDUCE boxes straddle slots), a K tail of 8 and an N tail of 32."""
+    from paper_2512_10236_b200 import ops
+    G, rank = 4, 2
+    M, Kg, N = 96 * G * G, 200, 544
+    a = [orc.seeded_inputs(11, p, (M, Kg)) for p in range(G)]
+    w = [orc.seeded_inputs(11, 100 + p, (N, Kg), "normal") for p in range(G)]
+    want = orc.execute_rs(a, w)[rank]
+    R = M // G
+    peers = [orc.bf16_round(a[p] @ w[p].T)[rank * R:(rank + 1) * R] for p in range(G) if p != rank]
+    grp = ops.FiccoGroup.virtual_group(G, rank)
+    try:
+        _, low, _ = ops.prepare_rs(grp, M, Kg, N, kind, comm_agent=agent)
+        grp.load_peer_partials(low, [_t(x) for x in peers])
+        for _ in range(2):
+            out = ops.matmul_reduce_scatter(_t(a[rank]), _t(w[rank]), kind=kind, group=grp, comm_agent=agent)
+            grp.comm.check()
+            np.testing.assert_allclose(_np(out), want, rtol=RTOL, atol=ATOL * math.sqrt(G))
+    finally:
+        grp.close()
+
+
+@pytest.mark.parametrize("kind", ["shard_overlap_p2p", "hetero_unfused_1d"])
+def test_cp_ragged(lib, kind):
+    """CP QK^T with 96-row kv chunks and a query count that is not a multiple of the tile width."""
+    from paper_2512_10236_b200 import ops
+    G, rank, d, Tq, Tkv = 4, 3, 128, 416, 96 * 16
+    q = orc.seeded_inputs(12, 50, (Tq, d), "normal")
+    ks = [orc.seeded_inputs(12, p, (Tkv // G, d), "normal") for p in range(G)]
+    want, _ = orc.execute_cp_qk(q, ks, 1.0 / math.sqrt(d))
+    grp = ops.FiccoGroup.virtual_group(G, rank)
+    try:
+        _, low, _ = ops.prepare_cp(grp, Tq, d, Tkv, kind)
+        grp.load_peer_shards(low, [_t(x) for x in ks])
+        out = ops.cp_kv_all_gather_qk(_t(q), _t(ks[rank]), kind=kind, group=grp)
+        grp.comm.check()
+        np.testing.assert_allclose(_np(out), want, rtol=RTOL, atol=ATOL)
+    finally:
+        grp.close()
