@@ -8,6 +8,7 @@ from paper_2512_10236_b200.domain import Collective
 from paper_2512_10236_b200.lowering import (F_RING, F_XFER, W_L2_BYTES, lower_ag, lower_rs, pair_tiles,
                                             raster)
 from paper_2512_10236_b200.ops import _scenario
+from paper_2512_10236_b200 import routing
 from paper_2512_10236_b200.routing import ScheduleKind, build_plan
 from paper_2512_10236_b200.runtime import EPI_REDUCE, EPI_STORE_REMOTE, EPI_STORE_SIGNAL
 
@@ -92,3 +93,22 @@ def test_pair_tiles_pads_unmatched_tiles_with_zero_row_partners():
     assert (_coverage(low.tiles, 8 * 96 * 8, 256) == 1).all()
     again = pair_tiles(list(low.tiles))
     assert len(again) >= len(low.tiles)
+
+
+@pytest.mark.parametrize("call", ["ag", "rs", "cp", "a2a"])
+def test_empty_and_indivisible_shapes_raise_reference_errors(call):
+    """Empty operands raise the reference's ValueError (GemmShape validation, core.py:47-64) and
+    rows that do not split into G^2 fine chunks raise PlanError (planner.py:30), before any GPU work."""
+    from paper_2512_10236_b200 import ops
+    grp = ops.FiccoGroup.virtual_group(4, 0)
+    prep = {"ag": lambda r, k, n: ops.prepare_ag(grp, r, k, n, "uniform_fused_1d"),
+            "a2a": lambda r, k, n: ops.prepare_a2a(grp, r, k, n, "uniform_fused_1d"),
+            "rs": lambda r, k, n: ops.prepare_rs(grp, 4 * r, k, n, "uniform_fused_1d"),
+            "cp": lambda r, k, n: ops.prepare_cp(grp, n, k, 4 * r, "uniform_fused_1d")}[call]
+    with pytest.raises(ValueError):
+        prep(0, 256, 256)          # no rows
+    with pytest.raises(ValueError):
+        prep(64, 256, 0)           # no output columns
+    with pytest.raises(routing.PlanError):
+        prep(2, 256, 256)          # 8 rows over G = 4: not divisible by G^2 = 16
+    assert grp.comm is None        # nothing was allocated
