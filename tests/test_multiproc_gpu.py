@@ -42,6 +42,7 @@ def _worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     errors = []
     calls = 3 if world < 8 else 2  # 8 processes time-slice one GPU: keep both parities, fewer repeats
+    calls = int(os.environ.get("FICCO_MP_CALLS", calls))  # stress runs: many consecutive calls per kind
     try:
         grp = ops.FiccoGroup.distributed()
         t = lambda x: torch.from_numpy(x).to(torch.bfloat16).cuda()  # noqa: E731
