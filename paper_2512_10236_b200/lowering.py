@@ -68,6 +68,13 @@ F_RING = 704     # + step i: ring step i landed
 F_RS = 1024      # + chunk*(G-1) + slot: a peer's partial chunk landed (RS; with comm_agent='core' a tile count)
 F_GO = 258       # RS core: the DONE barrier passed, owners' receive slots may be written (run-local)
 EV_START = 0     # event slot: the cross-rank barrier passed
+EV_RING = 1      # + (step-1)*split + part: shard-ring step fork / part-landed events (ring_split > 1)
+
+
+def ring_split() -> int:
+    """Copy-engine chains per shard-ring step (FICCO_RING_SPLIT, default 1): the step's shard
+    is pulled as that many row blocks on parallel copy streams, joined before RING[i]."""
+    return max(1, min(8, int(os.environ.get("FICCO_RING_SPLIT", "1"))))
 MAX_WORLD = 16
 
 ELT = 2  # bf16
@@ -317,11 +324,26 @@ def lower_ag(plan: ExecutionPlan, rank: int, gathered: str = "A", alpha: float =
         right = (g + 1) % G
         ops.append(_op(OP_STREAM_WAIT, value=EV_START, stream=1))
         ops.append(_op(OP_NOTIFY, peer=right, flag=F_RINGN + 0, stream=1))
+        split = ring_split()
+        bounds = [R * j // split for j in range(split + 1)]
         for x in xfers:
             i = x.round_idx + 1
             shard = (g - i) % G
             ops.append(_op(OP_WAIT, flag=F_RINGN + i - 1, stream=1))
-            ops.append(pull(x.src, shard * R, R, 1))
+            if split == 1:
+                ops.append(pull(x.src, shard * R, R, 1))
+            else:  # the shard as `split` row blocks on parallel copy streams 1, 2, ..., joined on stream 1
+                ev = EV_RING + (i - 1) * split
+                ops.append(_op(OP_RECORD, value=ev, stream=1))
+                for j in range(split):
+                    st = 1 + j
+                    if j:
+                        ops.append(_op(OP_STREAM_WAIT, value=ev, stream=st))
+                    ops.append(pull(x.src, shard * R + bounds[j], bounds[j + 1] - bounds[j], st))
+                    if j:
+                        ops.append(_op(OP_RECORD, value=ev + j, stream=st))
+                for j in range(1, split):
+                    ops.append(_op(OP_STREAM_WAIT, value=ev + j, stream=1))
             ops.append(_op(OP_SIGNAL, flag=F_RING + i, stream=1))
             if i < G - 1:
                 ops.append(_op(OP_NOTIFY, peer=right, flag=F_RINGN + i, stream=1))

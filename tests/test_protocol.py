@@ -249,3 +249,12 @@ def test_rs_core_without_done_barrier_is_caught():
             wrong.append("error")
         bad += bool(wrong)
     assert bad > 0
+
+
+@pytest.mark.parametrize("split", [2, 3])
+@pytest.mark.parametrize("G", [2, 4])
+def test_ag_ring_split_protocol(split, G, monkeypatch):
+    """The shard ring with each step's pull split over parallel copy streams (FICCO_RING_SPLIT):
+    every part lands before RING[i] and before the right neighbour is notified."""
+    monkeypatch.setenv("FICCO_RING_SPLIT", str(split))
+    test_ag_protocol("shard_overlap_p2p", G, 2)
