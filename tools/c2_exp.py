@@ -40,9 +40,10 @@ def timeit(fn, steps=30):
 
 a_full = torch.cat(shards)
 print("gemm_bf16 (flag-free kernel)", round(timeit(lambda: runtime.gemm_bf16(a_full, w, out)), 1), flush=True)
-for kind in sys.argv[1:] or ["shard_overlap_p2p", "hetero_unfused_1d"]:
+INPLACE = "--inplace" in sys.argv  # zero-copy publish, as the bench runs C2
+for kind in [a for a in sys.argv[1:] if not a.startswith("--")] or ["shard_overlap_p2p", "hetero_unfused_1d"]:
     for variant in ["full", "noflags", "nocopies", "graph_only"]:
-        low = lowering.lower_ag(build_plan(sc, ScheduleKind(kind)), 0, "A")
+        low = lowering.lower_ag(build_plan(sc, ScheduleKind(kind)), 0, "A", inplace=INPLACE)
         grp.ensure_workspace(low.ws_bytes)
         if variant in ("noflags", "nocopies"):
             for t in low.tiles:
@@ -52,6 +53,9 @@ for kind in sys.argv[1:] or ["shard_overlap_p2p", "hetero_unfused_1d"]:
         if variant == "graph_only":
             low.tiles = []
         grp.load_peer_shards(low, shards)
+        if INPLACE:
+            for par in (0, 1):
+                grp.ws_tensor(0, low.gather_off + par * low.gather_par, (R, K)).copy_(shards[0])
         plan = Plan(grp.comm, low.desc, low.ops, low.tiles)
         print(kind, variant, round(timeit(lambda: plan.run(shards[0], w, out)), 1), flush=True)
         plan.close()
