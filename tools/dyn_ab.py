@@ -1,5 +1,8 @@
 """A/B of the tile kernel's static round-robin vs dynamic (atomic counter) tile schedule (FICCO_DYNAMIC).
 
+The dynamic schedule was measured slower everywhere and removed from the library;
+this script is kept to re-run the comparison on a build that has it (git history).
+
 For each (workload, schedule, agent) given: the bench workload's op, calls alternating between
 FICCO_DYNAMIC=0 and =1 (the library reads it per launch), timed interleaved step by step with L2
 flushed before every call (bench.time_interleaved); the plain GEMM of the workload's shape too.
