@@ -1,7 +1,7 @@
 """A/B of the tile kernel's static round-robin vs dynamic (atomic counter) tile schedule (FICCO_DYNAMIC).
 
 The dynamic schedule was measured slower everywhere and removed from the library;
-this script is kept to re-run the comparison on a build that has it (git history).
+the implementation was not committed; the script documents how it was measured.
 
 For each (workload, schedule, agent) given: the bench workload's op, calls alternating between
 FICCO_DYNAMIC=0 and =1 (the library reads it per launch), timed interleaved step by step with L2
