@@ -169,6 +169,7 @@ class AGWorkload:
     """C2: all-gather -> GEMM (TP/SP up-projection)."""
 
     inplace = False
+    checks_multi_rank = True  # check() needs only data every rank holds
     agent = "dma"  # comm_agent: copy engines ("dma") or SM copy kernels ("core")
 
     key = "c2"
@@ -185,9 +186,13 @@ class AGWorkload:
         self.t, self.dev, self.G, self.rank, self.world, self.ops = torch, dev, G, rank, world, ops
         self.M, self.N, self.K = self.shape(G)
         self.R = self.M // G
-        gen = torch.Generator(device=dev).manual_seed(rank)
-        self.shards = [(torch.rand(self.R, self.K, generator=gen, device=dev) * 2 - 1).to(torch.bfloat16)
-                       for _ in range(G)]
+        # shard p from seed 1000 + p on every rank: each rank publishes shards[rank] and can check
+        # the gathered result against the same global A at any N (parity_spot_check)
+        self.shards = []
+        for p in range(G):
+            gen = torch.Generator(device=dev).manual_seed(1000 + p)
+            self.shards.append((torch.rand(self.R, self.K, generator=gen, device=dev) * 2 - 1).to(torch.bfloat16))
+        self.local = self.shards[rank]
         wgen = torch.Generator(device=dev).manual_seed(99)
         self.w = (torch.randn(self.N, self.K, generator=wgen, device=dev) / math.sqrt(self.K)).to(torch.bfloat16)
         self.out = torch.empty(self.M, self.N, dtype=torch.bfloat16, device=dev)
@@ -205,14 +210,14 @@ class AGWorkload:
         if self.inplace:  # the shard already sits in this rank's workspace slot, both parities
             for par in (0, 1):
                 off = low.gather_off + par * low.gather_par + grp.rank * self.R * self.K * 2
-                grp.ws_tensor(grp.rank, off, (self.R, self.K)).copy_(self.shards[0])
+                grp.ws_tensor(grp.rank, off, (self.R, self.K)).copy_(self.local)
 
     def lowered(self, grp, kind):
         return self.ops.prepare_ag(grp, self.R, self.K, self.N, kind, inplace=self.inplace, comm_agent=self.agent)[1]
 
     def run_plan(self, plan):
         """A raw lowered plan with this workload's call arguments (copy-program timing)."""
-        plan.run(self.shards[0], self.w, self.out)
+        plan.run(self.local, self.w, self.out)
 
     def step(self, grp, kind):
         agent = self.agent  # bound now: steps of both agents are interleaved
@@ -221,14 +226,14 @@ class AGWorkload:
                 a = grp.input_slot(self.R, self.K, self.N, kind)
                 self.ops.all_gather_matmul(a, self.w, kind=kind, group=grp, out=self.out, comm_agent=agent)
             return fn
-        return lambda: self.ops.all_gather_matmul(self.shards[0], self.w, kind=kind, group=grp, out=self.out,
+        return lambda: self.ops.all_gather_matmul(self.local, self.w, kind=kind, group=grp, out=self.out,
                                                   comm_agent=agent)
 
     def serial(self):
         t = self.t
         if self.world > 1:
             def fn():
-                t.distributed.all_gather_into_tensor(self.gathered, self.shards[0])
+                t.distributed.all_gather_into_tensor(self.gathered, self.local)
                 t.matmul(self.gathered, self.w.T, out=self.out)
             return fn, "NCCL all_gather_into_tensor + cuBLAS"
 
@@ -253,9 +258,9 @@ class AGWorkload:
 
     def e2e(self, grp, kind):
         t = self.t
-        host_a = self.shards[0].cpu().pin_memory()
+        host_a = self.local.cpu().pin_memory()
         host_c = t.empty(self.M, self.N, dtype=t.bfloat16).pin_memory()
-        dev_a = t.empty_like(self.shards[0])
+        dev_a = t.empty_like(self.local)
 
         def fn():
             dev_a.copy_(host_a, non_blocking=True)
@@ -287,6 +292,8 @@ class AGWorkload:
 
 class RSWorkload(AGWorkload):
     """C3: GEMM -> reduce-scatter (TP/SP down-projection)."""
+
+    checks_multi_rank = False  # check() needs peers' data this rank does not hold
 
     key = "c3"
     title = "C3 Llama-3-70B TP/SP down-proj GEMM->RS"
@@ -380,6 +387,8 @@ class RSWorkload(AGWorkload):
 
 class CPWorkload(AGWorkload):
     """C4: context-parallel KV all-gather -> attention scores S = Q K^T / sqrt(d)."""
+
+    checks_multi_rank = False  # check() needs peers' data this rank does not hold
 
     key = "c4"
     title = "C4 CP KV all-gather -> QK^T, 128K context, d=128"
@@ -477,6 +486,8 @@ class EPWorkload(AGWorkload):
     """EP all-to-all (token dispatch) -> expert GEMM: the reference corpus row g14 (Mixtral,
     data/scenarios_corpus.csv:17): per-GPU post-dispatch GEMM (M, N, K) = (147456, 28672, 4096), G = 8.
     Not a BASELINE.json config; same metric and method."""
+
+    checks_multi_rank = False  # check() needs peers' data this rank does not hold
 
     key = "ep"
     title = "EP Mixtral all-to-all -> expert GEMM (corpus g14)"
@@ -644,7 +655,7 @@ def our_arm(args) -> None:
     wl.prepare(grp, best)
     wl.step(grp, best)()
     grp.comm.check()
-    parity = wl.check() if world == 1 else None
+    parity = wl.check() if world == 1 or wl.checks_multi_rank else None
 
     # the headline: the best (schedule, agent) and the serialized baseline timed interleaved, K steps each
     serial_fn, serial_desc = wl.serial()
