@@ -293,8 +293,6 @@ class AGWorkload:
 class RSWorkload(AGWorkload):
     """C3: GEMM -> reduce-scatter (TP/SP down-projection)."""
 
-    checks_multi_rank = False  # check() needs peers' data this rank does not hold
-
     key = "c3"
     title = "C3 Llama-3-70B TP/SP down-proj GEMM->RS"
     kinds = ["uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d"]
@@ -303,11 +301,22 @@ class RSWorkload(AGWorkload):
         self.t, self.dev, self.G, self.rank, self.world, self.ops = torch, dev, G, rank, world, ops
         self.M, self.N, self.K = 16384, 8192, 28672 // G
         self.R = self.M // G
-        gen = torch.Generator(device=dev).manual_seed(rank)
-        self.a = (torch.rand(self.M, self.K, generator=gen, device=dev) * 2 - 1).to(torch.bfloat16)
-        self.w = (torch.randn(self.N, self.K, generator=gen, device=dev) / math.sqrt(self.K)).to(torch.bfloat16)
-        self.peer_parts = [(torch.randn(self.R, self.N, generator=gen, device=dev) * 0.1).to(torch.bfloat16)
-                           for _ in range(G - 1)]
+        # rank g's operands from seeds 2000 + g / 3000 + g on every rank: each rank regenerates the peers'
+        # partials of its own rows, which are the virtual peers' data at N = 1 and the reference the
+        # parity spot check sums at any N (owner's fp32 partial + peers' bf16 partials, rank order)
+        def operands(g):
+            ga = torch.Generator(device=dev).manual_seed(2000 + g)
+            gw = torch.Generator(device=dev).manual_seed(3000 + g)
+            return ((torch.rand(self.M, self.K, generator=ga, device=dev) * 2 - 1).to(torch.bfloat16),
+                    (torch.randn(self.N, self.K, generator=gw, device=dev) / math.sqrt(self.K)).to(torch.bfloat16))
+        self.a, self.w = operands(rank)
+        self.own = slice(rank * self.R, (rank + 1) * self.R)
+        self.peer_parts = []
+        for g in range(G):
+            if g != rank:
+                a_g, w_g = operands(g)
+                self.peer_parts.append(torch.matmul(a_g[self.own], w_g.t()).to(torch.bfloat16))
+                del a_g, w_g
         self.out = torch.empty(self.R, self.N, dtype=torch.bfloat16, device=dev)
         self.part = torch.empty(self.M, self.N, dtype=torch.bfloat16, device=dev)
         self.sink = torch.empty((G - 1) * self.R, self.N, dtype=torch.bfloat16, device=dev)
@@ -359,7 +368,7 @@ class RSWorkload(AGWorkload):
         return lambda: runtime.gemm_bf16(self.a, self.w, self.part), "tensor", self.flops
 
     def check(self):
-        ref = self.a[:self.R].float() @ self.w.float().T
+        ref = self.a[self.own].float() @ self.w.float().T
         for p in self.peer_parts:
             ref += p.float()
         return bool(self.t.allclose(self.out.float(), ref, rtol=1.6e-2, atol=3e-2))
@@ -388,8 +397,6 @@ class RSWorkload(AGWorkload):
 class CPWorkload(AGWorkload):
     """C4: context-parallel KV all-gather -> attention scores S = Q K^T / sqrt(d)."""
 
-    checks_multi_rank = False  # check() needs peers' data this rank does not hold
-
     key = "c4"
     title = "C4 CP KV all-gather -> QK^T, 128K context, d=128"
     kinds = ["uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d", "shard_overlap_p2p", "serial"]
@@ -400,7 +407,13 @@ class CPWorkload(AGWorkload):
         self.R = self.Tkv // G
         gen = torch.Generator(device=dev).manual_seed(rank)
         self.q = torch.randn(self.Tq, self.d, generator=gen, device=dev).to(torch.bfloat16)
-        self.shards = [torch.randn(self.R, self.d, generator=gen, device=dev).to(torch.bfloat16) for _ in range(G)]
+        # K shard p from seed 1000 + p on every rank (this rank publishes shards[rank]): the score check
+        # needs only the local queries and the global K, so it runs at any N
+        self.shards = []
+        for p in range(G):
+            kgen = torch.Generator(device=dev).manual_seed(1000 + p)
+            self.shards.append(torch.randn(self.R, self.d, generator=kgen, device=dev).to(torch.bfloat16))
+        self.local = self.shards[rank]
         self.out = torch.empty(self.Tq, self.Tkv, dtype=torch.bfloat16, device=dev)
         self.kall = torch.empty(self.Tkv, self.d, dtype=torch.bfloat16, device=dev)
         self.scale = 1.0 / math.sqrt(self.d)
@@ -420,18 +433,18 @@ class CPWorkload(AGWorkload):
             grp.load_peer_shards(low, self.shards)
 
     def run_plan(self, plan):
-        plan.run(self.q, self.shards[0], self.out)
+        plan.run(self.q, self.local, self.out)
 
     def step(self, grp, kind):
         agent = self.agent
-        return lambda: self.ops.cp_kv_all_gather_qk(self.q, self.shards[0], kind=kind, group=grp, out=self.out,
+        return lambda: self.ops.cp_kv_all_gather_qk(self.q, self.local, kind=kind, group=grp, out=self.out,
                                                     comm_agent=agent)
 
     def serial(self):
         t = self.t
         if self.world > 1:
             def fn():
-                t.distributed.all_gather_into_tensor(self.kall, self.shards[0])
+                t.distributed.all_gather_into_tensor(self.kall, self.local)
                 t.addmm(self.out, self.q, self.kall.T, beta=0, alpha=self.scale, out=self.out)
             return fn, "NCCL all_gather_into_tensor + cuBLAS (alpha = 1/sqrt(d))"
 
@@ -457,9 +470,9 @@ class CPWorkload(AGWorkload):
     def e2e(self, grp, kind):
         t = self.t
         host_q = self.q.cpu().pin_memory()
-        host_k = self.shards[0].cpu().pin_memory()
+        host_k = self.local.cpu().pin_memory()
         host_s = t.empty(self.Tq, self.Tkv, dtype=t.bfloat16).pin_memory()
-        dq, dk = t.empty_like(self.q), t.empty_like(self.shards[0])
+        dq, dk = t.empty_like(self.q), t.empty_like(self.local)
 
         def fn():
             dq.copy_(host_q, non_blocking=True)
