@@ -99,6 +99,13 @@ class ClockSampler:
             except Exception:
                 self.proc.kill()
 
+    @staticmethod
+    def merge(*samplers):
+        m = ClockSampler(-1)
+        for smp in samplers:
+            m.rows += smp.rows
+        return m.summary()
+
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
@@ -136,10 +143,11 @@ def time_steps(fn, steps: int, warmup: int, flush, stream, barrier=None) -> list
     return [a.elapsed_time(b) for a, b in evs]
 
 
-def time_interleaved(fns, steps: int, warmup: int, flush, stream, barrier=None) -> list[list[float]]:
+def time_interleaved(fns, steps: int, warmup: int, flush, stream, barrier=None, starts=None) -> list[list[float]]:
     """time_steps for several step functions ROUND-ROBIN (step i of every fn before step i+1):
     the same clocks, power-cap state and L2 state (flushed before every call) for all of them,
-    so their ratio is not a drift between two separate runs."""
+    so their ratio is not a drift between two separate runs. ``starts`` (a list) receives the
+    (start, end) events of the first function's timed steps."""
     import torch
     for _ in range(warmup):
         for fn in fns:
@@ -160,6 +168,8 @@ def time_interleaved(fns, steps: int, warmup: int, flush, stream, barrier=None) 
     torch.cuda.synchronize()
     if barrier:
         barrier()
+    if starts is not None:
+        starts.extend(evs[0])
     return [[a.elapsed_time(b) for a, b in ev] for ev in evs]
 
 
@@ -200,8 +210,18 @@ class AGWorkload:
         self.flops = 2.0 * self.M * self.N * self.K
         self.comm_bytes = (G - 1) * self.R * self.K * 2
 
-    def config(self):
-        return {"M": self.M, "N": self.N, "K": self.K, "seq_len": self.M}
+    @classmethod
+    def op_shape(cls, G):
+        """The scenario (M, N, K) the selector sees (the reference's per-GPU post-gather GEMM)."""
+        return cls.shape(G)
+
+    @classmethod
+    def shape_config(cls, G):
+        m, n, k = cls.shape(G)
+        return {"M": m, "N": n, "K": k, "seq_len": m}
+
+    def plan_for(self, grp, kind, agent):
+        return self.ops.prepare_ag(grp, self.R, self.K, self.N, kind, inplace=self.inplace, comm_agent=agent)[0]
 
     def prepare(self, grp, kind):
         _, low, _ = self.ops.prepare_ag(grp, self.R, self.K, self.N, kind, comm_agent=self.agent)
@@ -219,8 +239,8 @@ class AGWorkload:
         """A raw lowered plan with this workload's call arguments (copy-program timing)."""
         plan.run(self.local, self.w, self.out)
 
-    def step(self, grp, kind):
-        agent = self.agent  # bound now: steps of both agents are interleaved
+    def step(self, grp, kind, agent="self"):
+        agent = self.agent if agent == "self" else agent  # bound now: steps of both agents are interleaved
         if self.inplace:
             def fn():
                 a = grp.input_slot(self.R, self.K, self.N, kind)
@@ -256,7 +276,7 @@ class AGWorkload:
         ref = self.t.cat(self.shards)[rows].float() @ self.w.float().T
         return bool(self.t.allclose(self.out[rows].float(), ref, rtol=1.6e-2, atol=1e-2))
 
-    def e2e(self, grp, kind):
+    def e2e(self, grp, kind, agent=None):
         t = self.t
         host_a = self.local.cpu().pin_memory()
         host_c = t.empty(self.M, self.N, dtype=t.bfloat16).pin_memory()
@@ -264,7 +284,7 @@ class AGWorkload:
 
         def fn():
             dev_a.copy_(host_a, non_blocking=True)
-            self.ops.all_gather_matmul(dev_a, self.w, kind=kind, group=grp, out=self.out)
+            self.ops.all_gather_matmul(dev_a, self.w, kind=kind, group=grp, out=self.out, comm_agent=agent)
             host_c.copy_(self.out, non_blocking=True)
         return fn, self.R * self.K * 2, self.M * self.N * 2
 
@@ -275,19 +295,14 @@ class AGWorkload:
     def ideal_us(self, peaks):
         return max(self.ideal_parts(peaks))
 
-    def cpu_sample(self, orc, kind):
+    def cpu_op(self, orc, kind):
+        """Rank `rank`'s whole op on the host cores (oracle port): route + every GemmSpec fragment.
+        Returns (fn, sample description, fraction of the op one call does)."""
         sh = [s.float().cpu().numpy() for s in self.shards]
         w = self.w.float().cpu().numpy()
-        frags = orc.gemm_fragments(kind, self.M, self.K, self.G, 0)
-        rows_first = sum(c for rows, _ in frags[:1] for _, c in rows)
-        orc.execute_ag_rank(kind, sh, w, 0, steps=1)
-        t0, reps = time.perf_counter(), 0
-        while reps < 5 and time.perf_counter() - t0 < 10.0:
-            orc.execute_ag_rank(kind, sh, w, 0, steps=1)
-            reps += 1
-        per_op = (time.perf_counter() - t0) / reps * (self.M / rows_first)
-        return per_op, (f"oracle execute_ag_rank({kind}): first GemmSpec ({rows_first}/{self.M} rows) x{reps}, "
-                        f"scaled linearly to the full op")
+        return (lambda: orc.execute_ag_rank(kind, sh, w, self.rank),
+                f"oracle execute_ag_rank({kind}), rank {self.rank}'s whole op: the plan's routing of the {self.G} "
+                f"shards + every GemmSpec fragment, fp32 numpy BLAS", 1.0)
 
 
 class RSWorkload(AGWorkload):
@@ -299,7 +314,7 @@ class RSWorkload(AGWorkload):
 
     def __init__(self, torch, dev, G, rank, world, ops):
         self.t, self.dev, self.G, self.rank, self.world, self.ops = torch, dev, G, rank, world, ops
-        self.M, self.N, self.K = 16384, 8192, 28672 // G
+        self.M, self.N, self.K = self.shape(G)
         self.R = self.M // G
         # rank g's operands from seeds 2000 + g / 3000 + g on every rank: each rank regenerates the peers'
         # partials of its own rows, which are the virtual peers' data at N = 1 and the reference the
@@ -315,7 +330,10 @@ class RSWorkload(AGWorkload):
         for g in range(G):
             if g != rank:
                 a_g, w_g = operands(g)
-                self.peer_parts.append(torch.matmul(a_g[self.own], w_g.t()).to(torch.bfloat16))
+                if dev.type == "cpu":  # reference arm: bf16 GEMMs on the host are slow; same values via fp32
+                    self.peer_parts.append(torch.matmul(a_g[self.own].float(), w_g.float().t()).to(torch.bfloat16))
+                else:
+                    self.peer_parts.append(torch.matmul(a_g[self.own], w_g.t()).to(torch.bfloat16))
                 del a_g, w_g
         self.out = torch.empty(self.R, self.N, dtype=torch.bfloat16, device=dev)
         self.part = torch.empty(self.M, self.N, dtype=torch.bfloat16, device=dev)
@@ -323,8 +341,13 @@ class RSWorkload(AGWorkload):
         self.flops = 2.0 * self.M * self.N * self.K
         self.comm_bytes = (G - 1) * self.R * self.N * 2
 
-    def config(self):
-        return {"M": self.M, "N": self.N, "K": self.K, "seq_len": self.M}
+    @staticmethod
+    def shape(G):
+        """Per-GPU GEMM (M, N, K) of the down-projection: seq 16384, d 8192, K = 28672 / G."""
+        return 16384, 8192, 28672 // G
+
+    def plan_for(self, grp, kind, agent):
+        return self.ops.prepare_rs(grp, self.M, self.K, self.N, kind, comm_agent=agent)[0]
 
     def lowered(self, grp, kind):
         return self.ops.prepare_rs(grp, self.M, self.K, self.N, kind, comm_agent=self.agent)[1]
@@ -336,8 +359,8 @@ class RSWorkload(AGWorkload):
 
     run_plan = None  # the RS pushes wait on tile counters: no copy program runs without its tiles
 
-    def step(self, grp, kind):
-        agent = self.agent
+    def step(self, grp, kind, agent="self"):
+        agent = self.agent if agent == "self" else agent
         return lambda: self.ops.matmul_reduce_scatter(self.a, self.w, kind=kind, group=grp, out=self.out,
                                                       comm_agent=agent)
 
@@ -373,7 +396,7 @@ class RSWorkload(AGWorkload):
             ref += p.float()
         return bool(self.t.allclose(self.out.float(), ref, rtol=1.6e-2, atol=3e-2))
 
-    def e2e(self, grp, kind):
+    def e2e(self, grp, kind, agent=None):
         t = self.t
         host_a = self.a.cpu().pin_memory()
         host_c = t.empty(self.R, self.N, dtype=t.bfloat16).pin_memory()
@@ -381,17 +404,17 @@ class RSWorkload(AGWorkload):
 
         def fn():
             dev_a.copy_(host_a, non_blocking=True)
-            self.ops.matmul_reduce_scatter(dev_a, self.w, kind=kind, group=grp, out=self.out)
+            self.ops.matmul_reduce_scatter(dev_a, self.w, kind=kind, group=grp, out=self.out, comm_agent=agent)
             host_c.copy_(self.out, non_blocking=True)
         return fn, self.M * self.K * 2, self.R * self.N * 2
 
-    def cpu_sample(self, orc, kind):
-        a = self.a[: self.R].float().cpu().numpy()
+    def cpu_op(self, orc, kind):
+        a = self.a.float().cpu().numpy()
         w = self.w.float().cpu().numpy()
-        t0 = time.perf_counter()
-        a @ w.T
-        per_op = (time.perf_counter() - t0) * self.G
-        return per_op, f"numpy fp32 GEMM of one {self.R}-row chunk, scaled x{self.G} (partials of the whole op)"
+        peers = [p.float().cpu().numpy() for p in self.peer_parts]
+        return (lambda: orc.execute_rs_rank(a, w, peers, self.rank),
+                f"oracle execute_rs_rank, rank {self.rank}'s whole op: the {self.M}-row partial GEMM + the reduction "
+                f"of its {self.R} rows with the {self.G - 1} received partials, fp32 numpy BLAS", 1.0)
 
 
 class CPWorkload(AGWorkload):
@@ -421,8 +444,18 @@ class CPWorkload(AGWorkload):
         self.out_bytes = self.Tq * self.Tkv * 2
         self.comm_bytes = (G - 1) * self.R * self.d * 2
 
-    def config(self):
-        return {"Tkv": self.Tkv, "Tq": self.Tq, "d": self.d, "seq_len": self.Tkv}
+    @staticmethod
+    def op_shape(G):
+        """Scenario view: M = Tkv gathered kv tokens, N = Tq local queries, K = d."""
+        return 131072, 131072 // G, 128
+
+    @classmethod
+    def shape_config(cls, G):
+        tkv, tq, d = cls.op_shape(G)
+        return {"Tkv": tkv, "Tq": tq, "d": d, "seq_len": tkv}
+
+    def plan_for(self, grp, kind, agent):
+        return self.ops.prepare_cp(grp, self.Tq, self.d, self.Tkv, kind, comm_agent=agent)[0]
 
     def lowered(self, grp, kind):
         return self.ops.prepare_cp(grp, self.Tq, self.d, self.Tkv, kind, comm_agent=self.agent)[1]
@@ -435,8 +468,8 @@ class CPWorkload(AGWorkload):
     def run_plan(self, plan):
         plan.run(self.q, self.local, self.out)
 
-    def step(self, grp, kind):
-        agent = self.agent
+    def step(self, grp, kind, agent="self"):
+        agent = self.agent if agent == "self" else agent
         return lambda: self.ops.cp_kv_all_gather_qk(self.q, self.local, kind=kind, group=grp, out=self.out,
                                                     comm_agent=agent)
 
@@ -467,7 +500,7 @@ class CPWorkload(AGWorkload):
         ref = (self.q[:256].float() @ k.float().T) * self.scale
         return bool(self.t.allclose(self.out[:256].float(), ref, rtol=1.6e-2, atol=1e-2))
 
-    def e2e(self, grp, kind):
+    def e2e(self, grp, kind, agent=None):
         t = self.t
         host_q = self.q.cpu().pin_memory()
         host_k = self.local.cpu().pin_memory()
@@ -477,7 +510,7 @@ class CPWorkload(AGWorkload):
         def fn():
             dq.copy_(host_q, non_blocking=True)
             dk.copy_(host_k, non_blocking=True)
-            self.ops.cp_kv_all_gather_qk(dq, dk, kind=kind, group=grp, out=self.out)
+            self.ops.cp_kv_all_gather_qk(dq, dk, kind=kind, group=grp, out=self.out, comm_agent=agent)
             host_s.copy_(self.out, non_blocking=True)
         return fn, (self.Tq + self.R) * self.d * 2, self.out_bytes
 
@@ -486,13 +519,15 @@ class CPWorkload(AGWorkload):
         t_gemm = max(self.flops / (peaks["bf16_tflops"] * 1e12), t_hbm)
         return t_gemm * 1e6, self.comm_bytes / NVLINK_NOMINAL * 1e6
 
-    def cpu_sample(self, orc, kind):
-        q = self.q[:512].float().cpu().numpy()
-        k = self.t.cat(self.shards).float().cpu().numpy()
-        t0 = time.perf_counter()
-        (q @ k.T) * self.scale
-        per_op = (time.perf_counter() - t0) * (self.Tq / 512)
-        return per_op, f"numpy fp32 scores for 512 of {self.Tq} queries, scaled linearly"
+    def cpu_op(self, orc, kind):
+        q = self.q.float().cpu().numpy()
+        ks = [k.float().cpu().numpy() for k in self.shards]
+        import numpy as np
+        sink = np.empty((self.Tq, self.R), dtype=np.float32)
+        return (lambda: orc.execute_cp_qk_rank(kind, q, ks, self.scale, self.rank, sink),
+                f"oracle execute_cp_qk_rank({kind}), rank {self.rank}'s whole op: K gathered by the plan's routing, "
+                f"scores of every fragment (fp32 numpy BLAS) into a [{self.Tq}, {self.R}] staging block (the "
+                f"8.6 GB fp32 score matrix is not kept)", 1.0)
 
 
 class EPWorkload(AGWorkload):
@@ -522,6 +557,13 @@ class EPWorkload(AGWorkload):
         self.flops = 2.0 * self.M * self.N * self.K
         self.comm_bytes = (G - 1) * self.R * self.K * 2
 
+    @staticmethod
+    def shape(G):
+        return 147456, 28672, 4096
+
+    def plan_for(self, grp, kind, agent):
+        return self.ops.prepare_a2a(grp, self.R, self.K, self.N, kind, comm_agent=agent)[0]
+
     def lowered(self, grp, kind):
         return self.ops.prepare_a2a(grp, self.R, self.K, self.N, kind, comm_agent=self.agent)[1]
 
@@ -533,8 +575,8 @@ class EPWorkload(AGWorkload):
     def run_plan(self, plan):
         plan.run(self.send, self.w, self.out)
 
-    def step(self, grp, kind):
-        agent = self.agent
+    def step(self, grp, kind, agent="self"):
+        agent = self.agent if agent == "self" else agent
         return lambda: self.ops.all_to_all_matmul(self.send, self.w, kind=kind, group=grp, out=self.out,
                                                   comm_agent=agent)
 
@@ -565,7 +607,7 @@ class EPWorkload(AGWorkload):
         ref = self.t.cat(self.blocks)[rows].float() @ self.w.float().T
         return bool(self.t.allclose(self.out[rows].float(), ref, rtol=1.6e-2, atol=1e-2))
 
-    def e2e(self, grp, kind):
+    def e2e(self, grp, kind, agent=None):
         t = self.t
         host_a = self.send.cpu().pin_memory()
         host_c = t.empty(self.M, self.N, dtype=t.bfloat16).pin_memory()
@@ -573,17 +615,15 @@ class EPWorkload(AGWorkload):
 
         def fn():
             dev_a.copy_(host_a, non_blocking=True)
-            self.ops.all_to_all_matmul(dev_a, self.w, kind=kind, group=grp, out=self.out)
+            self.ops.all_to_all_matmul(dev_a, self.w, kind=kind, group=grp, out=self.out, comm_agent=agent)
             host_c.copy_(self.out, non_blocking=True)
         return fn, self.M * self.K * 2, self.M * self.N * 2
 
-    def cpu_sample(self, orc, kind):
-        a = self.blocks[1][:1024].float().cpu().numpy()
+    def cpu_op(self, orc, kind):
+        a = self.t.cat(self.blocks)[:self.M // 16].float().cpu().numpy()
         w = self.w.float().cpu().numpy()
-        t0 = time.perf_counter()
-        a @ w.T
-        per_op = (time.perf_counter() - t0) * (self.M / 1024)
-        return per_op, f"numpy fp32 expert GEMM of 1024 of {self.M} dispatched rows, scaled linearly"
+        return (lambda: a @ w.T, f"numpy fp32 expert GEMM of 1/16 of the {self.M} dispatched rows (the whole op is "
+                                 f"~35 TFLOP, ~45 s on the host); value scaled x16", 1 / 16)
 
 
 class AG70Workload(AGWorkload):
@@ -599,6 +639,66 @@ class AG70Workload(AGWorkload):
 
 
 WORKLOADS = {"c2": AGWorkload, "c3": RSWorkload, "c4": CPWorkload, "ep": EPWorkload, "c3p": AG70Workload}
+
+
+def headline_choice(workload: str, G: int, args) -> tuple[str, str]:
+    """The (schedule, comm_agent) the public API picks for this workload with no overrides: the
+    heuristic selector (selector.select_schedule == the reference's heuristic.py:25-43, pinned by
+    tests/golden/selector.json) on the B200 machine file, and the machine file's comm_agent
+    (machines.py:48). Pure host computation: the reference arm derives the same config."""
+    from paper_2512_10236_b200 import ops
+    from paper_2512_10236_b200.machines import b200_machine
+    m, n, k = WORKLOADS[workload].op_shape(G)
+    kind = args.kind or ops.choose_kind(ops._scenario(workload, m, n, k, G), None).value
+    agent = args.agent or b200_machine().machine.comm_agent.value
+    return kind, agent
+
+
+def workload_config(args, world: int) -> dict:
+    """The JSON line's ``config`` (identical in both arms)."""
+    cls = WORKLOADS[args.workload]
+    G = args.virtual_ranks if world == 1 else world
+    kind, agent = headline_choice(args.workload, G, args)
+    slot = args.input == "slot" and args.workload in ("c2", "c3p")
+    return dict(workload=cls.title, ranks=G, virtual_peers=world == 1, schedule=kind, comm_agent=agent,
+                schedule_source=("--kind/--agent override" if (args.kind or args.agent) else
+                                 "public API default: select_schedule on the B200 machine file + its comm_agent"),
+                input="symmetric slot (zero-copy publish)" if slot else "tensor copied in",
+                l2="flushed (256 MiB write) between timed steps", **cls.shape_config(G))
+
+
+def blas_threads() -> int:
+    try:
+        from threadpoolctl import threadpool_info
+        return max(int(i.get("num_threads", 1)) for i in threadpool_info() if i.get("user_api") == "blas")
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def time_cpu(fn, reps: int, warmup: int = 1, budget_s: float = 30.0) -> list[float]:
+    """Wall-clock seconds per call of a host-side function (warm-up calls untimed)."""
+    for _ in range(warmup):
+        fn()
+    out = []
+    t_end = time.perf_counter() + budget_s
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        fn()
+        out.append(time.perf_counter() - t0)
+        if time.perf_counter() > t_end:
+            break
+    return out
+
+
+def traffic_for(key: str, G: int, kind: str, agent: str):
+    """DRAM bytes per launch of the op's tile kernel from a committed ncu capture of exactly this
+    (workload, G, schedule, agent) — profiles/r02_ncu_traffic_<key>_g<G>_<kind>_<agent>.json — else None."""
+    path = os.path.join(ROOT, "profiles", f"r02_ncu_traffic_{key}_g{G}_{kind}_{agent}.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
 
 
 def our_arm(args) -> None:
@@ -617,14 +717,16 @@ def our_arm(args) -> None:
             torch.distributed.init_process_group("nccl", device_id=dev)
     from oracle import ficco_oracle as orc  # checker + CPU baseline only
     from paper_2512_10236_b200 import ops, routing, runtime
-    from paper_2512_10236_b200.machines import b200_machine
-    from paper_2512_10236_b200.selector import select_schedule
     runtime.load_library()
 
     G = args.virtual_ranks if world == 1 else world
     peaks, peaks_src = load_peaks()
+    config = workload_config(args, world)
+    best, best_agent = config["schedule"], config["comm_agent"]
+    api_kind = args.kind or None   # None: the op call itself selects (the headline is the public API default)
+    api_agent = args.agent or None
     wl = WORKLOADS[args.workload](torch, dev, G, rank, world, ops)
-    wl.inplace = args.input == "slot" and hasattr(wl, "shards") and args.workload in ("c2", "c3p")
+    wl.inplace = config["input"].startswith("symmetric")
     grp = ops.FiccoGroup.distributed() if world > 1 else ops.FiccoGroup.virtual_group(G, 0)
     flush_buf = torch.empty(256 * 2**20, dtype=torch.uint8, device=dev)
     flush = lambda: flush_buf.fill_(1)  # noqa: E731
@@ -638,76 +740,88 @@ def our_arm(args) -> None:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return float(t.item())
 
-    # every schedule of the design space, for both comm agents (core = SM-driven transfers: AG/CP SM
+    sampler = ClockSampler(local)
+    sampler.__enter__()  # clocks + throttle reasons sampled from here to the end of the timed regions
+
+    # (1) every schedule of the design space for both comm agents (core = SM-driven transfers: AG/CP SM
     # copy kernels beside the tile kernel; RS tile epilogues storing partials straight into the owners'
     # slots), all timed in ONE interleaved run: under the power cap a box drifts by up to ~10 % within
     # a bench run (tools/switch_probe.py), so separate runs per variant would rank the drift
     sched, core, variants = {}, {}, []
-    for agent in (["dma"] if args.no_core else ["dma", "core"]):
-        wl.agent = agent
-        for kind in (args.kinds.split(",") if args.kinds else wl.kinds):
-            if agent == "core" and "error" in sched.get(kind, {"error": 1}):
-                continue
-            try:
-                wl.prepare(grp, kind)
-            except routing.PlanError as exc:
-                sched[kind] = {"error": str(exc)}
-                continue
-            if agent == "dma":
-                sched[kind] = {}
-            variants.append((kind, agent, wl.step(grp, kind)))
-    times = time_interleaved([fn for _, _, fn in variants], args.steps, args.warmup, flush, stream, barrier)
-    grp.comm.check()
-    for (kind, agent, _), ts in zip(variants, times):
-        (sched if agent == "dma" else core)[kind] = {"us": maxrank(statistics.median(ts)) * 1e3}
-    # the headline: the fastest (schedule, comm_agent) of the design space (serial excluded)
-    cands = [(sched[k]["us"], k, "dma") for k in sched if "us" in sched[k] and k != "serial"]
-    cands += [(v["us"], k, "core") for k, v in core.items() if k != "serial"]
-    _, best, best_agent = min(cands)
+    if not args.headline_only:
+        for agent in (["dma"] if args.no_core else ["dma", "core"]):
+            wl.agent = agent
+            for kind in (args.kinds.split(",") if args.kinds else wl.kinds):
+                try:
+                    wl.prepare(grp, kind)
+                except routing.PlanError as exc:
+                    (sched if agent == "dma" else core)[kind] = {"error": str(exc)}
+                    continue
+                variants.append((kind, agent, wl.step(grp, kind)))
+        times = time_interleaved([fn for _, _, fn in variants], args.steps, args.warmup, flush, stream, barrier)
+        grp.comm.check()
+        for (kind, agent, _), ts in zip(variants, times):
+            (sched if agent == "dma" else core)[kind] = {"us": maxrank(statistics.median(ts)) * 1e3}
+
+    # (2) the headline: the public API call with no schedule / agent overrides (kind=None: the selector
+    # picks; comm_agent=None: the machine file's agent), interleaved step by step with the serialized
+    # baseline, cuBLAS on the same GEMM and our tile kernel as a plain GEMM (same clocks for all four).
+    # The op's tile kernel is timed in-op: an event recorded right behind it on the launch stream.
     wl.agent = best_agent
     wl.prepare(grp, best)
-    wl.step(grp, best)()
+    plan = wl.plan_for(grp, best, best_agent)
+    op_fn = wl.step(grp, api_kind, api_agent)
+    op_fn()
+    torch.cuda.synchronize()
     grp.comm.check()
     parity = wl.check() if world == 1 or wl.checks_multi_rank else None
+    kev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + args.warmup)]
+    for e in kev:
+        e.record(stream)  # materialise the CUDA events (their handles go to the library)
+    torch.cuda.synchronize()
+    k_i = [0]
 
-    # the headline: the best (schedule, agent) and the serialized baseline timed interleaved, K steps each
+    def op_timed():
+        plan.set_kernel_event(kev[k_i[0] % len(kev)])
+        k_i[0] += 1
+        op_fn()
+
     serial_fn, serial_desc = wl.serial()
-    t_best, t_serial = time_interleaved([wl.step(grp, best), serial_fn], args.steps, args.warmup, flush, stream,
-                                        barrier)
-    grp.comm.check()
-    value = maxrank(statistics.median(t_best)) * 1e3
-    serial_us = maxrank(statistics.median(t_serial)) * 1e3
-    cublas_us = statistics.median(time_steps(wl.cublas(), args.steps, args.warmup, flush, stream)) * 1e3
     kern_fn, bound, work = wl.kernel(runtime)
-    kern_us = statistics.median(time_steps(kern_fn, args.steps, args.warmup, flush, stream)) * 1e3
-    if bound == "tensor":
-        achieved, peak, unit = work / (kern_us * 1e-6) / 1e12, peaks["bf16_tflops"], "TFLOP/s"
-    else:
-        achieved, peak, unit = work / (kern_us * 1e-6) / 1e9, peaks["hbm_gbs"], "GB/s"
+    fns = [op_timed, serial_fn, wl.cublas(), kern_fn]
+    ev_starts = []
+    t_op, t_serial, t_cublas, t_kern = time_interleaved(fns, args.steps, args.warmup, flush, stream, barrier,
+                                                        starts=ev_starts)
+    plan.set_kernel_event(None)
+    grp.comm.check()
+    # kernel durations: step start event (recorded before the op's launches) -> event behind the kernel
+    kern_in_op = [ev_starts[i][0].elapsed_time(kev[args.warmup + i]) for i in range(args.steps)]
+    value = maxrank(statistics.median(t_op)) * 1e3
+    serial_us = maxrank(statistics.median(t_serial)) * 1e3
+    cublas_us = maxrank(statistics.median(t_cublas)) * 1e3
+    kern_alone_us = maxrank(statistics.median(t_kern)) * 1e3
+    kern_op_us = maxrank(statistics.mean(kern_in_op)) * 1e3
 
-    with ClockSampler(local) as cs:  # clocks while the headline op runs back to back (~1.5 s)
-        fn = wl.step(grp, best)
+    with ClockSampler(local) as cs_loop:  # the headline op back to back (~1.5 s) so the sampler sees load
         t_end = time.time() + 1.5
         while time.time() < t_end:
             for _ in range(10):
-                fn()
+                op_fn()
             torch.cuda.synchronize()
-    clocks = cs.summary()
+    sampler.__exit__(None, None, None)
+    clocks = ClockSampler.merge(sampler, cs_loop)
 
-    e2e_fn, h2d, d2h = wl.e2e(grp, best)
-    e2e_us = maxrank(statistics.median(time_steps(e2e_fn, max(3, args.steps // 3), 3, flush, stream,
+    e2e_fn, h2d, d2h = wl.e2e(grp, api_kind, api_agent)
+    e2e_us = maxrank(statistics.median(time_steps(e2e_fn, max(3, args.steps // 2), 3, flush, stream,
                                                   barrier))) * 1e3
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        per_op, sample = wl.cpu_sample(orc, best)
-        cpu = {"value": round(per_op * 1e6, 1), "unit": "us", "cores": torch.get_num_threads(), "kind": "port",
-               "sample": sample}
+        fn, sample, frac = wl.cpu_op(orc, best)
+        ts = time_cpu(fn, reps=3, warmup=1, budget_s=20.0)
+        cpu = {"value": round(statistics.median(ts) / frac * 1e6, 1), "unit": "us", "cores": blas_threads(),
+               "kind": "port", "sample": f"{sample}; median of {len(ts)} timed calls after 1 warm-up"}
 
-    b200 = b200_machine()
-    sc = ops._scenario(wl.key, *((wl.M, wl.N, wl.K) if hasattr(wl, "M") else (wl.Tkv, wl.Tq, wl.d)), G)
-    selector_kind = select_schedule(sc, b200.machine, b200.t_ref).value
-    value_sequential = (core if best_agent == "core" else sched)[best]["us"]
     low = wl.lowered(grp, best)
     core_copies = sum(op.op == runtime.OP_COPY and op.src_buf == runtime.BUF_WS and op.dst_buf == runtime.BUF_WS
                       for op in low.ops) if low.desc.hints & runtime.FICCO_HINT_CORE_COPIES else 0
@@ -716,50 +830,56 @@ def our_arm(args) -> None:
     # the copy program alone, replayed from its CUDA graph (empty tile list): measured transfer rate
     copy_gbps = None
     if world == 1 and wl.run_plan is not None:
-        copy_low = wl.lowered(grp, best)
-        copy_plan = runtime.Plan(grp.comm, copy_low.desc, list(copy_low.ops), [])
+        copy_plan = runtime.Plan(grp.comm, low.desc, list(low.ops), [])
         try:
             copy_us = statistics.median(time_steps(lambda: wl.run_plan(copy_plan), args.steps, args.warmup, flush,
                                                    stream)) * 1e3
             copy_gbps = round(wl.comm_bytes / (copy_us * 1e-6) / 1e9, 1)
         finally:
             copy_plan.close()
+    cands = [(v["us"], k, "dma") for k, v in sched.items() if "us" in v and k != "serial"]
+    cands += [(v["us"], k, "core") for k, v in core.items() if "us" in v and k != "serial"]
+    fastest = min(cands) if cands else None
+    if bound == "tensor":
+        unit, peak, scale = "TFLOP/s", peaks["bf16_tflops"], 1e12
+    else:
+        unit, peak, scale = "GB/s", peaks["hbm_gbs"], 1e9
+    achieved = work / (kern_op_us * 1e-6) / scale
     if rank == 0:
-        traffic = None
-        try:
-            with open(os.path.join(ROOT, "profiles", f"r01_ncu_traffic_{wl.key}.json")) as f:
-                traffic = json.load(f).get("dram_bytes_per_launch")
-        except Exception:
-            pass
         print(json.dumps({
             "metric": METRIC, "value": round(value, 2), "unit": "us", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(value / 1e3, 5), "higher_is_better": False,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded uniform/normal inputs of the config's shapes)",
-            "config": dict(workload=wl.title, ranks=G, virtual_peers=world == 1, schedule=best,
-                           comm_agent=best_agent,
-                           input="symmetric slot (zero-copy publish)" if wl.inplace else "tensor copied in",
-                           selector_schedule=selector_kind, l2="flushed (256 MiB write) between timed steps",
-                           **wl.config()),
+            "config": config,
             "speedup_vs_serial": round(serial_us / value, 4), "serial_us": round(serial_us, 2),
-            "timing": "schedules: every (kind, agent) variant interleaved step by step in one run; value and "
-                      "serial_us: the best variant and the serialized baseline interleaved in a second run "
-                      "(the box drifts up to ~10 % between runs under the power cap)",
-            "value_sequential": round(value_sequential, 2),
-            "serial_baseline": serial_desc, "cublas_gemm_us": round(cublas_us, 2),
+            "serial_baseline": serial_desc,
+            "timing": "value: median of the public API op (no schedule/agent override), interleaved step by step "
+                      "with the serialized baseline, cuBLAS and the plain tile GEMM (L2 flushed before each call); "
+                      "schedules: every (kind, agent) variant interleaved in an earlier run",
+            "cublas_gemm_us": round(cublas_us, 2),
             "ideal_overlap_us": round(t_star, 2), "pct_ideal_overlap": round(t_star / value, 4),
             "ideal_overlap_fill_us": round(t_fill, 2), "pct_ideal_overlap_fill": round(t_fill / value, 4),
             "copy_program_GBps": copy_gbps,
+            "fastest_variant": ({"schedule": fastest[1], "comm_agent": fastest[2], "us": round(fastest[0], 2)}
+                                if fastest else None),
             "schedules": {k: ({"us": round(v["us"], 2)} if "us" in v else v) for k, v in sched.items()},
-            "schedules_comm_agent_core": {k: {"us": round(v["us"], 2)} for k, v in core.items()},
+            "schedules_comm_agent_core": {k: ({"us": round(v["us"], 2)} if "us" in v else v)
+                                          for k, v in core.items()},
             "parity_spot_check": parity,
             "roofline": {"bound": bound, "achieved": round(achieved, 1), "peak": peak, "unit": unit,
-                         "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "frac": round(achieved / peak, 4), "traffic": traffic_for(wl.key, G, best, best_agent),
+                         "kernel": f"ficco::tile_gemm_kernel inside the {best}/{best_agent} op: mean in-op duration "
+                                   f"over the timed steps (CUDA events on the launch stream: step start -> event "
+                                   f"recorded behind the kernel)",
+                         "kernel_us": round(kern_op_us, 2),
+                         "work_per_launch": work, "work_unit": "flop" if bound == "tensor" else "byte",
+                         "op_frac": round(work / (value * 1e-6) / scale / peak, 4),
+                         "kernel_alone_us": round(kern_alone_us, 2),
+                         "kernel_alone_frac": round(work / (kern_alone_us * 1e-6) / scale / peak, 4),
                          "frac_sustained": (round(achieved / peaks["bf16_tflops_sustained"], 4)
                                             if bound == "tensor" and "bf16_tflops_sustained" in peaks else None),
-                         "kernel": "ficco::tile_gemm_kernel (flag-free plain GEMM of the op's shape, same kernel)",
-                         "kernel_us": round(kern_us, 2),
-                         "peak_source": f"MEASURED_PEAKS.json ({peaks_src}; burst figure, kernel timed alone)"},
+                         "peak_source": f"MEASURED_PEAKS.json ({peaks_src}; burst figure)"},
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_us, 2), "unit": "us", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": args.steps * (1 + core_copies),
@@ -770,39 +890,72 @@ def our_arm(args) -> None:
         torch.distributed.destroy_process_group()
 
 
+def reference_simulator_us(workload: str, G: int, budget_s: float = 3.0):
+    """The reference's own CPU path for this config, from the unmodified install in baseline/_ref:
+    build_plan + simulate (every executable kind) + select_schedule (planner.py:409, engine.py:117,
+    heuristic.py:25) on the B200 machine file, 1 host thread. Returns (µs per pass, note) or (None, why)."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "overlap_sim")):
+        return None, "baseline/_ref not installed"
+    sys.path.insert(0, ref)
+    try:
+        from overlap_sim import core, engine, heuristic, lossmodel, machines, planner
+        with open(os.path.join(ROOT, "paper_2512_10236_b200", "data", "machine_b200.json")) as f:
+            spec = machines.machine_spec_from_dict(json.load(f))
+        model = lossmodel.default_calibration()
+        m, n, k = WORKLOADS[workload].op_shape(G)
+        sc = core.Scenario(name=workload, parallelism=core.Parallelism.SP_TP, model="bench",
+                           gemm=core.GemmShape(m, n, k, 2), collective=core.Collective.ALL_GATHER, n_gpus=G)
+        topo = spec.topo if spec.topo.n_gpus == G else type(spec.topo)(
+            kind=spec.topo.kind, n_gpus=G, link_bw=spec.topo.link_bw, nic_bw=spec.topo.nic_bw,
+            latency=spec.topo.latency)
+
+        def one_pass():
+            heuristic.select_schedule(sc, spec.machine, spec.t_ref)
+            for kind in planner.supported_kinds(sc):
+                engine.simulate(planner.build_plan(sc, kind, topo), spec.machine, topo, model)
+
+        ts = time_cpu(one_pass, reps=1000, warmup=1, budget_s=budget_s)
+        return statistics.median(ts) * 1e6, (f"overlap_sim {G}-rank {workload} scenario: select_schedule + "
+                                             f"build_plan/simulate of every supported kind, {len(ts)} passes")
+    except Exception as exc:  # pragma: no cover - reported, never fatal
+        return None, f"reference simulator failed: {exc!r}"
+    finally:
+        sys.path.remove(ref)
+
+
 def reference_arm(args) -> None:
-    """CPU restatement of the reference's path (the oracle port) on the host cores, C2 config."""
+    """The reference's CPU implementation of the path on the host cores, on our arm's config.
+
+    The reference (overlap_sim) is a simulator: it plans and prices schedules but moves no tensor
+    data, so the executable CPU path is the oracle port (oracle/ficco_oracle.py, which
+    restates the reference's routing and is pinned to its plans): each step runs rank 0's WHOLE op of
+    the config's schedule (no sampling or scaling; numpy fp32 BLAS on all host threads). The
+    reference's own planning/pricing path (baseline/_ref) is timed beside it.
+    """
     world, rank, _ = dist_env()
     if rank != 0:
         return
     import torch
     from oracle import ficco_oracle as orc
-    G, M, N, K = G_VIRTUAL, 8192, 3584, 4096
-    R = M // G
-    shards = [orc.seeded_inputs(0, p, (R, K)) for p in range(G)]
-    w = orc.seeded_inputs(0, 99, (N, K), "normal")
-    kind = "uniform_fused_1d"
-    frags = orc.gemm_fragments(kind, M, K, G, 0)
-    rows_first = sum(c for rows, _ in frags[:1] for _, c in rows)
-    scale = M / rows_first
-    for _ in range(max(1, min(args.warmup, 2))):
-        orc.execute_ag_rank(kind, shards, w, 0, steps=1)
-    times = []
-    for _ in range(max(1, min(args.steps, 20))):
-        t0 = time.perf_counter()
-        orc.execute_ag_rank(kind, shards, w, 0, steps=1)
-        times.append((time.perf_counter() - t0) * scale)
-    us = statistics.median(times) * 1e6
-    sample = (f"oracle port (numpy fp32 BLAS) of rank 0's {kind} AG->GEMM: first step ({rows_first}/{M} rows) "
-              f"per timed step, scaled x{scale:g}")
+    config = workload_config(args, world)
+    G = config["ranks"]
+    wl = WORKLOADS[args.workload](torch, torch.device("cpu"), G, 0, 1, None)
+    fn, sample, frac = wl.cpu_op(orc, config["schedule"])
+    steps = max(1, args.steps)
+    ts = time_cpu(fn, reps=steps, warmup=max(1, args.warmup), budget_s=240.0)
+    us = statistics.median(ts) / frac * 1e6
+    sim_us, sim_note = reference_simulator_us(args.workload, G)
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(us, 1), "unit": "us", "n_gpus": world,
-        "steps": len(times), "warmup": args.warmup, "ms_per_step": round(us / 1e3, 3), "higher_is_better": False,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": AGWorkload.title, "M": M, "N": N, "K": K, "ranks": G, "schedule": kind},
-        "cpu_baseline": {"value": round(us, 1), "unit": "us", "cores": torch.get_num_threads(), "kind": "port",
+        "steps": len(ts), "warmup": args.warmup, "ms_per_step": round(us / 1e3, 3), "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (our arm's shapes and seeds, drawn by the host generator)",
+        "config": config,
+        "cpu_baseline": {"value": round(us, 1), "unit": "us", "cores": blas_threads(), "kind": "port",
                          "sample": sample},
         "e2e": {"value": round(us, 1), "unit": "us", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_simulator": {"us_per_pass": None if sim_us is None else round(sim_us, 1), "cores": 1,
+                                "what": sim_note},
     }))
 
 
@@ -813,7 +966,10 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ficco", choices=["ficco", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
-    ap.add_argument("--kinds", default="", help="comma-separated subset of schedules")
+    ap.add_argument("--kinds", default="", help="comma-separated subset of schedules for the variants table")
+    ap.add_argument("--kind", default="", help="override the headline schedule (default: the selector's choice)")
+    ap.add_argument("--agent", default="", help="override the headline comm agent (default: the machine file's)")
+    ap.add_argument("--headline-only", action="store_true", help="skip the all-variants table")
     ap.add_argument("--virtual-ranks", type=int, default=G_VIRTUAL,
                     help="N=1 only: the job size G this GPU plays rank 0 of (C3 is quoted at G = 2, 4 and 8)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")

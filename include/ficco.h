@@ -240,6 +240,10 @@ int ficco_cp_qk(ficco_plan_t* plan, const void* q, const void* k_shard, void* sc
  * 2t+1: tile stored} at offset grid. NULL disables. Rebuilds the plan's graphs. */
 int ficco_plan_set_trace(ficco_plan_t* plan, void* buf);
 int ficco_plan_info(ficco_plan_t* plan, int* n_tiles, int* grid, int* n_streams);
+/* Optional: record `event` (a cudaEvent_t) on the caller's stream right after the tile kernel in
+ * every later ficco_plan_run, so (event before the call -> event) times the in-op kernel alone
+ * (bench.py's roofline). NULL detaches. Not available with FICCO_KERNEL_IN_GRAPH=1. */
+int ficco_plan_set_kernel_event(ficco_plan_t* plan, void* event);
 
 /* stand-alone primitives (calibration, benchmarks) */
 int ficco_gemm_bf16(const void* a, const void* b, void* c, int64_t m, int64_t n, int64_t k, float alpha,

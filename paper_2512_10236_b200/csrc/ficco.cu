@@ -2,10 +2,13 @@
 //
 // Host side of the executor declared in include/ficco.h. Responsibilities:
 //   * symmetric workspace + CUDA IPC plumbing (ranks exchange handles in Python),
-//   * the copy program: copy-engine copies batched per round with
-//     cudaMemcpyBatchAsync (1D) / cudaMemcpy2DAsync (2D slabs) on a dedicated
-//     copy stream, stream memory operations (cuStreamWriteValue32 /
-//     cuStreamWaitValue32) for readiness flags — no SMs, no host round trips,
+//   * the copy program: one copy-engine copy per chunk (cudaMemcpyAsync 1D /
+//     cudaMemcpy2DAsync for 2D slabs) on per-peer copy streams, readiness flags
+//     written by tiny copy-engine copies of a constant word right behind the data,
+//     waits as stream memory operations (cuStreamWaitValue32/64) — no SMs, no host
+//     round trips; the whole program is captured once per workspace parity into a
+//     CUDA graph and replayed. (ficco_copy_batch exposes cudaMemcpyBatchAsync for
+//     calibration probes; the plans do not use it.)
 //   * the tile program: TMA descriptors + one persistent tcgen05 kernel launch.
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -164,8 +167,11 @@ int kernel_for(int tn, int cg, int eb, const void** fn, int* smem, int* b_rows) 
 }
 
 int configure_kernels(int dev) {
-  static int configured = -1;
-  if (configured == dev) return 0;
+  // per device: cudaFuncSetAttribute is per (function, device) and processes may drive several GPUs
+  static std::mutex mu;
+  static uint64_t configured = 0;  // bit d: device d done
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev >= 0 && dev < 64 && (configured >> dev) & 1u) return 0;
 #define FICCO_CFG(T, G, E)                                                                              \
   CK(cudaFuncSetAttribute(ficco::tile_gemm_kernel<T, G, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                           ficco::TileCfg<T, G, E>::SMEM_BYTES));                                        \
@@ -177,7 +183,7 @@ int configure_kernels(int dev) {
   }
   FICCO_FOR_EACH_CFG(FICCO_CFG)
 #undef FICCO_CFG
-  configured = dev;
+  if (dev >= 0 && dev < 64) configured |= uint64_t(1) << dev;
   return 0;
 }
 
@@ -206,6 +212,10 @@ struct ficco_comm {
   cudaEvent_t ev_fork = nullptr;
   cudaEvent_t ev_join[FICCO_MAX_STREAMS] = {};
   cudaEvent_t ev_pool[FICCO_MAX_EVENTS] = {};
+  // host-mapped copy of the abort word: the tile kernel raises it with the device word when a flag
+  // wait times out, so every later run can refuse a poisoned communicator without a device sync
+  uint32_t* host_abort = nullptr;
+  uint32_t* dev_host_abort = nullptr;
   Driver* drv = nullptr;
   uint32_t* flags(int r) { return reinterpret_cast<uint32_t*>(ws[r]); }
   uint32_t* block(int r, uint32_t parity) { return flags(r) + parity * FICCO_FLAG_BLOCK; }
@@ -231,6 +241,7 @@ struct ficco_plan {
   cudaGraphNode_t captured_kernel = nullptr;
   std::vector<std::pair<cudaGraphNode_t, int>> captured_copies;  // (node, op index) touching call arguments
   unsigned long long* trace = nullptr;  // optional device timeline buffer
+  cudaEvent_t kernel_event = nullptr;   // optional: recorded on the launch stream right after the tile kernel
   bool concurrent = true;               // false: copies complete before the kernel starts (profilers)
   // Default: the tile kernel is launched directly on the caller's stream, THEN the copy-only
   // graph on a side stream (kernel first: it is queued before any of the graph's stream-wait
@@ -523,6 +534,7 @@ int make_params(ficco_plan* p, uint32_t parity, const void* a, const void* b, vo
   prm->flags = cm->block(cm->rank, parity);
   prm->counters = cm->block(cm->rank, parity) + FICCO_FLAG_COUNTERS;
   prm->abort_word = cm->flags(cm->rank) + FICCO_FLAG_ABORT;
+  prm->abort_host = cm->dev_host_abort;
   prm->epoch = 1u;  // one-shot flags: wait for != 0
   {
     // a flag wait longer than this is a protocol failure (FICCO_ETIMEOUT -> DeadlockError); ops of
@@ -645,6 +657,15 @@ int repoint_graph(ficco_plan* p, uint32_t parity, const void* a, const void* b, 
   return 0;
 }
 
+// A run of this communicator timed out on a readiness flag (the kernel drained without its
+// inputs): its flag words and workspaces are in an unknown state, so it refuses further runs.
+bool poisoned(const ficco_comm* c) { return c->host_abort && *reinterpret_cast<volatile uint32_t*>(c->host_abort); }
+int poisoned_error() {
+  return fail(FICCO_ETIMEOUT,
+              "communicator poisoned: an earlier run timed out waiting for a readiness flag; destroy the "
+              "communicator (FiccoGroup.close) and create a new one");
+}
+
 }  // namespace
 
 extern "C" {
@@ -726,7 +747,12 @@ int ficco_comm_create(int rank, int world, void* const* ws, size_t ws_bytes, int
   c->ws_bytes = ws_bytes;
   c->drv = drv;
   for (int i = 0; i < world; ++i) c->ws.push_back(reinterpret_cast<uint8_t*>(ws[i]));
-  cudaError_t e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
+  cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&c->host_abort), 4, cudaHostAllocMapped);
+  if (e == cudaSuccess) {
+    *c->host_abort = 0;
+    e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->dev_host_abort), c->host_abort, 0);
+  }
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
   for (int i = 0; i < FICCO_MAX_STREAMS && e == cudaSuccess; ++i) {
     e = cudaStreamCreateWithFlags(&c->copy[i], cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_join[i], cudaEventDisableTiming);
@@ -753,6 +779,7 @@ int ficco_comm_destroy(ficco_comm_t* c) {
   for (int i = 0; i < FICCO_MAX_EVENTS; ++i)
     if (c->ev_pool[i]) cudaEventDestroy(c->ev_pool[i]);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->host_abort) cudaFreeHost(c->host_abort);
   delete c;
   return 0;
 }
@@ -769,7 +796,8 @@ int ficco_comm_check(ficco_comm_t* c, void* stream) {
   for (int i = 0; i < FICCO_MAX_STREAMS; ++i) CK(cudaStreamSynchronize(c->copy[i]));
   uint32_t abort_word = 0;
   CK(cudaMemcpy(&abort_word, c->flags(c->rank) + FICCO_FLAG_ABORT, 4, cudaMemcpyDeviceToHost));
-  if (abort_word) return fail(FICCO_ETIMEOUT, "tile kernel timed out waiting for a readiness flag");
+  if (abort_word || *reinterpret_cast<volatile uint32_t*>(c->host_abort))
+    return fail(FICCO_ETIMEOUT, "tile kernel timed out waiting for a readiness flag");
   return 0;
 }
 
@@ -835,6 +863,8 @@ int ficco_plan_create(ficco_comm_t* c, const ficco_plan_desc* d, ficco_plan_t** 
     if (op.op == FICCO_OP_COPY && (is_user(op.src_buf) || is_user(op.dst_buf))) user = true;
     if (op.stream + 1 > n_streams) n_streams = op.stream + 1;
   }
+  if (has_remote && (d->recv.rows <= 0 || d->recv.ld <= 0))
+    return fail(FICCO_EINVAL, "STORE_REMOTE tiles need the receive-slot geometry (recv)");
   auto* p = new ficco_plan();
   p->comm = c;
   p->desc = *d;
@@ -847,8 +877,6 @@ int ficco_plan_create(ficco_comm_t* c, const ficco_plan_desc* d, ficco_plan_t** 
   p->epi_bufs = epi_bufs_for(d->k);
   p->has_remote = has_remote;
   p->role = plan_role(*d);
-  if (has_remote && (d->recv.rows <= 0 || d->recv.ld <= 0))
-    return fail(FICCO_EINVAL, "STORE_REMOTE tiles need the receive-slot geometry (recv)");
   {
     const char* env = getenv("FICCO_KERNEL_IN_GRAPH");
     p->kernel_in_graph = env && env[0] == '1';
@@ -892,6 +920,13 @@ int ficco_plan_set_trace(ficco_plan_t* p, void* buf) {
   return 0;
 }
 
+int ficco_plan_set_kernel_event(ficco_plan_t* p, void* event) {
+  if (!p) return fail(FICCO_EINVAL, "null plan");
+  if (p->kernel_in_graph && event) return fail(FICCO_EINVAL, "kernel events need the direct kernel launch mode");
+  p->kernel_event = reinterpret_cast<cudaEvent_t>(event);
+  return 0;
+}
+
 int ficco_plan_info(ficco_plan_t* p, int* n_tiles, int* grid, int* n_streams) {
   if (!p) return fail(FICCO_EINVAL, "null plan");
   int g = p->desc.grid > 0 ? p->desc.grid : p->comm->sms;
@@ -905,6 +940,7 @@ int ficco_plan_info(ficco_plan_t* p, int* n_tiles, int* grid, int* n_streams) {
 int ficco_plan_run_parts(ficco_plan_t* p, const void* a, const void* b, void* c, void* stream, int run_copies,
                          int run_tiles) {
   if (!p) return fail(FICCO_EINVAL, "null plan");
+  if (poisoned(p->comm)) return poisoned_error();
   p->concurrent = run_tiles != 2;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const uint32_t parity = p->comm->runs & 1u;
@@ -914,6 +950,7 @@ int ficco_plan_run_parts(ficco_plan_t* p, const void* a, const void* b, void* c,
 
 int ficco_plan_run(ficco_plan_t* p, const void* a, const void* b, void* c, void* stream) {
   if (!p) return fail(FICCO_EINVAL, "null plan");
+  if (poisoned(p->comm)) return poisoned_error();
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const uint32_t parity = p->comm->runs & 1u;
   GraphInst& gi = p->graph[parity];
@@ -934,6 +971,7 @@ int ficco_plan_run(ficco_plan_t* p, const void* a, const void* b, void* c, void*
   cudaStream_t gs = cm->copy[FICCO_MAX_STREAMS - 1];  // graph launch stream (idle between runs)
   CK(cudaEventRecord(cm->ev_fork, s));
   if ((r = launch_tiles(p, parity, a, b, c, s))) return r;
+  if (p->kernel_event) CK(cudaEventRecord(p->kernel_event, s));  // completes with the tile kernel
   CK(cudaStreamWaitEvent(gs, cm->ev_fork, 0));
   CK(cudaGraphLaunch(gi.exec, gs));
   CK(cudaEventRecord(cm->ev_join[0], gs));
@@ -997,11 +1035,13 @@ int ficco_gemm_bf16_cfg(const void* a, const void* b, void* c, int64_t m, int64_
   if (cta_group == 0) cta_group = 2;
   if (cta_group != 1 && cta_group != 2) return fail(FICCO_EINVAL, "cta_group must be 1 or 2");
   static std::mutex mu;
-  static std::map<std::tuple<int64_t, int64_t, int, int, int, int>, std::pair<ficco_comm*, ficco_plan*>> cache;
+  // keyed on the full shape: the tile width, raster grouping and L2 hints all depend on (m, n, k)
+  static std::map<std::tuple<int64_t, int64_t, int64_t, int, int, int, int>, std::pair<ficco_comm*, ficco_plan*>>
+      cache;
   std::lock_guard<std::mutex> lock(mu);
   int dev;
   CK(cudaGetDevice(&dev));
-  auto key = std::make_tuple(m, n, grid, dev, tile_n, cta_group);
+  auto key = std::make_tuple(m, n, k, grid, dev, tile_n, cta_group);
   auto it = cache.find(key);
   if (it == cache.end()) {
     static std::map<int, void*> ws_by_dev;

@@ -123,6 +123,7 @@ struct alignas(64) TileParams {
   uint32_t* flags;         // local flag block of this run's parity
   uint32_t* counters;      // local tile counters
   uint32_t* abort_word;
+  uint32_t* abort_host;    // host-mapped mirror of abort_word (ficco_plan_run refuses a poisoned communicator)
   uint32_t epoch;          // value a flag must reach (1: one-shot flags)
   unsigned long long timeout_ns;  // flag waits abort after this long (FICCO_FLAG_TIMEOUT_S, default 30 s)
   float alpha;
@@ -143,7 +144,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // `timeout_ns` of waiting (%globaltimer; TileParams.timeout_ns) raise the abort word
 // and give up so the kernel drains instead of hanging the device.
 __device__ __forceinline__ void wait_flag(const uint32_t* f, uint32_t epoch, uint32_t* abort_word,
-                                          unsigned long long timeout_ns) {
+                                          unsigned long long timeout_ns, uint32_t* abort_host) {
   uint32_t spins = 0;
   unsigned long long t0 = 0;
   while (static_cast<int32_t>(ld_acquire_sys(f) - epoch) < 0) {
@@ -153,6 +154,10 @@ __device__ __forceinline__ void wait_flag(const uint32_t* f, uint32_t epoch, uin
         t0 = now;
       } else if (now - t0 > timeout_ns) {
         atomicExch(abort_word, 1u);
+        if (abort_host) {
+          *reinterpret_cast<volatile uint32_t*>(abort_host) = 1u;
+          __threadfence_system();
+        }
         break;
       }
       if (*reinterpret_cast<volatile uint32_t*>(abort_word)) break;
@@ -169,10 +174,11 @@ __device__ __forceinline__ void wait_flag(const uint32_t* f, uint32_t epoch, uin
 constexpr int SEEN_WORDS = FICCO_FLAG_BLOCK / 32;
 
 __device__ __forceinline__ void wait_flag_cached(uint32_t* seen, const uint32_t* flags, int idx, uint32_t epoch,
-                                                 uint32_t* abort_word, unsigned long long timeout_ns) {
+                                                 uint32_t* abort_word, unsigned long long timeout_ns,
+                                                 uint32_t* abort_host) {
   const uint32_t bit = 1u << (idx & 31);
   if (seen[idx >> 5] & bit) return;
-  wait_flag(flags + idx, epoch, abort_word, timeout_ns);
+  wait_flag(flags + idx, epoch, abort_word, timeout_ns, abort_host);
   seen[idx >> 5] |= bit;
 }
 
@@ -202,7 +208,8 @@ __device__ __forceinline__ void producer_loop(const TileParams& p, uint8_t* sA, 
           const uint32_t window = uint32_t(((uint64_t(w1) << 32) | w0) >> (base & 31));
           if ((window & td.fmask) != td.fmask)
             for (uint32_t m = td.fmask; m; m &= m - 1)
-              wait_flag_cached(seen, p.flags, base + (__ffs(m) - 1), p.epoch, p.abort_word, p.timeout_ns);
+              wait_flag_cached(seen, p.flags, base + (__ffs(m) - 1), p.epoch, p.abort_word, p.timeout_ns,
+                               p.abort_host);
         }
       }
       if (kb == 0 && p.trace) p.trace[gridDim.x + 2 * t] = globaltimer();
@@ -228,7 +235,7 @@ __device__ __forceinline__ void producer_loop(const TileParams& p, uint8_t* sA, 
       // so the reduction rides the TMA/tensor pipeline instead of the epilogue's loads.
       for (int j = 0; j < p.n_recv; ++j)
         wait_flag_cached(seen, p.flags, p.rs_flag0 + td.chunk * p.n_recv + j, p.rs_target, p.abort_word,
-                         p.timeout_ns);
+                         p.timeout_ns, p.abort_host);
       for (int j = 0; j < p.n_recv; ++j) {
         for (int kb = 0; kb < Cfg::RKB; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1u);
@@ -398,7 +405,8 @@ __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfu
       // peers' partial chunks must have landed in our receive slots
       if (threadIdx.x == 64) {
         for (int j = 0; j < p.n_recv; ++j)
-          wait_flag(p.flags + p.rs_flag0 + td.chunk * p.n_recv + j, p.rs_target, p.abort_word, p.timeout_ns);
+          wait_flag(p.flags + p.rs_flag0 + td.chunk * p.n_recv + j, p.rs_target, p.abort_word, p.timeout_ns,
+                    p.abort_host);
       }
       named_bar_sync(1, EPI_THREADS);
     }
@@ -411,7 +419,8 @@ __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfu
     const bool reduce_row = epi_reduce && row_ok;
     if (remote && !go_seen) {
       // the owners' receive slots are free once the DONE barrier of this run passed
-      if (p.go_flag > 0 && lane == 0) wait_flag(p.flags + p.go_flag, p.epoch, p.abort_word, p.timeout_ns);
+      if (p.go_flag > 0 && lane == 0)
+        wait_flag(p.flags + p.go_flag, p.epoch, p.abort_word, p.timeout_ns, p.abort_host);
       __syncwarp();
       go_seen = true;
     }

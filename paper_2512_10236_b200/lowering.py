@@ -492,11 +492,80 @@ def lower_ag(plan: ExecutionPlan, rank: int, gathered: str = "A", alpha: float =
     return low
 
 
-def rs_plan(scenario: Scenario, kind: ScheduleKind) -> ExecutionPlan:
-    """The AG plan whose routing the RS schedule is the adjoint of (same chunks, reversed flow)."""
-    if kind not in (ScheduleKind.UNIFORM_FUSED_1D, ScheduleKind.HETERO_FUSED_1D, ScheduleKind.HETERO_UNFUSED_1D):
-        raise PlanError(f"GEMM->reduce-scatter supports the 1D fine-grain kinds, not {kind.value}")
-    return build_plan(scenario, kind)
+RS_KINDS = (ScheduleKind.SERIAL, ScheduleKind.SHARD_OVERLAP_P2P, ScheduleKind.UNIFORM_FUSED_1D,
+            ScheduleKind.HETERO_FUSED_1D, ScheduleKind.HETERO_UNFUSED_1D, ScheduleKind.UNIFORM_FUSED_2D)
+
+
+@dataclass(frozen=True)
+class RSPiece:
+    """One pushed block of a GEMM -> RS schedule: rows [row0, +nrows) x cols [col0, +ncols) of the
+    partial P_g, owned by rank ``owner``; ``idx`` selects its landing words F_RS + idx*(G-1) + slot."""
+
+    owner: int
+    row0: int
+    nrows: int
+    col0: int
+    ncols: int
+    idx: int
+
+
+def rs_pieces(scenario: Scenario, kind: ScheduleKind, rank: int):
+    """The adjoint routing of ``kind`` for rank ``rank``: (emission order, push units).
+
+    order: [(remote?, piece)] in tile order; units: [[pieces pushed together]] (dma agent).
+    Time-reversal of the AG schedules (planner.py:170-390): where the AG schedule receives chunk
+    (p, c) before the GEMM that reads it, the RS schedule computes the partial of chunk (q, c)
+    before pushing it to its owner q, and the owner's own-rows tiles reduce last:
+
+    serial            all remote shards, ONE push unit after the whole GEMM (planner.py:170-191)
+    shard_overlap     shard ring reversed: step i computes owner (g+i)'s shard and pushes it
+                      (whole shard, one unit per step), own shard last (planner.py:194-240)
+    uniform_fused_1d  round c: chunk c of every remote owner (one unit), then the own chunk c
+    hetero_fused_1d   all remote rounds (one unit per round), own shard last (planner.py:291-331)
+    hetero_unfused_1d as fused, one unit per chunk (planner.py:332-347)
+    uniform_fused_2d  the N-block adjoint of the K-block schedule (planner.py:351-390): round c
+                      computes output column block c of every remote owner's rows (an R x N/G
+                      slab, one unit), then the own slab c, which reduces as soon as round c landed
+    """
+    if kind not in RS_KINDS:
+        raise PlanError(f"GEMM->reduce-scatter has no executable adjoint of {kind.value}")
+    g, G = rank, scenario.n_gpus
+    M, N = scenario.gemm.m, scenario.gemm.n
+    if kind is ScheduleKind.UNIFORM_FUSED_2D:
+        if M % G or N % G:
+            raise PlanError(f"uniform_fused_2d (N-block) GEMM->RS needs M={M} and N={N} divisible by G={G}")
+        if (N // G) % 32:
+            raise PlanError(f"uniform_fused_2d (N-block) GEMM->RS needs N/G={N // G} to be a multiple of 32")
+    elif kind in (ScheduleKind.SERIAL, ScheduleKind.SHARD_OVERLAP_P2P):
+        build_plan(scenario, kind)  # M % G, exactly as the AG schedule
+    else:
+        build_plan(scenario, kind)  # M % G^2
+    R = M // G
+    remote = [(g + j) % G for j in range(1, G)]
+    order: list[tuple[bool, RSPiece]] = []
+    units: list[list[RSPiece]] = []
+    if kind in (ScheduleKind.SERIAL, ScheduleKind.SHARD_OVERLAP_P2P):
+        pcs = [RSPiece(q, q * R, R, 0, N, 0) for q in remote]
+        order = [(True, pc) for pc in pcs] + [(False, RSPiece(g, g * R, R, 0, N, 0))]
+        units = [pcs] if kind is ScheduleKind.SERIAL else [[pc] for pc in pcs]
+        return order, units
+    if kind is ScheduleKind.UNIFORM_FUSED_2D:
+        b = N // G
+        for c in range(G):
+            pcs = [RSPiece(q, q * R, R, c * b, b, c) for q in remote]
+            units.append(pcs)
+            order += [(True, pc) for pc in pcs] + [(False, RSPiece(g, g * R, R, c * b, b, c))]
+        return order, units
+    r = M // (G * G)
+    for c in range(G):
+        pcs = [RSPiece(q, q * R + c * r, r, 0, N, c) for q in remote]
+        units += [[pc] for pc in pcs] if kind is ScheduleKind.HETERO_UNFUSED_1D else [pcs]
+        order += [(True, pc) for pc in pcs]
+        if kind is ScheduleKind.UNIFORM_FUSED_1D:
+            order.append((False, RSPiece(g, g * R + c * r, r, 0, N, c)))
+    if kind is not ScheduleKind.UNIFORM_FUSED_1D:
+        order += [(False, RSPiece(g, g * R + c * r, r, 0, N, c)) for c in range(G)]
+    return order, units
 
 
 def lower_rs(scenario: Scenario, kind: ScheduleKind, rank: int, grid: int = 0, virtual: bool = False,
@@ -504,31 +573,26 @@ def lower_rs(scenario: Scenario, kind: ScheduleKind, rank: int, grid: int = 0, v
     """GEMM -> reduce-scatter (not in the reference, parity unpinned).
 
     Rank g holds A_g [M, Kg] and W_g [N, Kg]; P_g = A_g @ W_g^T [M, N]; rank q
-    ends with C_q = sum_g P_g[q*R:(q+1)*R] [R, N]. Fine chunk (q, c) = rows
-    q*R + c*r. Partial tiles of remote chunks are stored to the local partial
-    buffer and counted; the copy stream pushes each finished chunk into the
-    owner's receive slot (copy engine) and notifies it; the owner's tiles of
-    its own chunk reduce ``acc + sum_j recv_j`` in the epilogue
-    (rank-ascending over the G-1 peers, fp32, one bf16 rounding).
-
-    uniform_fused_1d: round c = remote chunks c (rotated owners) then own chunk c.
-    hetero_fused_1d:  all remote chunks round by round, own shard last; push per round.
-    hetero_unfused_1d: as fused but each chunk is pushed as soon as it is done.
+    ends with C_q = sum_g P_g[q*R:(q+1)*R] [R, N]. The schedule's pieces (``rs_pieces``):
+    remote pieces' tiles store their partial and are counted; the copy stream pushes each
+    finished unit into the owners' receive slots (copy engine) and notifies them; the
+    owner's own-rows tiles (REDUCE) fold the G-1 received partials into the fp32
+    accumulator (rank-ascending, one bf16 rounding) once their landing words are set.
 
     comm_agent='core' (the SM-driven variant, reference CommAgent.CORE): no
-    partial buffer and no push copies. A remote chunk's tile epilogue TMA-stores
+    partial buffer and no push copies. A remote piece's tile epilogue TMA-stores
     the partial straight into the owner's receive slot (peer memory over
-    NVLink) and bumps the owner's per-(chunk, sender) word; the owner reduces
+    NVLink) and bumps the owner's per-(piece, sender) word; the owner reduces
     once that word reaches the sender's tile count (``rs_target``). Stores wait
     for the DONE barrier (flag F_GO), as the copy-engine pushes do.
     """
-    plan = rs_plan(scenario, kind)  # validates divisibility exactly like the AG schedule
+    order, units = rs_pieces(scenario, kind, rank)
     g, G = rank, scenario.n_gpus
     M, N, K = scenario.gemm.m, scenario.gemm.n, scenario.gemm.k
     _check_shape(M, N, K)
     if G - 1 > MAX_RECV or G > MAX_WORLD:
         raise PlanError(f"at most {MAX_RECV + 1} ranks")
-    R, r = M // G, M // (G * G)
+    R = M // G
     row_bytes = N * ELT
     low = Lowered()
     direct = getattr(comm_agent, "value", comm_agent) == "core"
@@ -538,46 +602,34 @@ def lower_rs(scenario: Scenario, kind: ScheduleKind, rank: int, grid: int = 0, v
     low.recv_par = 0  # single buffer: a peer pushes run e only after our DONE(e), i.e. after run e-1 finished
     low.ws_bytes = low.recv_off + (G - 1) * low.recv_slot
     ops, tiles = low.ops, low.tiles
-    unfused = kind is ScheduleKind.HETERO_UNFUSED_1D
     _agent_hint(comm_agent)  # validates the name
 
     def slot_of(src: int, owner: int) -> int:
         return src if src < owner else src - 1
 
-    # units of work that are pushed together: list of (counter id, [(owner q, round c)])
-    units: list[tuple[int, list[tuple[int, int]]]] = []
-    order: list[tuple[str, int, int]] = []  # ("remote"|"own", q, c) tile emission order
-    for c in range(G):
-        remote = [((g + j) % G, c) for j in range(1, G)]
-        if unfused:
-            for q, cc in remote:
-                units.append((len(units), [(q, cc)]))
-        else:
-            units.append((len(units), remote))
-        order += [("remote", q, cc) for q, cc in remote]
-        if kind is ScheduleKind.UNIFORM_FUSED_1D:
-            order.append(("own", g, c))
-    if kind is not ScheduleKind.UNIFORM_FUSED_1D:
-        order += [("own", g, c) for c in range(G)]
-    unit_of = {qc: uid for uid, qcs in units for qc in qcs}
+    def cdiv(a: int, b: int) -> int:
+        return -(-a // b)
 
-    tn = choose_tile_n(lambda w: -(-(G * G * (-(-r // TILE_M))) // cta_group) * (-(-N // w)), B200_SMS // cta_group)
-    tiles_per_chunk = ((r + TILE_M - 1) // TILE_M) * ((N + tn - 1) // tn)
-    def emit(what, q, c, m0, n0):
-        rows, cols = min(TILE_M, q * R + c * r + r - m0), min(tn, N - n0)
-        if what == "remote" and direct:
-            tiles.append(_tile(m0, n0, m0 - q * R, n0, rows, cols, mode=EPI_STORE_REMOTE, chunk=q,
-                               recv_row=F_RS + c * (G - 1) + slot_of(g, q)))
-        elif what == "remote":
-            tiles.append(_tile(m0, n0, m0, n0, rows, cols, mode=EPI_STORE_SIGNAL, chunk=unit_of[(q, c)]))
-        else:
-            local = m0 - g * R
-            tiles.append(_tile(m0, n0, local, n0, rows, cols, mode=EPI_REDUCE, chunk=c, recv_row=local))
+    shape0 = order[0][1]
+    tn = choose_tile_n(lambda w: cdiv(len(order) * cdiv(shape0.nrows, TILE_M), cta_group) * cdiv(shape0.ncols, w),
+                       B200_SMS // cta_group)
+    tiles_per_piece = cdiv(shape0.nrows, TILE_M) * cdiv(shape0.ncols, tn)
+    unit_of = {pc: uid for uid, pcs in enumerate(units) for pc in pcs}
 
-    for what, q, c in order:  # chunk-major (row-major inside a chunk: measured best for W reuse)
-        for m0 in range(q * R + c * r, q * R + c * r + r, TILE_M):
-            for n0 in range(0, N, tn):
-                emit(what, q, c, m0, n0)
+    for is_remote, pc in order:  # piece-major (row-major inside a piece: measured best for W reuse)
+        for m0 in range(pc.row0, pc.row0 + pc.nrows, TILE_M):
+            rows = min(TILE_M, pc.row0 + pc.nrows - m0)
+            for n0 in range(pc.col0, pc.col0 + pc.ncols, tn):
+                cols = min(tn, pc.col0 + pc.ncols - n0)
+                if is_remote and direct:
+                    tiles.append(_tile(m0, n0, m0 - pc.owner * R, n0, rows, cols, mode=EPI_STORE_REMOTE,
+                                       chunk=pc.owner, recv_row=F_RS + pc.idx * (G - 1) + slot_of(g, pc.owner)))
+                elif is_remote:
+                    tiles.append(_tile(m0, n0, m0, n0, rows, cols, mode=EPI_STORE_SIGNAL, chunk=unit_of[pc]))
+                else:
+                    local = m0 - g * R
+                    tiles.append(_tile(m0, n0, local, n0, rows, cols, mode=EPI_REDUCE, chunk=pc.idx,
+                                       recv_row=local))
 
     if cta_group == 2:
         tiles[:] = pair_tiles(tiles)
@@ -585,8 +637,9 @@ def lower_rs(scenario: Scenario, kind: ScheduleKind, rank: int, grid: int = 0, v
     # copy program. Stream 0: DONE barrier (every peer has started this run, so its
     # receive slots are free), then one counter wait per push unit, each published as
     # an event the owners' push chains (one per peer q) wait on before their copies.
+    n_idx = 1 + max(pc.idx for _, pc in order)
     if virtual:  # stand-in peers never push: their partials are pre-loaded, mark them all landed at once
-        ops.append(_op(OP_SIGNAL, flag=F_RS, value=G * (G - 1), stream=0))
+        ops.append(_op(OP_SIGNAL, flag=F_RS, value=n_idx * (G - 1), stream=0))
     ops.append(_op(OP_BARRIER, flag=F_DONE, stream=0))
     if direct:  # the tile epilogues push: release them, nothing else to copy
         ops.append(_op(OP_SIGNAL, flag=F_GO, stream=0))
@@ -596,18 +649,24 @@ def lower_rs(scenario: Scenario, kind: ScheduleKind, rank: int, grid: int = 0, v
         for q in range(G):
             if q != g:
                 ops.append(_op(OP_STREAM_WAIT, value=EV_START, stream=_peer_stream(q, g)))
-    for uid, qcs in units:
+    for uid, pcs in enumerate(units):
         slot = 1 + uid % 63
-        ops.append(_op(OP_WAIT_COUNTER, flag=uid, value=tiles_per_chunk * len(qcs), stream=0))
+        ops.append(_op(OP_WAIT_COUNTER, flag=uid, value=tiles_per_piece * len(pcs), stream=0))
         ops.append(_op(OP_RECORD, value=slot, stream=0))
-        for q, c in qcs:
+        for pc in pcs:
+            q = pc.owner
             st = _peer_stream(q, g)
             ops.append(_op(OP_STREAM_WAIT, value=slot, stream=st))
-            src = part_off + (q * R + c * r) * row_bytes
-            dst = low.recv_off + slot_of(g, q) * low.recv_slot + c * r * row_bytes
-            ops.append(_op(OP_COPY, src_buf=BUF_WS, dst_buf=BUF_WS, dst_peer=q, src_off=src, dst_off=dst,
-                           width=r * row_bytes, stream=st))
-            ops.append(_op(OP_NOTIFY, peer=q, flag=F_RS + c * (G - 1) + slot_of(g, q), stream=st))
+            src = part_off + pc.row0 * row_bytes + pc.col0 * ELT
+            dst = low.recv_off + slot_of(g, q) * low.recv_slot + (pc.row0 - q * R) * row_bytes + pc.col0 * ELT
+            if pc.ncols == N:
+                ops.append(_op(OP_COPY, src_buf=BUF_WS, dst_buf=BUF_WS, dst_peer=q, src_off=src, dst_off=dst,
+                               width=pc.nrows * row_bytes, stream=st))
+            else:  # an R x N/G column slab: one 2D copy-engine copy
+                ops.append(_op(OP_COPY, src_buf=BUF_WS, dst_buf=BUF_WS, dst_peer=q, src_off=src, dst_off=dst,
+                               width=pc.ncols * ELT, height=pc.nrows, src_pitch=row_bytes, dst_pitch=row_bytes,
+                               stream=st))
+            ops.append(_op(OP_NOTIFY, peer=q, flag=F_RS + pc.idx * (G - 1) + slot_of(g, q), stream=st))
 
     d = low.desc
     d.a, d.b = _operand(BUF_A, M, K), _operand(BUF_B, N, K)
@@ -616,7 +675,7 @@ def lower_rs(scenario: Scenario, kind: ScheduleKind, rank: int, grid: int = 0, v
     if direct:
         per_word = Counter((t.chunk, t.recv_row) for t in tiles if t.mode == EPI_STORE_REMOTE)
         if len(set(per_word.values())) != 1:
-            raise PlanError("uneven STORE_REMOTE tile counts per (chunk, sender)")
+            raise PlanError("uneven STORE_REMOTE tile counts per (piece, sender)")
         d.rs_target, d.go_flag = next(iter(per_word.values())), F_GO
     d.recv = _operand(BUF_WS, R, N, low.recv_off, low.recv_par)
     d.a2, d.b2 = _operand(BUF_NONE, 0, 0), _operand(BUF_NONE, 0, 0)
@@ -627,8 +686,8 @@ def lower_rs(scenario: Scenario, kind: ScheduleKind, rank: int, grid: int = 0, v
         d.hints |= _agent_hint(comm_agent)
     if len(units) >= 4096 - 1:
         raise PlanError("too many push units")
-    if F_RS + G * (G - 1) >= 4096:
+    if F_RS + n_idx * (G - 1) >= 4096:
         raise PlanError("too many ranks for the RS flag area")
     low.notes = {"kind": kind.value, "rank": g, "world": G, "op": "rs", "units": len(units),
-                 "tiles_per_chunk": tiles_per_chunk, "comm_agent": comm_agent}
+                 "tiles_per_chunk": tiles_per_piece, "comm_agent": comm_agent}
     return low

@@ -62,6 +62,7 @@ class FiccoGroup:
         self._plans: dict = {}
         self._fast: dict = {}
         self._ws_bytes = 0
+        self.device: int | None = None  # CUDA device of the workspaces (set with the first workspace)
 
     @classmethod
     def virtual_group(cls, world: int, rank: int = 0) -> "FiccoGroup":
@@ -78,18 +79,40 @@ class FiccoGroup:
         if self.comm is not None and nbytes <= self._ws_bytes:
             return
         nbytes = 1 << max(20, math.ceil(math.log2(nbytes)))
-        if self.comm is not None:
-            torch.cuda.synchronize()
-            for plan, _ in self._plans.values():
-                plan.close()
-            self._plans.clear()
-            self._fast.clear()
-            self.comm.close()
+        self._retire()
         if self.virtual:
             self.comm = Communicator.virtual(self.world, self.rank, nbytes)
         else:
             self.comm = Communicator.from_process_group(nbytes, self.pg)
         self._ws_bytes = nbytes
+        self.device = torch.cuda.current_device()
+
+    def _barrier(self) -> None:
+        if not self.virtual:
+            import torch.distributed as dist
+            dist.barrier(group=self.pg)
+
+    def _retire(self) -> None:
+        """Free the plans and the communicator without pulling memory from under a peer.
+
+        A peer may still be pulling from our workspace, notifying into our flag block or
+        TMA-storing into our receive slots when we finish our last call, so in a distributed
+        group every rank first drains its own work (synchronize) and meets the others
+        (barrier): after that no rank has device work touching any workspace. Each rank then
+        unmaps the peers' workspaces, meets them again, and only then frees its own — the
+        IPC mappings of it in other processes are gone by then (CUDA leaves freeing memory
+        that peers still map undefined).
+        """
+        if self.comm is None:
+            return
+        torch.cuda.synchronize()
+        self._barrier()
+        for plan, _ in self._plans.values():
+            plan.close()
+        self._plans.clear()
+        self._fast.clear()
+        self.comm.close(between=self._barrier)
+        self.comm = None
 
     def plan(self, key, make) -> tuple[Plan, Lowered]:
         hit = self._plans.get(key)
@@ -123,13 +146,8 @@ class FiccoGroup:
         return self.ws_tensor(self.rank, off, (rows, cols))
 
     def close(self) -> None:
-        for plan, _ in self._plans.values():
-            plan.close()
-        self._plans.clear()
-        self._fast.clear()
-        if self.comm is not None:
-            self.comm.close()
-            self.comm = None
+        """Release the group (collective for distributed groups: every rank must call it)."""
+        self._retire()
 
     # ---------------------------------------------------------------- virtual-mode data
     def load_peer_shards(self, low: Lowered, shards: list[torch.Tensor]) -> None:
@@ -192,6 +210,44 @@ def _default_group(group, world):
     raise ValueError("pass a FiccoGroup (FiccoGroup.distributed(pg) or FiccoGroup.virtual_group(world, rank))")
 
 
+def _check_tensor(name: str, t, shape=None, device=None) -> None:
+    """Validate a call argument before its pointer crosses the C-ABI (the library sizes its TMA maps
+    and copies from the plan, so a wrong dtype, stride, shape or device would read or write out of
+    bounds instead of failing). Raises ValueError, like the reference API's invariant checks."""
+    if not isinstance(t, torch.Tensor):
+        raise ValueError(f"{name} must be a torch.Tensor, got {type(t).__name__}")
+    if t.dtype != torch.bfloat16:
+        raise ValueError(f"{name} must be bfloat16 (the B200 executor computes bf16 x bf16 -> fp32), got {t.dtype}")
+    if t.dim() != 2:
+        raise ValueError(f"{name} must be 2-D, got shape {tuple(t.shape)}")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor, got device {t.device}")
+    if device is not None and t.device != device:
+        raise ValueError(f"{name} is on {t.device}, expected {device}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous (row-major, unit column stride)")
+    if t.data_ptr() % 16:
+        raise ValueError(f"{name} must be 16-byte aligned (TMA / copy-engine rows)")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+
+
+def _check_call(grp: FiccoGroup, args: dict, out, out_shape) -> torch.device:
+    """All operands on the group's device, bf16, contiguous; ``out`` (if given) of ``out_shape``."""
+    dev = None
+    for name, (t, shape) in args.items():
+        _check_tensor(name, t, shape, dev)
+        dev = t.device
+    if dev.index != torch.cuda.current_device():
+        raise ValueError(f"operands are on {dev}, but the current CUDA device is cuda:{torch.cuda.current_device()}"
+                         " (the group's workspaces and streams live there)")
+    if grp.device is not None and dev.index != grp.device:
+        raise ValueError(f"operands are on {dev}, but this FiccoGroup runs on cuda:{grp.device}")
+    if out is not None:
+        _check_tensor("out", out, out_shape, dev)
+    return dev
+
+
 def _cached(grp: FiccoGroup, key, make):
     """Per-call fast path: (plan, lowered, kind) memoised per (op, shape, requested kind)."""
     hit = grp._fast.get(key)
@@ -240,8 +296,6 @@ def prepare_rs(grp: FiccoGroup, M: int, K: int, N: int, kind=None, comm_agent: s
     def make():
         sc = _scenario("gemm_rs", M, N, K, grp.world)
         kd = choose_kind(sc, kind)
-        if kd not in (ScheduleKind.UNIFORM_FUSED_1D, ScheduleKind.HETERO_FUSED_1D, ScheduleKind.HETERO_UNFUSED_1D):
-            kd = ScheduleKind.HETERO_FUSED_1D  # the 2D/serial choices have no RS adjoint on this executor
         plan, low = grp.plan(("rs", M, N, K, kd, comm_agent),
                              lambda: lower_rs(sc, kd, grp.rank, virtual=grp.virtual, comm_agent=comm_agent))
         return plan, low, kd
@@ -253,8 +307,6 @@ def prepare_cp(grp: FiccoGroup, Tq: int, d: int, Tkv: int, kind=None, scale: flo
     def make():
         sc = _scenario("cp_qk", Tkv, Tq, d, grp.world)
         kd = choose_kind(sc, kind)
-        if kd is ScheduleKind.UNIFORM_FUSED_2D:
-            kd = ScheduleKind.UNIFORM_FUSED_1D  # K=d is a single k-segment; the 2D split does not apply
         alpha = (1.0 / math.sqrt(d)) if scale is None else scale
         plan, low = grp.plan(("cp", Tkv, Tq, d, kd, alpha, comm_agent),
                              lambda: lower_ag(build_plan(sc, kd), grp.rank, "B", alpha=alpha, other_rows=Tq,
@@ -263,28 +315,44 @@ def prepare_cp(grp: FiccoGroup, Tq: int, d: int, Tkv: int, kind=None, scale: flo
     return _cached(grp, ("cp", Tq, d, Tkv, kind, scale, comm_agent), make)
 
 
+def _agent(comm_agent) -> str:
+    """comm_agent None -> the B200 machine file's (the reference's MachineConfig.comm_agent, machines.py:48)."""
+    if comm_agent is None:
+        return b200_machine().machine.comm_agent.value
+    return getattr(comm_agent, "value", comm_agent)
+
+
+def _run(grp: FiccoGroup, plan: Plan, op: str, a, b, c, stream) -> None:
+    if SERIALIZE:
+        plan.run_parts(a, b, c, stream, tiles=2)
+    else:
+        plan.run_op(op, a, b, c, stream)
+
+
 def all_gather_matmul(a_shard: torch.Tensor, weight: torch.Tensor, kind=None, group: FiccoGroup | None = None,
                       out: torch.Tensor | None = None, stream=None, return_gathered: bool = False,
-                      comm_agent: str = "dma"):
+                      comm_agent: str | None = None):
     """C = all_gather(A_shard) @ W^T with FiCCO overlap. A_shard [R, K], W [N, K] -> C [G*R, N].
 
     ``return_gathered`` also returns the gathered A (a view into the group's
     double-buffered workspace, valid until the call after next). ``comm_agent``
-    'dma' moves chunks with the copy engines, 'core' with SM copy kernels.
+    'dma' moves chunks with the copy engines, 'core' with SM copy kernels (None:
+    the B200 machine file's agent).
     """
     grp = _default_group(group, None)
+    _check_tensor("a_shard", a_shard)
     R, K = a_shard.shape
+    _check_tensor("weight", weight)
     N = weight.shape[0]
     M = R * grp.world
-    plan, low, kd = prepare_ag(grp, R, K, N, kind, comm_agent=comm_agent)
+    _check_call(grp, {"a_shard": (a_shard, None), "weight": (weight, (N, K))}, out, (M, N))
+    agent = _agent(comm_agent)
+    plan, low, kd = prepare_ag(grp, R, K, N, kind, comm_agent=agent)
     if _is_slot(grp, a_shard, low):  # zero-copy publish: the shard already sits in its slot
-        plan, low, _ = prepare_ag(grp, R, K, N, kd, inplace=True, comm_agent=comm_agent)
+        plan, low, _ = prepare_ag(grp, R, K, N, kd, inplace=True, comm_agent=agent)
     if out is None:
         out = torch.empty(M, N, dtype=torch.bfloat16, device=a_shard.device)
-    if SERIALIZE:
-        plan.run_parts(a_shard, weight, out, stream, tiles=2)
-    else:
-        plan.run_op("ag_gemm", a_shard, weight, out, stream)
+    _run(grp, plan, "ag_gemm", a_shard, weight, out, stream)
     if return_gathered:
         par = (grp.comm.epoch() - 1) & 1  # parity of the run just enqueued
         gathered = grp.ws_tensor(grp.rank, low.gather_off + par * low.gather_par, (M, K))
@@ -294,7 +362,7 @@ def all_gather_matmul(a_shard: torch.Tensor, weight: torch.Tensor, kind=None, gr
 
 def all_to_all_matmul(a_send: torch.Tensor, weight: torch.Tensor, kind=None, group: FiccoGroup | None = None,
                       out: torch.Tensor | None = None, stream=None, return_gathered: bool = False,
-                      comm_agent: str = "dma"):
+                      comm_agent: str | None = None):
     """EP dispatch -> expert GEMM with FiCCO overlap: C = all_to_all(A_send) @ W^T.
 
     ``a_send`` [G*R, K] holds G blocks of R token rows, block d addressed to rank d (uniform
@@ -303,17 +371,17 @@ def all_to_all_matmul(a_send: torch.Tensor, weight: torch.Tensor, kind=None, gro
     returns the dispatched tokens (a view into the group's double-buffered workspace).
     """
     grp = _default_group(group, None)
+    _check_tensor("a_send", a_send)
     M, K = a_send.shape
     if M % grp.world:
         raise PlanError(f"send rows {M} must split into {grp.world} equal blocks")
+    _check_tensor("weight", weight)
     R, N = M // grp.world, weight.shape[0]
-    plan, low, _ = prepare_a2a(grp, R, K, N, kind, comm_agent=comm_agent)
+    _check_call(grp, {"a_send": (a_send, None), "weight": (weight, (N, K))}, out, (M, N))
+    plan, low, _ = prepare_a2a(grp, R, K, N, kind, comm_agent=_agent(comm_agent))
     if out is None:
         out = torch.empty(M, N, dtype=torch.bfloat16, device=a_send.device)
-    if SERIALIZE:
-        plan.run_parts(a_send, weight, out, stream, tiles=2)
-    else:
-        plan.run_op("a2a_gemm", a_send, weight, out, stream)
+    _run(grp, plan, "a2a_gemm", a_send, weight, out, stream)
     if return_gathered:
         par = (grp.comm.epoch() - 1) & 1
         return out, grp.ws_tensor(grp.rank, low.gather_off + par * low.gather_par, (M, K))
@@ -321,36 +389,38 @@ def all_to_all_matmul(a_send: torch.Tensor, weight: torch.Tensor, kind=None, gro
 
 
 def matmul_reduce_scatter(a: torch.Tensor, weight: torch.Tensor, kind=None, group: FiccoGroup | None = None,
-                          out: torch.Tensor | None = None, stream=None, comm_agent: str = "dma"):
+                          out: torch.Tensor | None = None, stream=None, comm_agent: str | None = None):
     """C_shard = reduce_scatter_rows(A @ W^T). A [M, Kg], W [N, Kg] -> [M/G, N] (this rank's rows)."""
     grp = _default_group(group, None)
+    _check_tensor("a", a)
     M, K = a.shape
+    if M % grp.world:
+        raise PlanError(f"rows {M} must split into {grp.world} equal output shards")
+    _check_tensor("weight", weight)
     N = weight.shape[0]
-    plan, _, _ = prepare_rs(grp, M, K, N, kind, comm_agent=comm_agent)
+    _check_call(grp, {"a": (a, None), "weight": (weight, (N, K))}, out, (M // grp.world, N))
+    plan, _, _ = prepare_rs(grp, M, K, N, kind, comm_agent=_agent(comm_agent))
     if out is None:
         out = torch.empty(M // grp.world, N, dtype=torch.bfloat16, device=a.device)
-    if SERIALIZE:
-        plan.run_parts(a, weight, out, stream, tiles=2)
-    else:
-        plan.run_op("gemm_rs", a, weight, out, stream)
+    _run(grp, plan, "gemm_rs", a, weight, out, stream)
     return out
 
 
 def cp_kv_all_gather_qk(q: torch.Tensor, k_shard: torch.Tensor, kind=None, scale: float | None = None,
                         group: FiccoGroup | None = None, out: torch.Tensor | None = None, stream=None,
-                        comm_agent: str = "dma"):
+                        comm_agent: str | None = None):
     """S = scale * Q @ all_gather(K_shard)^T. Q [Tq, d], K_shard [Tkv/G, d] -> S [Tq, Tkv] (bf16).
 
     Scenario view: M = Tkv (gathered kv tokens), N = Tq, K = d.
     """
     grp = _default_group(group, None)
+    _check_tensor("q", q)
     Tq, d = q.shape
+    _check_tensor("k_shard", k_shard)
     Tkv = k_shard.shape[0] * grp.world
-    plan, _, _ = prepare_cp(grp, Tq, d, Tkv, kind, scale, comm_agent=comm_agent)
+    _check_call(grp, {"q": (q, None), "k_shard": (k_shard, (Tkv // grp.world, d))}, out, (Tq, Tkv))
+    plan, _, _ = prepare_cp(grp, Tq, d, Tkv, kind, scale, comm_agent=_agent(comm_agent))
     if out is None:
         out = torch.empty(Tq, Tkv, dtype=torch.bfloat16, device=q.device)
-    if SERIALIZE:
-        plan.run_parts(q, k_shard, out, stream, tiles=2)
-    else:
-        plan.run_op("cp_qk", q, k_shard, out, stream)
+    _run(grp, plan, "cp_qk", q, k_shard, out, stream)
     return out

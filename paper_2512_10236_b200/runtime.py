@@ -45,6 +45,7 @@ EXPORTED = (
     "ficco_plan_create", "ficco_plan_destroy", "ficco_plan_run", "ficco_plan_run_parts",
     "ficco_gemm_bf16", "ficco_copy_batch", "ficco_plan_set_trace", "ficco_plan_info", "ficco_gemm_bf16_cfg", "ficco_occupy_sms",
     "ficco_timestamp", "ficco_ag_gemm", "ficco_a2a_gemm", "ficco_gemm_rs", "ficco_cp_qk",
+    "ficco_plan_set_kernel_event",
 )
 
 
@@ -124,6 +125,7 @@ def load_library(path: os.PathLike | str | None = None) -> C.CDLL:
             "ficco_occupy_sms": ([i64, vp], i32),
             "ficco_timestamp": ([vp, vp], i32),
             "ficco_plan_set_trace": ([vp, vp], i32),
+            "ficco_plan_set_kernel_event": ([vp, vp], i32),
             "ficco_plan_info": ([vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)], i32),
         }
         for name, (args, res) in sig.items():
@@ -257,15 +259,20 @@ class Communicator:
         check(load_library().ficco_comm_set_flags(C.c_void_p(self.handle), first, count, value,
                                                   C.c_void_p(_stream_ptr(stream))))
 
-    def close(self) -> None:
+    def close(self, between=None) -> None:
+        """Destroy the communicator, unmap the peers' workspaces, then (after ``between()``,
+        e.g. a process-group barrier) free the own ones."""
         if self.handle:
             load_library().ficco_comm_destroy(C.c_void_p(self.handle))
             self.handle = None
             for p in self._opened:
                 ipc_close(p)
+            self._opened = []
+            if between is not None:
+                between()
             for w in self._owned:
                 w.free()
-            self._owned, self._opened = [], []
+            self._owned = []
 
     def __del__(self):  # pragma: no cover - best effort
         try:
@@ -319,6 +326,13 @@ class Plan:
         self._trace = buf
         check(load_library().ficco_plan_set_trace(C.c_void_p(self.handle),
                                                   C.c_void_p(0 if buf is None else buf.data_ptr())))
+
+    def set_kernel_event(self, event) -> None:
+        """Record ``event`` (a torch.cuda.Event that has been recorded once, or None) on the launch
+        stream right after the tile kernel of every later run: times the in-op kernel alone."""
+        self._kernel_event = event
+        check(load_library().ficco_plan_set_kernel_event(
+            C.c_void_p(self.handle), C.c_void_p(0 if event is None else event.cuda_event)))
 
     def close(self) -> None:
         if self.handle:

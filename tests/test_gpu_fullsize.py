@@ -11,8 +11,10 @@ properties of the path:
   routing or gating error shows up as a mismatch;
 * identity with the flag-free tile GEMM of the gathered operand (AG / CP);
 * idempotence: consecutive calls (alternating workspace parities) give identical results;
-* numerics: sampled rows from every shard against the oracle's fp32 arithmetic on the
-  same bf16 inputs (numpy), within the stated tolerance rtol 1.6e-2 / atol 1e-2 (x sqrt(G) for RS).
+* numerics: the WHOLE output against a plain PyTorch fp32 reference of the same op (cuBLAS
+  fp32 GEMM, TF32 off, computed in row blocks), and sampled rows from every shard against the
+  oracle's fp32 arithmetic on the same bf16 inputs (numpy), both within the stated tolerance
+  rtol 1.6e-2 / atol 1e-2 (x sqrt(G) for RS).
 """
 import math
 
@@ -28,7 +30,7 @@ RTOL, ATOL = 1.6e-2, 1e-2
 G = 8
 AG_KINDS = ["serial", "shard_overlap_p2p", "uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d",
             "uniform_fused_2d"]
-RS_KINDS = ["uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d"]
+RS_KINDS = AG_KINDS  # every executable kind has an RS adjoint (2D: N blocks)
 CP_KINDS = ["serial", "shard_overlap_p2p", "uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d"]
 
 
@@ -51,6 +53,27 @@ def _rand(shape, seed, kind="uniform"):
 
 def _np(t):
     return t.float().cpu().numpy()
+
+
+def _assert_close_fp32(out, a, w, alpha=1.0, addends=(), atol=ATOL, block=8192):
+    """Every element of out [M, N] against alpha * a @ w^T (+ sum of addends) computed in fp32 by cuBLAS
+    with TF32 off, in row blocks (C4's fp32 reference alone would be 8.6 GB)."""
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        wf = w.float()
+        for r0 in range(0, out.shape[0], block):
+            ref = torch.matmul(a[r0:r0 + block].float(), wf.t())
+            if alpha != 1.0:
+                ref.mul_(alpha)
+            for x in addends:
+                ref += x[r0:r0 + block].float()
+            got = out[r0:r0 + block].float()
+            if not torch.allclose(got, ref, rtol=RTOL, atol=atol):
+                err = ((got - ref).abs() - RTOL * ref.abs()).max().item()
+                raise AssertionError(f"rows {r0}..: exceeds rtol {RTOL} / atol {atol} by {err}")
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
 
 
 def _sample_rows(total, per_block, blocks, seed=0):
@@ -87,6 +110,7 @@ def test_c2_full_size_all_kinds_bit_identical(ops, rank):
                     assert torch.equal(out, plain), (agent, kind, it, "output differs from the plain GEMM")
     finally:
         grp.close()
+    _assert_close_fp32(plain, a_all, w)
     rows = _sample_rows(G * R, 4, G)
     want = _np(a_all[rows]) @ _np(w).T
     np.testing.assert_allclose(_np(plain[rows]), want, rtol=RTOL, atol=ATOL)
@@ -122,6 +146,7 @@ def test_c3_full_size_all_kinds_bit_identical(ops, world):
                         assert torch.equal(out, first), (agent, kind, it, "RS output differs between schedules")
     finally:
         grp.close()
+    _assert_close_fp32(first, a[rank * R:(rank + 1) * R], w, addends=peers, atol=ATOL * math.sqrt(G))
     # oracle arithmetic on sampled rows: own fp32 partial + peers' bf16 partials in rank order
     rows = _sample_rows(R, 6, 4)
     acc = _np(a[rank * R + rows]) @ _np(w).T
@@ -154,6 +179,7 @@ def test_c4_full_size_all_kinds_bit_identical(ops):
                     assert torch.equal(out, plain), (agent, kind, it, "scores differ from the plain GEMM")
     finally:
         grp.close()
+    _assert_close_fp32(plain, q, k_all, alpha=scale, block=4096)
     rows = _sample_rows(Tq, 4, 8)
     want, _ = orc.execute_cp_qk(_np(q[rows]), [_np(k) for k in ks], scale)
     np.testing.assert_allclose(_np(plain[rows]), want, rtol=RTOL, atol=ATOL)
@@ -186,5 +212,37 @@ def test_ep_full_size_all_kinds_bit_identical(ops):
                     assert torch.equal(out, plain), (agent, kind, it, "expert GEMM differs from the plain GEMM")
     finally:
         grp.close()
+    _assert_close_fp32(plain, disp_ref, w)
     rows = _sample_rows(M, 3, G)
     np.testing.assert_allclose(_np(plain[rows]), _np(disp_ref[rows]) @ _np(w).T, rtol=RTOL, atol=ATOL)
+
+
+@pytest.mark.parametrize("agent", ["dma", "core"])
+def test_c1_all_kinds_vs_oracle(ops, agent):
+    """BASELINE.json configs[0] on the GPU: 4 ranks, M = N = K = 4096 (bf16 here; the CPU oracle runs it in
+    fp32, tests/test_oracle.py::test_c1_at_size_every_kind), every executable schedule, every rank, against
+    the oracle's execute_ag of the same bf16-valued inputs: gathered operand bit-exact, the whole product
+    within rtol 1.6e-2 / atol 1e-2."""
+    Gc, R, K, N = 4, 1024, 4096, 4096
+    shards = [orc.seeded_inputs(0, p, (R, K)) for p in range(Gc)]
+    w = orc.seeded_inputs(0, 99, (N, K), "normal")
+    full = np.concatenate(shards)
+    want = full @ w.T  # every kind's oracle output equals the full product up to fp32 summation order
+    ts = [torch.from_numpy(x).to(torch.bfloat16).cuda() for x in shards]
+    wt = torch.from_numpy(w).to(torch.bfloat16).cuda()
+    for rank in range(Gc):
+        grp = ops.FiccoGroup.virtual_group(Gc, rank)
+        try:
+            for kind in AG_KINDS:
+                gathered_ref, outs = orc.execute_ag(kind, shards, w) if rank == 0 else (None, None)
+                if rank == 0:  # the oracle's own per-kind result (fragment order, 2D K blocks) is the product
+                    np.testing.assert_allclose(outs[0], want, rtol=1e-4, atol=1e-4)
+                _, low, _ = ops.prepare_ag(grp, R, K, N, kind, comm_agent=agent)
+                grp.load_peer_shards(low, ts)
+                out, gathered = ops.all_gather_matmul(ts[rank], wt, kind=kind, group=grp, return_gathered=True,
+                                                      comm_agent=agent)
+                grp.comm.check()
+                assert np.array_equal(_np(gathered), full), (kind, rank)
+                np.testing.assert_allclose(_np(out), want, rtol=RTOL, atol=ATOL, err_msg=f"{kind} rank {rank}")
+        finally:
+            grp.close()

@@ -100,7 +100,10 @@ def test_ag_ragged_chunks(lib, kind):
         grp.close()
 
 
-@pytest.mark.parametrize("kind", ["uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d"])
+RS_KINDS = AG_KINDS  # every executable kind has an RS adjoint (lowering.rs_pieces); 2D = N blocks
+
+
+@pytest.mark.parametrize("kind", RS_KINDS)
 @pytest.mark.parametrize("G,rank", [(2, 0), (4, 2), (8, 7)])
 def test_rs_virtual_matches_oracle(lib, kind, G, rank):
     from paper_2512_10236_b200 import ops
@@ -188,7 +191,7 @@ def test_ag_core_agent_matches_oracle(lib, kind):
         grp.close()
 
 
-@pytest.mark.parametrize("kind", ["uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d"])
+@pytest.mark.parametrize("kind", RS_KINDS)
 def test_rs_core_agent_matches_oracle(lib, kind):
     from paper_2512_10236_b200 import ops
     G, rank = 4, 2
@@ -304,6 +307,9 @@ def test_missing_transfer_times_out_as_deadlock_error(lib, monkeypatch):
         with pytest.raises(DeadlockError):
             grp.comm.check()
         assert time.time() - t0 < 30
+        # the communicator is poisoned: later runs refuse up front instead of computing on stale chunks
+        with pytest.raises(DeadlockError, match="poisoned"):
+            plan.run(a, w, c)
         plan.close()
     finally:
         grp.close()
@@ -372,5 +378,99 @@ def test_ag_ring_split_matches_oracle(lib, split, monkeypatch):
             grp.comm.check()
             assert np.array_equal(_np(gathered), gathered_ref[rank])
             np.testing.assert_allclose(_np(out), outs[rank], rtol=RTOL, atol=ATOL)
+    finally:
+        grp.close()
+
+
+@pytest.mark.parametrize("agent", ["dma", "core"])
+def test_rs_2d_ragged(lib, agent):
+    """N-block (2D-adjoint) GEMM -> RS: 160-column blocks (tile-width tails inside each block), K tail of 8."""
+    from paper_2512_10236_b200 import ops
+    G, rank = 4, 1
+    M, Kg, N = 128 * G, 200, 640
+    a = [orc.seeded_inputs(14, p, (M, Kg)) for p in range(G)]
+    w = [orc.seeded_inputs(14, 100 + p, (N, Kg), "normal") for p in range(G)]
+    want = orc.execute_rs(a, w)[rank]
+    R = M // G
+    peers = [orc.bf16_round(a[p] @ w[p].T)[rank * R:(rank + 1) * R] for p in range(G) if p != rank]
+    grp = ops.FiccoGroup.virtual_group(G, rank)
+    try:
+        _, low, _ = ops.prepare_rs(grp, M, Kg, N, "uniform_fused_2d", comm_agent=agent)
+        grp.load_peer_partials(low, [_t(x) for x in peers])
+        for _ in range(2):
+            out = ops.matmul_reduce_scatter(_t(a[rank]), _t(w[rank]), kind="uniform_fused_2d", group=grp,
+                                            comm_agent=agent)
+            grp.comm.check()
+            np.testing.assert_allclose(_np(out), want, rtol=RTOL, atol=ATOL * math.sqrt(G))
+    finally:
+        grp.close()
+
+
+def test_unsupported_kinds_raise_instead_of_substituting(lib):
+    """No silent schedule rewrite: a kind the executor cannot run for this shape raises PlanError."""
+    from paper_2512_10236_b200 import ops
+    from paper_2512_10236_b200.routing import PlanError
+    grp = ops.FiccoGroup.virtual_group(4, 0)
+    try:
+        with pytest.raises(PlanError, match="N/G"):  # 544 / 4 = 136 columns: not a multiple of 32
+            ops.prepare_rs(grp, 128 * 4, 256, 544, "uniform_fused_2d")
+        with pytest.raises(PlanError, match="multiple of 64"):  # d / G = 32: no whole k-block per round
+            ops.prepare_cp(grp, 256, 128, 1024, "uniform_fused_2d")
+        with pytest.raises(PlanError):
+            ops.prepare_rs(grp, 128 * 4, 256, 512, "ideal")
+    finally:
+        grp.close()
+
+
+def test_cp_2d_kblocks_matches_oracle(lib):
+    """CP QK^T under uniform_fused_2d (d = 512, G = 4: one 128-column k-slab of every K shard per round)."""
+    from paper_2512_10236_b200 import ops
+    G, rank, d, Tq, Tkv = 4, 2, 512, 256, 2048
+    q = orc.seeded_inputs(15, 50, (Tq, d), "normal")
+    ks = [orc.seeded_inputs(15, p, (Tkv // G, d), "normal") for p in range(G)]
+    want, _ = orc.execute_cp_qk(q, ks, 1.0 / math.sqrt(d))
+    grp = ops.FiccoGroup.virtual_group(G, rank)
+    try:
+        _, low, _ = ops.prepare_cp(grp, Tq, d, Tkv, "uniform_fused_2d")
+        grp.load_peer_shards(low, [_t(x) for x in ks])
+        for _ in range(2):
+            out = ops.cp_kv_all_gather_qk(_t(q), _t(ks[rank]), kind="uniform_fused_2d", group=grp)
+            grp.comm.check()
+            np.testing.assert_allclose(_np(out), want, rtol=RTOL, atol=ATOL)
+    finally:
+        grp.close()
+
+
+def test_op_boundary_validates_operands(lib):
+    """Malformed call arguments raise ValueError before any pointer reaches the C-ABI."""
+    from paper_2512_10236_b200 import ops
+    G, R, K, N = 4, 256, 256, 256
+    grp = ops.FiccoGroup.virtual_group(G, 0)
+    bf = dict(dtype=torch.bfloat16, device="cuda")
+    a, w = torch.zeros(R, K, **bf), torch.zeros(N, K, **bf)
+    try:
+        bad = [
+            (lambda: ops.all_gather_matmul(a.float(), w, group=grp), "bfloat16"),
+            (lambda: ops.all_gather_matmul(a, torch.zeros(N, K // 2, **bf), group=grp), "shape"),
+            (lambda: ops.all_gather_matmul(a, w[:, :128], group=grp), "contiguous"),
+            (lambda: ops.all_gather_matmul(torch.zeros(K, R, **bf).t(), w, group=grp), "contiguous"),
+            (lambda: ops.all_gather_matmul(a, w, group=grp, out=torch.empty(R, N, **bf)), "shape"),
+            (lambda: ops.all_gather_matmul(a, w, group=grp, out=torch.empty(G * R, N, device="cuda")), "bfloat16"),
+            (lambda: ops.all_gather_matmul(a.cpu(), w, group=grp), "CUDA"),
+            (lambda: ops.matmul_reduce_scatter(torch.zeros(G * R, K, **bf), torch.zeros(N, 64, **bf), group=grp),
+             "shape"),
+            (lambda: ops.matmul_reduce_scatter(torch.zeros(G * R, K, **bf), w, group=grp,
+                                               out=torch.empty(G * R, N, **bf)), "shape"),
+            (lambda: ops.cp_kv_all_gather_qk(torch.zeros(R, 128, **bf), torch.zeros(R, 64, **bf), group=grp),
+             "shape"),
+            (lambda: ops.all_to_all_matmul(torch.zeros(G * R, K, **bf), w.to(torch.float16), group=grp), "bfloat16"),
+            (lambda: ops.all_gather_matmul(torch.zeros(R * K + 1, **bf)[1:].view(R, K), w, group=grp), "aligned"),
+        ]
+        for call, msg in bad:
+            with pytest.raises(ValueError, match=msg):
+                call()
+        out = ops.all_gather_matmul(a, w, kind="hetero_fused_1d", group=grp)  # well-formed: runs
+        grp.comm.check()
+        assert out.shape == (G * R, N)
     finally:
         grp.close()

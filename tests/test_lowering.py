@@ -54,7 +54,8 @@ def test_ag_tiles_cover_output_once_and_gates_cover_rows(kind, M, N, K, G, colle
                 assert (a.b_row, a.c_col, a.cols) == (b.b_row, b.c_col, b.cols)
 
 
-@pytest.mark.parametrize("kind", ["uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d"])
+@pytest.mark.parametrize("kind", ["serial", "shard_overlap_p2p", "uniform_fused_1d", "hetero_fused_1d",
+                                  "hetero_unfused_1d", "uniform_fused_2d"])
 @pytest.mark.parametrize("agent", ["dma", "core"])
 def test_rs_tiles_cover_partials_and_own_rows_once(kind, agent):
     G, M, N, K = 8, 4096, 1024, 512

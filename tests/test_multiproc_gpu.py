@@ -18,7 +18,7 @@ pytestmark = pytest.mark.gpu
 
 AG_KINDS = ["serial", "shard_overlap_p2p", "uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d",
             "uniform_fused_2d"]
-RS_KINDS = ["uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d"]
+RS_KINDS = AG_KINDS  # every executable kind has an RS adjoint (2D: N blocks)
 
 
 def _free_port() -> int:

@@ -114,3 +114,39 @@ def test_a2a_plans_equal_all_gather_plans():
     for kind in supported_kinds(ag):
         a, e = build_plan(ag, kind), build_plan(ep, kind)
         assert [(t.gpu, t.deps, t.kind) for t in a.tasks] == [(t.gpu, t.deps, t.kind) for t in e.tasks], kind
+
+
+C1_KINDS = ["serial", "shard_overlap_p2p", "uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d",
+            "uniform_fused_2d"]
+
+
+def test_c1_at_size_every_kind():
+    """BASELINE.json configs[0] at its size: 4 simulated ranks, M = N = K = 4096, fp32, every executable
+    schedule through the oracle (the reference's CPU sweep, /root/reference/pkg/tests/test_acceptance.py:87-118).
+
+    Per rank and kind: the routed (gathered) operand is bit-exact, per-GPU ingress is (G-1)*R*K*e and the
+    GEMM fragments cover 2MNK exactly (the reference's conservation criterion), and the result matches
+    one full fp32 matmul (only the fragmenting / the 2D K-block summation order differs).
+    """
+    from paper_2512_10236_b200 import ops
+    from paper_2512_10236_b200.routing import GemmSpec, ScheduleKind, TransferSpec, build_plan
+    G, M, N, K, elt = 4, 4096, 4096, 4096, 4
+    R = M // G
+    shards = [orc.seeded_inputs(0, p, (R, K)) for p in range(G)]
+    w = orc.seeded_inputs(0, 99, (N, K), "normal")
+    full = np.concatenate(shards)
+    want = full @ w.T
+    sc = ops._scenario("c1", M, N, K, G)
+    sc = type(sc)(name=sc.name, parallelism=sc.parallelism, model=sc.model,
+                  gemm=type(sc.gemm)(M, N, K, elt), collective=sc.collective, n_gpus=G)
+    for kind in C1_KINDS:
+        plan = build_plan(sc, ScheduleKind(kind))
+        for gpu in range(G):
+            ingress = sum(t.kind.bytes for t in plan.tasks if isinstance(t.kind, TransferSpec) and t.kind.dst == gpu)
+            flops = sum(t.kind.flops for t in plan.tasks if t.gpu == gpu and isinstance(t.kind, GemmSpec))
+            assert ingress == (G - 1) * R * K * elt and flops == 2 * M * N * K, (kind, gpu)
+            assert sum(x[2] for x in orc.transfers(kind, M, K, G, elt) if x[0] == gpu) == ingress
+        for gpu in (0, G - 1):
+            buf, c = orc._route_and_gemm(kind, shards, w, gpu)
+            assert np.array_equal(buf, full), kind
+            np.testing.assert_allclose(c, want, rtol=1e-4, atol=1e-4, err_msg=kind)

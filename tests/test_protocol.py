@@ -105,14 +105,16 @@ def test_a2a_protocol(kind, G, cta_group):
         assert len(checked) == G * RUNS
 
 
-@pytest.mark.parametrize("kind", ["uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d"])
+@pytest.mark.parametrize("kind", AG_KINDS)
 @pytest.mark.parametrize("G", [2, 3, 4])
 @pytest.mark.parametrize("cta_group", [1, 2])
 @pytest.mark.parametrize("agent", ["dma", "core"])
 def test_rs_protocol(kind, G, cta_group, agent):
-    """comm_agent 'dma': copy-engine pushes of the partial chunks; 'core': the tile epilogues store
-    the partials straight into the owners' receive slots and count tiles into their flag words."""
-    r, Kg, N = 16, 64, 64
+    """comm_agent 'dma': copy-engine pushes of the partial pieces; 'core': the tile epilogues store
+    the partials straight into the owners' receive slots and count tiles into their flag words.
+    Every executable kind has an RS adjoint (lowering.rs_pieces), uniform_fused_2d as N blocks."""
+    r, Kg = 16, 64
+    N = 64 if kind != "uniform_fused_2d" else 32 * G
     M = r * G * G
     R = M // G
     for seed in range(3):
