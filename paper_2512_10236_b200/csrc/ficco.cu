@@ -153,12 +153,13 @@ int64_t raster_rows(int64_t m, int64_t n, int64_t k, int64_t mstep) {
 
 // Resolve the (tile width, CTA group, staging buffers) instantiation: entry point, dynamic smem,
 // B box rows.
-int kernel_for(int tn, int cg, int eb, const void** fn, int* smem, int* b_rows) {
+int kernel_for(int tn, int cg, int eb, const void** fn, int* smem, int* b_rows, int* stages = nullptr) {
 #define FICCO_CASE(T, G, E)                                                  \
   if (tn == T && cg == G && eb == E) {                                       \
     *fn = reinterpret_cast<const void*>(ficco::tile_gemm_kernel<T, G, E>);   \
     *smem = ficco::TileCfg<T, G, E>::SMEM_BYTES;                             \
     *b_rows = ficco::TileCfg<T, G, E>::B_ROWS;                               \
+    if (stages) *stages = ficco::TileCfg<T, G, E>::STAGES;                   \
     return 0;                                                                \
   }
   FICCO_FOR_EACH_CFG(FICCO_CASE)
@@ -444,9 +445,15 @@ int make_params(ficco_plan* p, uint32_t parity, const void* a, const void* b, vo
   if ((r = encode_bf16_2d(cm->drv, &prm->tmap_a, pa, d.a.rows, d.k, d.a.ld, ficco::BM))) return r;
   {
     const void* fn;
-    int smem, b_rows;
-    if ((r = kernel_for(p->tile_n, p->cta_group, p->epi_bufs, &fn, &smem, &b_rows))) return r;
+    int smem, b_rows, stages;
+    if ((r = kernel_for(p->tile_n, p->cta_group, p->epi_bufs, &fn, &smem, &b_rows, &stages))) return r;
     if ((r = encode_bf16_2d(cm->drv, &prm->tmap_b, pb, d.b.rows, d.k, d.b.ld, b_rows))) return r;
+    // B-resident mode for short-K programs without REDUCE tiles (their identity-MMA boxes use the B slots):
+    // consecutive tiles of a CTA that share B rows stream only A (FICCO_B_RESIDENT=0/1 overrides)
+    const char* env = getenv("FICCO_B_RESIDENT");
+    const int kbs = int((d.k + ficco::BK - 1) / ficco::BK);
+    const bool can = kbs <= stages && p->role != ROLE_REDUCE_SCATTER;
+    prm->b_resident = can && (env ? env[0] == '1' : kbs <= 4) ? 1 : 0;
     prm->tmap_a2 = prm->tmap_a;
     prm->tmap_b2 = prm->tmap_b;
     if (d.a2.buf != FICCO_BUF_NONE) {
@@ -545,6 +552,15 @@ int make_params(ficco_plan* p, uint32_t parity, const void* a, const void* b, vo
   }
   prm->alpha = d.alpha;
   prm->a_evict_last = (d.hints & FICCO_HINT_A_EVICT_LAST) != 0;
+  {
+    // Output stores: evict_first keeps the operands L2-resident under compute-bound programs; a
+    // store-bound program (short K: C4's score write) writes HBM ~10 % faster with plain stores
+    // (tools/epi_probe.cu: 6.35 vs 5.72 TB/s). FICCO_OUT_HINT=first|none overrides.
+    const char* env = getenv("FICCO_OUT_HINT");
+    prm->out_plain = env && env[0] == 'n' ? 1 : env && env[0] == 'f' ? 0 : (p->epi_bufs > 1 ? 1 : 0);
+    const char* fast = getenv("FICCO_EPI_FAST");
+    prm->epi_fast = fast && fast[0] == '0' ? 0 : 1;
+  }
   prm->b_evict_first = (d.hints & FICCO_HINT_B_EVICT_FIRST) != 0;
   prm->trace = p->trace;
   int g = d.grid > 0 ? d.grid : cm->sms;
@@ -1073,25 +1089,39 @@ int ficco_gemm_bf16_cfg(const void* a, const void* b, void* c, int64_t m, int64_
     }
     std::vector<ficco_tile> tiles;
     const int64_t mstep = int64_t(ficco::BM) * cta_group;
+    auto push = [&](int64_t i, int64_t j, bool pad) {
+      for (int h = 0; h < cta_group; ++h) {
+        const int64_t row = i + h * ficco::BM;
+        ficco_tile t{};
+        t.a_row = int32_t(row < m ? row : i);
+        t.b_row = int32_t(j);
+        t.c_row = int32_t(row);
+        t.c_col = int32_t(j);
+        t.rows = int16_t(pad || row >= m ? 0 : (m - row < ficco::BM ? m - row : ficco::BM));
+        t.cols = int16_t(n - j < tn ? n - j : tn);
+        t.flag = -1;
+        t.fmask = 0;
+        t.mode = FICCO_EPI_STORE;
+        tiles.push_back(t);
+      }
+    };
     const char* genv = getenv("FICCO_GEMM_GROUP_M");  // pair-blocks per raster group (A/B experiments)
-    const int64_t group = genv ? std::max<int64_t>(1, atoll(genv)) * mstep : raster_rows(m, n, k, mstep);
-    for (int64_t i0 = 0; i0 < m; i0 += group)
-      for (int64_t j = 0; j < n; j += tn)
-        for (int64_t i = i0; i < std::min(m, i0 + group); i += mstep)
-        for (int h = 0; h < cta_group; ++h) {
-          const int64_t row = i + h * ficco::BM;
-          ficco_tile t{};
-          t.a_row = int32_t(row < m ? row : i);
-          t.b_row = int32_t(j);
-          t.c_row = int32_t(row);
-          t.c_col = int32_t(j);
-          t.rows = int16_t(row >= m ? 0 : (m - row < ficco::BM ? m - row : ficco::BM));
-          t.cols = int16_t(n - j < tn ? n - j : tn);
-          t.flag = -1;
-          t.fmask = 0;
-          t.mode = FICCO_EPI_STORE;
-          tiles.push_back(t);
-        }
+    const int64_t slots = (grid > 0 ? grid : cm->sms) / cta_group;
+    const int64_t ncb = (n + tn - 1) / tn;
+    const char* benv = getenv("FICCO_B_RESIDENT");
+    if (!genv && cta_group == 2 && k <= 256 && ncb >= slots && !(benv && benv[0] == '0')) {
+      // short K (store-bound, b_resident): waves of `slots` column blocks listed row-block by row-block, so
+      // CTA pair p (which takes pair-tiles p, p + slots, ...) keeps ONE column block of B in smem for all of
+      // M and streams only A; a partial last wave is padded with load-only pair tiles to keep the mapping
+      for (int64_t w0 = 0; w0 < ncb; w0 += slots)
+        for (int64_t i = 0; i < m; i += mstep)
+          for (int64_t u = w0; u < w0 + slots; ++u) push(i, (u < ncb ? u : w0) * tn, u >= ncb);
+    } else {
+      const int64_t group = genv ? std::max<int64_t>(1, atoll(genv)) * mstep : raster_rows(m, n, k, mstep);
+      for (int64_t i0 = 0; i0 < m; i0 += group)
+        for (int64_t j = 0; j < n; j += tn)
+          for (int64_t i = i0; i < std::min(m, i0 + group); i += mstep) push(i, j, false);
+    }
     ficco_plan_desc d{};
     d.n_tiles = int32_t(tiles.size());
     d.tiles = tiles.data();

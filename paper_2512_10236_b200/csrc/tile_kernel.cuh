@@ -117,9 +117,15 @@ struct alignas(64) TileParams {
   int reduce_mma;          // REDUCE tiles fold the peers' partials in with identity MMAs (else epilogue loads;
                            // 2: boxes streamed through the ring without the MMAs, timing experiments only)
   int recv_rows;           // rows per receive slot in tmap_recv (slot j starts at row j * recv_rows)
+  int b_resident;          // short-K programs: a CTA's B rows stay in smem while consecutive tiles share them
+                           // (b_row, b_src): only A is streamed through the ring (halves the L2->SM bytes
+                           // of C4's store-bound tiles). Requires num_kb <= STAGES and no REDUCE tiles.
   int a_evict_last;        // FICCO_HINT_A_EVICT_LAST
   int b_evict_first;       // FICCO_HINT_B_EVICT_FIRST
   int part_hint;           // L2 policy of STORE_SIGNAL (to-be-pushed) stores: 0 evict_first, 1 normal, 2 last
+  int epi_fast;            // full 64-column chunks take the straight-line epilogue path (FICCO_EPI_FAST=0: off)
+  int out_plain;           // STORE / REDUCE output boxes stored without an L2 policy (store-bound programs:
+                           // +10 % HBM write rate over evict_first, tools/epi_probe.cu)
   uint32_t* flags;         // local flag block of this run's parity
   uint32_t* counters;      // local tile counters
   uint32_t* abort_word;
@@ -184,16 +190,29 @@ __device__ __forceinline__ void wait_flag_cached(uint32_t* seen, const uint32_t*
 
 template <int TN, int CG, int EB>
 __device__ __forceinline__ void producer_loop(const TileParams& p, uint8_t* sA, uint8_t* sB, uint64_t* full,
-                                              uint64_t* empty, uint32_t rank, uint32_t* seen) {
+                                              uint64_t* empty, uint32_t rank, uint32_t* seen, uint64_t* bfree) {
   using Cfg = TileCfg<TN, CG, EB>;
   const uint64_t hint_a = p.a_evict_last ? policy_evict_last() : policy_evict_first();
   const uint64_t hint_b = p.b_evict_first ? policy_evict_first() : policy_evict_last();
   uint32_t stage = 0, phase = 0;
+  int res_b_row = -1, res_b_src = -1;  // B rows resident in smem (b_resident mode)
+  uint32_t bfree_phase = 0;
   for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
     const ficco_tile td = p.tiles[t];
     const int b_row = td.b_row + int(rank) * Cfg::B_ROWS;
     const CUtensorMap* map_a = td.a_src ? &p.tmap_a2 : &p.tmap_a;
     const CUtensorMap* map_b = td.b_src ? &p.tmap_b2 : &p.tmap_b;
+    // b_resident: (re)load B only when this tile's B rows differ from the resident ones, after the MMAs
+    // of every tile that read the old rows completed (b_free, committed by the MMA issuer)
+    const bool load_b = !p.b_resident || td.b_row != res_b_row || int(td.b_src) != res_b_src;
+    if (p.b_resident && load_b) {
+      if (res_b_row >= 0) {
+        mbar_wait(bfree, bfree_phase);
+        bfree_phase ^= 1u;
+      }
+      res_b_row = td.b_row;
+      res_b_src = td.b_src;
+    }
     for (int kb = 0; kb < p.num_kb; ++kb) {
       if (td.flag >= 0) {
         int base = -1;
@@ -214,15 +233,19 @@ __device__ __forceinline__ void producer_loop(const TileParams& p, uint8_t* sA, 
       }
       if (kb == 0 && p.trace) p.trace[gridDim.x + 2 * t] = globaltimer();
       mbar_wait(&empty[stage], phase ^ 1u);
+      // resident B of k-block kb lives in the B slot of stage kb (the A ring uses only the A slots)
+      uint8_t* dst_b = sB + (p.b_resident ? kb : int(stage)) * Cfg::B_STAGE;
+      const uint32_t bytes = load_b ? Cfg::STAGE : A_STAGE;
       if constexpr (CG == 1) {
-        mbar_arrive_expect_tx(&full[stage], Cfg::STAGE);
+        mbar_arrive_expect_tx(&full[stage], bytes);
         tma_load_2d(sA + stage * A_STAGE, map_a, &full[stage], kb * BK, td.a_row, hint_a);
-        tma_load_2d(sB + stage * Cfg::B_STAGE, map_b, &full[stage], kb * BK, b_row, hint_b);
+        if (load_b) tma_load_2d(dst_b, map_b, &full[stage], kb * BK, b_row, hint_b);
       } else {
-        // both CTAs' bytes complete on the leader's barrier; the leader arms it for the pair
-        if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE);
+        // both CTAs' bytes complete on the leader's barrier; the leader arms it for the pair (the pair's
+        // tiles share b_row, so both CTAs agree on load_b)
+        if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * bytes);
         tma_load_2d_pair(sA + stage * A_STAGE, map_a, &full[stage], kb * BK, td.a_row, hint_a);
-        tma_load_2d_pair(sB + stage * Cfg::B_STAGE, map_b, &full[stage], kb * BK, b_row, hint_b);
+        if (load_b) tma_load_2d_pair(dst_b, map_b, &full[stage], kb * BK, b_row, hint_b);
       }
       if (++stage == Cfg::STAGES) {
         stage = 0;
@@ -262,7 +285,8 @@ __device__ __forceinline__ void producer_loop(const TileParams& p, uint8_t* sA, 
 
 template <int TN, int CG, int EB>
 __device__ __forceinline__ void mma_loop(const TileParams& p, uint8_t* sA, uint8_t* sB, uint64_t* full,
-                                         uint64_t* empty, uint64_t* tfull, uint64_t* tempty, uint32_t tmem) {
+                                         uint64_t* empty, uint64_t* tfull, uint64_t* tempty, uint32_t tmem,
+                                         uint64_t* bfree) {
   using Cfg = TileCfg<TN, CG, EB>;
   constexpr uint32_t idesc = make_idesc_bf16(BM * CG, TN);
   constexpr uint32_t idesc64 = make_idesc_bf16(BM * CG, 64);
@@ -276,7 +300,7 @@ __device__ __forceinline__ void mma_loop(const TileParams& p, uint8_t* sA, uint8
       mbar_wait(&full[stage], phase);
       tc_fence_after();
       const uint64_t ad = make_sdesc_sw128(smem_addr(sA + stage * A_STAGE));
-      const uint64_t bd = make_sdesc_sw128(smem_addr(sB + stage * Cfg::B_STAGE));
+      const uint64_t bd = make_sdesc_sw128(smem_addr(sB + (p.b_resident ? kb : int(stage)) * Cfg::B_STAGE));
 #pragma unroll
       for (int k = 0; k < BK / UMMA_K; ++k) {
         // +32 bytes per K step inside the 128B swizzle row (>>4 in the descriptor)
@@ -323,6 +347,16 @@ __device__ __forceinline__ void mma_loop(const TileParams& p, uint8_t* sA, uint8
       umma_commit(&tfull[acc]);  // accumulator complete
     else
       umma_commit_pair(&tfull[acc]);
+    if (p.b_resident) {
+      // the resident B rows are free once this tile's MMAs retire, if the CTA's next tile reads other rows
+      const int nt = t + int(gridDim.x);
+      if (nt < p.num_tiles && (p.tiles[nt].b_row != p.tiles[t].b_row || p.tiles[nt].b_src != p.tiles[t].b_src)) {
+        if constexpr (CG == 1)
+          umma_commit(bfree);
+        else
+          umma_commit_pair(bfree);
+      }
+    }
   }
 }
 
@@ -443,6 +477,58 @@ __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfu
         if (lane == 0) tma_store_wait_read<EB - 1>();
         __syncwarp();
       }
+      if (p.epi_fast && tma && !reduce_row && col + 64 <= td.cols) {
+        // fast path (every full 64-column chunk without epilogue reduction): both 32-column TMEM loads
+        // in flight before one wait, scale, pack, eight 16-byte swizzled st.shared, one TMA store
+        uint32_t v0[32], v1[32];
+        tmem_ld_32x32b_x32(taddr + col, v0);
+        tmem_ld_32x32b_x32(taddr + col + 32, v1);
+        tmem_ld_wait();
+        const uint32_t srow = smem_addr(buf + bi * EPI_BUF_BYTES) + uint32_t(lane) * 128u;
+        const uint32_t l7 = uint32_t(lane) & 7u;
+        if (scale != 1.0f) {
+          const uint64_t s2 = f32x2(scale, scale);
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            float x0 = __uint_as_float(v0[i]), y0 = __uint_as_float(v0[i + 1]);
+            float x1 = __uint_as_float(v1[i]), y1 = __uint_as_float(v1[i + 1]);
+            fmul2(x0, y0, s2);
+            fmul2(x1, y1, s2);
+            v0[i] = __float_as_uint(x0), v0[i + 1] = __float_as_uint(y0);
+            v1[i] = __float_as_uint(x1), v1[i + 1] = __float_as_uint(y1);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t* f = v0 + 8 * j;
+          st_shared_v4(srow + ((uint32_t(j) ^ l7) << 4),
+                       pack_bf16x2(__uint_as_float(f[0]), __uint_as_float(f[1])),
+                       pack_bf16x2(__uint_as_float(f[2]), __uint_as_float(f[3])),
+                       pack_bf16x2(__uint_as_float(f[4]), __uint_as_float(f[5])),
+                       pack_bf16x2(__uint_as_float(f[6]), __uint_as_float(f[7])));
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t* f = v1 + 8 * j;
+          st_shared_v4(srow + ((uint32_t(j + 4) ^ l7) << 4),
+                       pack_bf16x2(__uint_as_float(f[0]), __uint_as_float(f[1])),
+                       pack_bf16x2(__uint_as_float(f[2]), __uint_as_float(f[3])),
+                       pack_bf16x2(__uint_as_float(f[4]), __uint_as_float(f[5])),
+                       pack_bf16x2(__uint_as_float(f[6]), __uint_as_float(f[7])));
+        }
+        fence_async_shared();
+        __syncwarp();
+        if (lane == 0) {
+          if (p.out_plain && !signal && !remote)
+            tma_store_2d(map64, buf + bi * EPI_BUF_BYTES, td.c_col + col, td.c_row + quarter * 32);
+          else
+            tma_store_2d_hint(map64, buf + bi * EPI_BUF_BYTES, td.c_col + col, td.c_row + quarter * 32,
+                              signal ? hint_part : hint_out);
+          tma_store_commit();
+        }
+        bi = bi + 1 == EB ? 0 : bi + 1;
+        continue;
+      }
       // the two 32-column halves one after the other: one half's values live at a time
 #pragma unroll 1
       for (int h = 0; h < (live1 ? 2 : 1); ++h) {
@@ -463,8 +549,11 @@ __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfu
         fence_async_shared();
         __syncwarp();
         if (lane == 0) {
-          tma_store_2d_hint(live1 ? map64 : map32, buf + bi * EPI_BUF_BYTES, td.c_col + col,
-                            td.c_row + quarter * 32, signal ? hint_part : hint_out);
+          if (p.out_plain && !signal && !remote)
+            tma_store_2d(live1 ? map64 : map32, buf + bi * EPI_BUF_BYTES, td.c_col + col, td.c_row + quarter * 32);
+          else
+            tma_store_2d_hint(live1 ? map64 : map32, buf + bi * EPI_BUF_BYTES, td.c_col + col,
+                              td.c_row + quarter * 32, signal ? hint_part : hint_out);
           tma_store_commit();
         }
         bi = bi + 1 == EB ? 0 : bi + 1;
@@ -501,7 +590,8 @@ __global__ void __maxnreg__(MAX_REGS) tile_gemm_kernel(const __grid_constant__ T
   uint64_t* empty = full + Cfg::STAGES;
   uint64_t* tfull = empty + Cfg::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* bfree = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfree + 1);
   __shared__ uint32_t seen_flags[SEEN_WORDS];  // producer's record of flags already observed set
 
   const int warp = threadIdx.x / 32;
@@ -533,6 +623,7 @@ __global__ void __maxnreg__(MAX_REGS) tile_gemm_kernel(const __grid_constant__ T
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], EPI_THREADS * CG);
     }
+    mbar_init(bfree, 1);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -552,10 +643,10 @@ __global__ void __maxnreg__(MAX_REGS) tile_gemm_kernel(const __grid_constant__ T
   if (warp == 0) {
     if (lane == 0) {
       for (int i = 0; i < SEEN_WORDS; ++i) seen_flags[i] = 0;
-      producer_loop<TN, CG, EB>(p, sA, sB, full, empty, rank, seen_flags);
+      producer_loop<TN, CG, EB>(p, sA, sB, full, empty, rank, seen_flags, bfree);
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) mma_loop<TN, CG, EB>(p, sA, sB, full, empty, tfull, tempty, tmem);
+    if (lane == 0 && rank == 0) mma_loop<TN, CG, EB>(p, sA, sB, full, empty, tfull, tempty, tmem, bfree);
   } else {
     epilogue_loop<TN, CG, EB>(p, tfull, tempty, tmem, sEpi);
   }

@@ -24,13 +24,15 @@ import statistics
 import torch
 
 from . import ops
-from .lowering import F_RING, F_XFER, lower_ag
+from .lowering import F_RING, F_XFER
 from .routing import ExecutionPlan, GemmSpec, ScheduleKind, TransferSpec, build_plan
 from .simulator import SimResult, TaskSpan
 
 
-def _gemm_tile_groups(plan: ExecutionPlan, rank: int, low) -> list[tuple[int, list[int]]]:
-    """(task id, tile indices) per GemmSpec of this rank, matched by output rows."""
+def _gemm_tile_groups(plan: ExecutionPlan, rank: int, low, gathered: str = "A") -> list[tuple[int, list[int]]]:
+    """(task id, tile indices) per GemmSpec of this rank, matched by the plan rows a tile computes
+    (output rows for the gathered-A ops; output COLUMNS for the CP gathered-B op, whose plan rows are
+    kv tokens)."""
     tiles = low.tiles
     groups = []
     for t in plan.tasks:
@@ -41,8 +43,9 @@ def _gemm_tile_groups(plan: ExecutionPlan, rank: int, low) -> list[tuple[int, li
                 continue
             idx = [i for i, tl in enumerate(tiles) if tl.rows > 0]
         else:
+            pos = (lambda tl: tl.c_col) if gathered == "B" else (lambda tl: tl.c_row)
             idx = [i for i, tl in enumerate(tiles)
-                   if tl.rows > 0 and any(s <= tl.c_row < s + c for s, c in t.kind.rows)]
+                   if tl.rows > 0 and any(s <= pos(tl) < s + c for s, c in t.kind.rows)]
         groups.append((t.id, idx))
     return groups
 
@@ -60,58 +63,115 @@ def _transfer_flag(plan: ExecutionPlan, x: TransferSpec, rank: int) -> int:
     return F_XFER + x.round_idx * G + x.src
 
 
-def execute(plan: ExecutionPlan, a_shard: torch.Tensor, weight: torch.Tensor, group: "ops.FiccoGroup",
-            out: torch.Tensor | None = None, warmup: int = 2) -> tuple[torch.Tensor, SimResult]:
-    """Run an all-gather -> GEMM plan for this rank; returns (C, measured SimResult)."""
-    if plan.schedule is ScheduleKind.IDEAL:
-        raise ValueError("ideal is a pricing bound, not an executable schedule")
-    rank = group.rank
-    sc = plan.scenario
-    key = ("exec", sc.gemm.m, sc.gemm.n, sc.gemm.k, plan.schedule)
-    pl, low = group.plan(key, lambda: lower_ag(plan, rank, "A"))
-    if out is None:
-        out = torch.empty(sc.gemm.m, sc.gemm.n, dtype=torch.bfloat16, device=a_shard.device)
+def _timed_runs(pl, run, warmup: int, reps: int = 3) -> tuple[list[float], list[int], dict]:
+    """Run ``run()`` (one op through plan ``pl``) warmup + reps times with the kernel trace attached;
+    returns (seconds per rep, the last rep's trace, plan info)."""
     info = pl.info()
-    trace = torch.zeros(info["grid"] + 2 * info["tiles"], dtype=torch.int64, device=a_shard.device)
+    trace = torch.zeros(info["grid"] + 2 * info["tiles"], dtype=torch.int64, device="cuda")
     pl.set_trace(trace)
     try:
         for _ in range(warmup):
-            pl.run(a_shard, weight, out)
+            run()
         times = []
-        for _ in range(3):
+        for _ in range(reps):
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s.record()
-            pl.run(a_shard, weight, out)
+            run()
             e.record()
             e.synchronize()
             times.append(s.elapsed_time(e) * 1e-3)
-        group.comm.check()
     finally:
         tr = trace.cpu().tolist()
         pl.set_trace(None)
+    return times, tr, info
+
+
+def execute(plan: ExecutionPlan, a: torch.Tensor, weight: torch.Tensor, group: "ops.FiccoGroup",
+            out: torch.Tensor | None = None, warmup: int = 2, op: str = "ag", comm_agent: str = "dma",
+            scale: float | None = None) -> tuple[torch.Tensor, SimResult]:
+    """Run one rank's share of ``plan`` on the B200 and return (output, measured SimResult).
+
+    op 'ag'  all-gather -> GEMM: a = A shard [R, K], weight [N, K] (plan = the AG scenario);
+    op 'a2a' all-to-all -> expert GEMM: a = send buffer [M, K] (plan of an all_to_all scenario);
+    op 'cp'  CP KV all-gather -> QK^T: a = Q [Tq, d], weight = K shard [Tkv/G, d] (plan scenario
+             (M, N, K) = (Tkv, Tq, d), SURVEY.md §8a R2);
+    op 'rs'  GEMM -> reduce-scatter: a = A [M, Kg], weight [N, Kg] (plan = the schedule kind's AG plan
+             of the same scenario; the executed program is its adjoint, lowering.rs_pieces).
+    The timeline is in the simulator's schema (export_trace_csv, engine.py:310-318): one span per
+    GemmSpec task (first tile load start -> last tile stored; RS: per pushed piece / own reduce piece)
+    and per arriving transfer (AG/A2A/CP: kernel start -> first tile gated on its flag started).
+    """
+    if plan.schedule is ScheduleKind.IDEAL:
+        raise ValueError("ideal is a pricing bound, not an executable schedule")
+    if op not in ("ag", "a2a", "cp", "rs"):
+        raise ValueError(f"op must be 'ag', 'a2a', 'cp' or 'rs', got {op!r}")
+    rank, sc, kind = group.rank, plan.scenario, plan.schedule
+    M, N, K = sc.gemm.m, sc.gemm.n, sc.gemm.k
+    G = sc.n_gpus
+    if op == "rs":
+        pl, low, _ = ops.prepare_rs(group, M, K, N, kind, comm_agent=comm_agent)
+        shape, run_op = (M // G, N), "gemm_rs"
+    elif op == "cp":
+        pl, low, _ = ops.prepare_cp(group, N, K, M, kind, scale, comm_agent=comm_agent)
+        shape, run_op = (N, M), "cp_qk"
+    elif op == "a2a":
+        pl, low, _ = ops.prepare_a2a(group, M // G, K, N, kind, comm_agent=comm_agent)
+        shape, run_op = (M, N), "a2a_gemm"
+    else:
+        pl, low, _ = ops.prepare_ag(group, M // G, K, N, kind, comm_agent=comm_agent)
+        shape, run_op = (M, N), "ag_gemm"
+    if out is None:
+        out = torch.empty(*shape, dtype=torch.bfloat16, device=a.device)
+    times, tr, info = _timed_runs(pl, lambda: pl.run_op(run_op, a, weight, out), warmup)
+    group.comm.check()
     grid = info["grid"]
     t0 = min(tr[:grid])
     ready = [(tr[grid + 2 * i] - t0) * 1e-9 for i in range(info["tiles"])]
     done = [(tr[grid + 2 * i + 1] - t0) * 1e-9 for i in range(info["tiles"])]
     spans = []
-    for tid, idx in _gemm_tile_groups(plan, rank, low):
-        if idx:
-            spans.append(TaskSpan(tid, rank, "gemm", min(ready[i] for i in idx), max(done[i] for i in idx), 0.0))
-    # a transfer has landed no later than the first tile gated on its readiness flag started
-    # its loads (the tile producer's stamp is taken right after its first gate is satisfied)
-    first_gated: dict[int, float] = {}
-    for i, tl in enumerate(low.tiles):
-        if tl.rows > 0 and tl.flag >= 0:
-            for f in _first_gate(tl):
-                first_gated[f] = min(first_gated.get(f, ready[i]), ready[i])
-    for t in plan.tasks:
-        if isinstance(t.kind, TransferSpec) and t.kind.dst == rank:
-            end = first_gated.get(_transfer_flag(plan, t.kind, rank))
-            if end is not None:
-                spans.append(TaskSpan(t.id, rank, f"transfer[{t.kind.src}->{t.kind.dst}]", 0.0, end, 0.0))
+    if op == "rs":
+        spans = _rs_spans(sc, kind, rank, low, ready, done)
+    else:
+        for tid, idx in _gemm_tile_groups(plan, rank, low, "B" if op == "cp" else "A"):
+            if idx:
+                spans.append(TaskSpan(tid, rank, "gemm", min(ready[i] for i in idx), max(done[i] for i in idx), 0.0))
+        # a transfer has landed no later than the first tile gated on its readiness flag started
+        # its loads (the tile producer's stamp is taken right after its first gate is satisfied)
+        first_gated: dict[int, float] = {}
+        for i, tl in enumerate(low.tiles):
+            if tl.rows > 0 and tl.flag >= 0:
+                for f in _first_gate(tl):
+                    first_gated[f] = min(first_gated.get(f, ready[i]), ready[i])
+        for t in plan.tasks:
+            if isinstance(t.kind, TransferSpec) and t.kind.dst == rank:
+                end = first_gated.get(_transfer_flag(plan, t.kind, rank))
+                if end is not None:
+                    spans.append(TaskSpan(t.id, rank, f"transfer[{t.kind.src}->{t.kind.dst}]", 0.0, end, 0.0))
     spans.sort(key=lambda s: s.task_id)
-    res = SimResult(sc.name, plan.schedule, statistics.median(times), tuple(spans), {}, 0.0)
+    res = SimResult(sc.name, kind, statistics.median(times), tuple(spans), {}, 0.0)
     return out, res
+
+
+def _rs_spans(sc, kind, rank, low, ready, done) -> list[TaskSpan]:
+    """GEMM -> RS timeline: one span per piece of the schedule's adjoint routing (lowering.rs_pieces), in
+    emission order: 'gemm[->q]' for a remote owner's partial (its push starts when the span ends),
+    'reduce' for the own rows folded with the received partials. Task ids number the pieces."""
+    from .lowering import EPI_REDUCE, EPI_STORE_REMOTE, rs_pieces
+    order, _ = rs_pieces(sc, kind, rank)
+    R = sc.gemm.m // sc.n_gpus
+    spans = []
+    for pid, (remote, pc) in enumerate(order):
+        idx = []
+        for i, tl in enumerate(low.tiles):
+            if tl.rows <= 0 or (tl.mode == EPI_REDUCE) == remote:
+                continue
+            row = tl.c_row + (tl.chunk * R if tl.mode == EPI_STORE_REMOTE else 0) if remote else tl.c_row + rank * R
+            if pc.row0 <= row < pc.row0 + pc.nrows and pc.col0 <= tl.c_col < pc.col0 + pc.ncols:
+                idx.append(i)
+        if idx:
+            spans.append(TaskSpan(pid, rank, f"gemm[->{pc.owner}]" if remote else "reduce",
+                                  min(ready[i] for i in idx), max(done[i] for i in idx), 0.0))
+    return spans
 
 
 class MeasuredMakespan:

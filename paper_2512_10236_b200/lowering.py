@@ -444,21 +444,46 @@ def lower_ag(plan: ExecutionPlan, rank: int, gathered: str = "A", alpha: float =
             for m0, n0, rows in raster(frags, N, K, tn):
                 tiles.append(_tile(m0 - shift, n0, m0, n0, rows, min(tn, N - n0), flag, fmask, ks, kstride,
                                    a_src=int(local)))
-    for start, count in (frag_lists if gathered == "B" else []):
-        flag, fmask, ks, kstride = gate(start)
-        local = start // R == g  # rows of the own shard come from the call argument (alternate map)
-        shift = g * R if local else 0
-        if count % 32:
-            raise PlanError(f"gathered-B fragments must be multiples of 32 rows, got {count}")
-        # query-row-major inside the fragment: concurrently running tiles then write long
-        # contiguous row segments of the (HBM-bound) score matrix; 256-row steps keep CTA-pair
-        # partners (m0, m0 + 128) adjacent
+    if gathered == "B":
+        # kv column blocks ("units", one B tile each) in plan order, each gated by the flags of its rows
+        units = []
+        for fi, (start, count) in enumerate(frag_lists):
+            if count % 32:
+                raise PlanError(f"gathered-B fragments must be multiples of 32 rows, got {count}")
+            gt = gate(start)
+            local = start // R == g  # rows of the own shard come from the call argument (alternate map)
+            for n0 in range(start, start + count, tn):
+                units.append((n0, min(tn, start + count - n0), gt, local, g * R if local else 0, fi))
         step = TILE_M * cta_group
-        for mb, n0 in [(mb, n0) for mb in range(0, Q, step) for n0 in range(start, start + count, tn)]:
-            cols = min(tn, start + count - n0)
+        slots = B200_SMS // cta_group
+
+        def emit(unit, mb, pad=False):
+            n0, cols, (flag, fmask, ks, kstride), local, shift, _ = unit
             for m0 in range(mb, min(Q, mb + step), TILE_M):
-                tiles.append(_tile(m0, n0 - shift, m0, n0, min(TILE_M, Q - m0), cols, flag, fmask, ks,
-                                   kstride, b_src=int(local)))
+                tiles.append(_tile(m0, n0 - shift, m0, n0, 0 if pad else min(TILE_M, Q - m0), cols, flag, fmask,
+                                   ks, kstride, b_src=int(local)))
+
+        if len(units) >= slots:
+            # B-stationary: the persistent kernel hands pair-tile i to CTA pair i mod 74, so listing a
+            # wave of 74 units query-block by query-block gives every pair ONE kv block for all its query
+            # blocks. With K = d <= 256 the tile kernel then keeps those B rows in smem (b_resident) and
+            # streams only Q: half the L2->SM bytes of this store-bound op. A last partial wave is
+            # padded with load-only tiles (rows = 0) so the pair mapping stays aligned.
+            for w0 in range(0, len(units), slots):
+                wave = units[w0:w0 + slots]
+                for mb in range(0, Q, step):
+                    for u in wave:
+                        emit(u, mb)
+                    for _ in range(slots - len(wave)):
+                        emit(wave[0], mb, pad=True)
+        else:
+            # few units: query-row-major inside each fragment (concurrent tiles write long contiguous row
+            # segments of the score matrix); 256-row steps keep CTA-pair partners (m0, m0 + 128) adjacent
+            for fi in range(len(frag_lists)):
+                fr = [u for u in units if u[5] == fi]
+                for mb in range(0, Q, step):
+                    for u in fr:
+                        emit(u, mb)
 
     if cta_group == 2:
         low.tiles[:] = pair_tiles(low.tiles)

@@ -474,3 +474,40 @@ def test_op_boundary_validates_operands(lib):
         assert out.shape == (G * R, N)
     finally:
         grp.close()
+
+
+@pytest.mark.parametrize("m,n,k", [(512, 20480, 128), (384, 19200, 64), (256, 20480, 256), (640, 19968, 192)])
+@pytest.mark.parametrize("b_resident", ["1", "0"])
+def test_tile_gemm_short_k_b_stationary(lib, m, n, k, b_resident, monkeypatch):
+    """Short K (store-bound): the plain GEMM rasters B-stationary waves (each CTA pair keeps one column
+    block of B in smem for all of M, padded last wave) and the kernel reuses the resident B rows."""
+    monkeypatch.setenv("FICCO_B_RESIDENT", b_resident)
+    a = orc.seeded_inputs(16, 0, (m, k))
+    w = orc.seeded_inputs(16, 1, (n, k), "normal")
+    out = torch.empty(m, n, dtype=torch.bfloat16, device="cuda")
+    lib.gemm_bf16(_t(a), _t(w), out, alpha=0.5)
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(_np(out), 0.5 * (a @ w.T), rtol=RTOL, atol=ATOL)
+
+
+@pytest.mark.parametrize("kind", ["shard_overlap_p2p", "uniform_fused_1d", "hetero_unfused_1d", "serial"])
+@pytest.mark.parametrize("agent", ["dma", "core"])
+def test_cp_b_stationary_waves(lib, kind, agent):
+    """CP QK^T with more kv blocks than CTA pairs (80 units: one full wave of 74 + a padded partial wave):
+    the B-stationary tile order with resident K rows, gated per fragment, matches the oracle."""
+    from paper_2512_10236_b200 import ops
+    G, rank, d, Tq, Tkv = 4, 1, 128, 512, 20480
+    q = orc.seeded_inputs(17, 50, (Tq, d), "normal")
+    ks = [orc.seeded_inputs(17, p, (Tkv // G, d), "normal") for p in range(G)]
+    want, _ = orc.execute_cp_qk(q, ks, 1.0 / math.sqrt(d))
+    grp = ops.FiccoGroup.virtual_group(G, rank)
+    try:
+        _, low, _ = ops.prepare_cp(grp, Tq, d, Tkv, kind, comm_agent=agent)
+        assert sum(t.rows == 0 for t in low.tiles) > 0  # the padded wave is there
+        grp.load_peer_shards(low, [_t(x) for x in ks])
+        for _ in range(2):
+            out = ops.cp_kv_all_gather_qk(_t(q), _t(ks[rank]), kind=kind, group=grp, comm_agent=agent)
+            grp.comm.check()
+            np.testing.assert_allclose(_np(out), want, rtol=RTOL, atol=ATOL)
+    finally:
+        grp.close()

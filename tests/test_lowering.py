@@ -9,7 +9,7 @@ from paper_2512_10236_b200.lowering import (F_RING, F_XFER, W_L2_BYTES, lower_ag
                                             raster)
 from paper_2512_10236_b200.ops import _scenario
 from paper_2512_10236_b200 import routing
-from paper_2512_10236_b200.routing import ScheduleKind, build_plan
+from paper_2512_10236_b200.routing import PlanError, ScheduleKind, build_plan
 from paper_2512_10236_b200.runtime import EPI_REDUCE, EPI_STORE_REMOTE, EPI_STORE_SIGNAL
 
 AG_KINDS = ["serial", "shard_overlap_p2p", "uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d",
@@ -113,3 +113,68 @@ def test_empty_and_indivisible_shapes_raise_reference_errors(call):
     with pytest.raises(routing.PlanError):
         prep(2, 256, 256)          # 8 rows over G = 4: not divisible by G^2 = 16
     assert grp.comm is None        # nothing was allocated
+
+
+def test_rs_pieces_are_the_time_reversed_ag_schedules():
+    """lowering.rs_pieces: the adjoint routing of every kind (what is pushed, in which order, grouped how)."""
+    from paper_2512_10236_b200.lowering import RS_KINDS, rs_pieces
+    G, M, N, K = 4, 1024, 512, 256
+    R, r = M // G, M // (G * G)
+    sc = _scenario("x", M, N, K, G)
+    g = 1
+    for kind in RS_KINDS:
+        order, units = rs_pieces(sc, kind, g)
+        remote = [pc for rem, pc in order if rem]
+        own = [pc for rem, pc in order if not rem]
+        # every remote owner's rows x all columns exactly once; own rows exactly once
+        cover = np.zeros((M, N), dtype=int)
+        for pc in remote + own:
+            cover[pc.row0:pc.row0 + pc.nrows, pc.col0:pc.col0 + pc.ncols] += 1
+        assert (cover == 1).all(), kind
+        assert all(pc.owner == g for pc in own) and all(pc.owner != g for pc in remote)
+        assert sorted(map(id, [pc for u in units for pc in u])) == sorted(map(id, remote))
+        if kind is ScheduleKind.SERIAL:
+            assert len(units) == 1 and order[-1][0] is False
+        elif kind is ScheduleKind.SHARD_OVERLAP_P2P:  # ring reversed: owners g+1, g+2, ..., own last
+            assert [pc.owner for pc in remote] == [(g + i) % G for i in range(1, G)] and len(units) == G - 1
+            assert all(pc.nrows == R for pc in remote)
+        elif kind is ScheduleKind.UNIFORM_FUSED_2D:  # N blocks: round c = column block c, own slab after it
+            assert [pc.col0 for rem, pc in order if not rem] == [c * (N // G) for c in range(G)]
+            assert all(pc.nrows == R and pc.ncols == N // G for pc in remote + own)
+        else:
+            assert all(pc.nrows == r for pc in remote + own)
+            if kind is ScheduleKind.HETERO_UNFUSED_1D:
+                assert all(len(u) == 1 for u in units)
+            else:
+                assert all(len(u) == G - 1 for u in units)
+            if kind is ScheduleKind.UNIFORM_FUSED_1D:
+                assert [rem for rem, _ in order] == ([True] * (G - 1) + [False]) * G
+            else:
+                assert [rem for rem, _ in order] == [True] * (G * (G - 1)) + [False] * G
+
+
+def test_rs_2d_needs_column_blocks_of_32():
+    from paper_2512_10236_b200.lowering import rs_pieces
+    with pytest.raises(PlanError, match="N/G"):
+        rs_pieces(_scenario("x", 512, 544, 256, 4), ScheduleKind.UNIFORM_FUSED_2D, 0)
+    with pytest.raises(PlanError):
+        rs_pieces(_scenario("x", 512, 512, 256, 4), ScheduleKind.IDEAL, 0)
+
+
+def test_cp_b_stationary_order_keeps_one_kv_block_per_pair():
+    """C4's gathered-B tile list: pair-tile i goes to CTA pair i mod 74; every pair sees runs of 64 consecutive
+    tiles with one kv block (b_row) each, and the padded last wave has load-only tiles (rows = 0)."""
+    from paper_2512_10236_b200.lowering import lower_ag
+    sc = _scenario("cp", 131072, 16384, 128, 8)
+    low = lower_ag(build_plan(sc, ScheduleKind.SHARD_OVERLAP_P2P), 0, "B", alpha=0.1, other_rows=16384)
+    tiles = low.tiles
+    pairs = [(tiles[2 * i], tiles[2 * i + 1]) for i in range(len(tiles) // 2)]
+    assert all(a.b_row == b.b_row and a.c_col == b.c_col for a, b in pairs)
+    for p in (0, 37, 73):
+        mine = pairs[p::74]
+        changes = sum(1 for x, y in zip(mine, mine[1:]) if (x[0].b_row, x[0].b_src) != (y[0].b_row, y[0].b_src))
+        assert changes <= len(mine) // 64, (p, changes)
+    assert sum(t.rows == 0 for t in tiles) == 2 * 64 * (74 - 512 % 74)
+    real = [t for t in tiles if t.rows]
+    cover = {(t.c_row, t.c_col) for t in real}
+    assert len(cover) == len(real) == (16384 // 128) * (131072 // 256)

@@ -12,7 +12,10 @@ a G-rank job at BASELINE.json's full sizes:
 Checks, per rank and call:
 * the WHOLE output against a plain PyTorch fp32 reference of the same op (cuBLAS fp32,
   TF32 off): the owner's fp32 partial plus the peers' bf16-rounded partials, rank order
-  (the oracle's reduction order, oracle/ficco_oracle.py:execute_rs);
+  (the oracle's reduction order, oracle/ficco_oracle.py:execute_rs). Each peer's partial is
+  rounded to bf16 on its own GPU after ITS fp32 accumulation, so a reference that rounds a
+  differently-ordered fp32 sum may land one bf16 ulp of |P_g| away: the RS bound is therefore
+  elementwise atol*sqrt(G) + rtol * sum_g |P_g| (the magnitude of the terms, not of their sum);
 * sampled rows x columns against the numpy oracle's reduction (oracle.bf16_round, execute_rs's order);
 * AG: the gathered buffer bit-exact (torch.equal) against the concatenated shards.
 
@@ -72,17 +75,23 @@ def _worker(rank, world, port, q, what):
                 ops_g = [_rs_operands(torch, g, M, K, N, call) for g in range(world)]
                 # fp32 torch reference of this rank's shard (owner fp32 + peers' bf16 partials, rank order)
                 ref = ops_g[rank][0][own].float() @ ops_g[rank][1].float().T
+                mag = ref.abs()
                 for g in range(world):
                     if g != rank:
-                        ref += (ops_g[g][0][own].float() @ ops_g[g][1].float().T).to(torch.bfloat16).float()
+                        p_g = (ops_g[g][0][own].float() @ ops_g[g][1].float().T).to(torch.bfloat16).float()
+                        ref += p_g
+                        mag += p_g.abs()
                 # numpy oracle on sampled rows: execute_rs's formula on the owner's rows
                 cols = np.r_[0:32, N // 2:N // 2 + 16, N - 16:N]
                 a_s = [ops_g[g][0][own][sample].float().cpu().numpy() for g in range(world)]
                 w_s = [ops_g[g][1][cols].float().cpu().numpy() for g in range(world)]
                 want = a_s[rank] @ w_s[rank].T
+                mag_s = np.abs(want)
                 for g in range(world):
                     if g != rank:
-                        want = want + orc.bf16_round(a_s[g] @ w_s[g].T)
+                        p_g = orc.bf16_round(a_s[g] @ w_s[g].T)
+                        want = want + p_g
+                        mag_s = mag_s + np.abs(p_g)
                 a, w = ops_g[rank]
                 del ops_g
                 for agent in ("dma", "core"):
@@ -91,13 +100,14 @@ def _worker(rank, world, port, q, what):
                         out = ops.matmul_reduce_scatter(a, w, kind=kind, group=grp, comm_agent=agent)
                         grp.comm.check()
                         atol = 1e-2 * math.sqrt(world)
-                        if not torch.allclose(out.float(), ref, rtol=1.6e-2, atol=atol):
-                            err = (out.float() - ref).abs().max().item()
-                            errors.append(f"RS {kind} {agent} call {call}: output vs fp32 reference, max err {err}")
+                        excess = ((out.float() - ref).abs() - (atol + 1.6e-2 * mag)).max().item()
+                        if excess > 0:
+                            errors.append(f"RS {kind} {agent} call {call}: output vs fp32 reference exceeds the "
+                                          f"bound by {excess}")
                         got = out[sample][:, cols].float().cpu().numpy()
-                        if not np.allclose(got, want, rtol=1.6e-2, atol=atol):
+                        if (np.abs(got - want) > atol + 1.6e-2 * mag_s).any():
                             errors.append(f"RS {kind} {agent} call {call}: sampled rows vs the oracle")
-                del a, w, ref
+                del a, w, ref, mag
                 torch.cuda.empty_cache()
         else:  # C2-shaped AG at G = world
             M, N, K = 8192, 2 * 14336 // world, 4096

@@ -41,10 +41,6 @@ def main():
             plan = build_plan(sc, ScheduleKind(kind))
             _, low, _ = ops.prepare_ag(grp, R, K, N, kind)
             grp.load_peer_shards(low, shards)
-            # executor.execute lowers its own (cached) program; load the peers' shards into it too
-            key = ("exec", sc.gemm.m, sc.gemm.n, sc.gemm.k, plan.schedule)
-            _, elow = grp.plan(key, lambda: executor.lower_ag(plan, 0, "A"))
-            grp.load_peer_shards(elow, shards)
             _, measured = executor.execute(plan, shards[0], w, grp)
             simulated = simulate(plan, spec.machine, spec.topo, model)
             for tag, res in (("measured", measured), ("simulated", simulated)):
