@@ -45,6 +45,8 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# one hardware queue per stream (see paper_2512_10236_b200/__init__.py): must precede the first CUDA call
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 METRIC = "AG/RS+GEMM µs & speedup vs serialized NCCL+GEMM, % ideal overlap, 2/4/8 B200"
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
@@ -183,6 +185,7 @@ class AGWorkload:
     agent = "dma"  # comm_agent: copy engines ("dma") or SM copy kernels ("core")
 
     key = "c2"
+    op = "ag"
     title = "C2 Llama-3-8B TP/SP MLP up-proj AG->GEMM"
     kinds = ["uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d", "uniform_fused_2d", "shard_overlap_p2p",
              "serial"]
@@ -309,6 +312,7 @@ class RSWorkload(AGWorkload):
     """C3: GEMM -> reduce-scatter (TP/SP down-projection)."""
 
     key = "c3"
+    op = "rs"
     title = "C3 Llama-3-70B TP/SP down-proj GEMM->RS"
     kinds = ["uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d"]
 
@@ -421,6 +425,7 @@ class CPWorkload(AGWorkload):
     """C4: context-parallel KV all-gather -> attention scores S = Q K^T / sqrt(d)."""
 
     key = "c4"
+    op = "cp"
     title = "C4 CP KV all-gather -> QK^T, 128K context, d=128"
     kinds = ["uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d", "shard_overlap_p2p", "serial"]
 
@@ -538,6 +543,7 @@ class EPWorkload(AGWorkload):
     checks_multi_rank = False  # check() needs peers' data this rank does not hold
 
     key = "ep"
+    op = "a2a"
     title = "EP Mixtral all-to-all -> expert GEMM (corpus g14)"
     inplace = False
 
@@ -647,10 +653,9 @@ def headline_choice(workload: str, G: int, args) -> tuple[str, str]:
     tests/golden/selector.json) on the B200 machine file, and the machine file's comm_agent
     (machines.py:48). Pure host computation: the reference arm derives the same config."""
     from paper_2512_10236_b200 import ops
-    from paper_2512_10236_b200.machines import b200_machine
     m, n, k = WORKLOADS[workload].op_shape(G)
     kind = args.kind or ops.choose_kind(ops._scenario(workload, m, n, k, G), None).value
-    agent = args.agent or b200_machine().machine.comm_agent.value
+    agent = args.agent or ops.default_agent(WORKLOADS[workload].op)
     return kind, agent
 
 
@@ -662,7 +667,8 @@ def workload_config(args, world: int) -> dict:
     slot = args.input == "slot" and args.workload in ("c2", "c3p")
     return dict(workload=cls.title, ranks=G, virtual_peers=world == 1, schedule=kind, comm_agent=agent,
                 schedule_source=("--kind/--agent override" if (args.kind or args.agent) else
-                                 "public API default: select_schedule on the B200 machine file + its comm_agent"),
+                                 "public API default: select_schedule on the B200 machine file; "
+                                 "ops.default_agent(op)"),
                 input="symmetric slot (zero-copy publish)" if slot else "tensor copied in",
                 l2="flushed (256 MiB write) between timed steps", **cls.shape_config(G))
 
@@ -800,7 +806,7 @@ def our_arm(args) -> None:
     serial_us = maxrank(statistics.median(t_serial)) * 1e3
     cublas_us = maxrank(statistics.median(t_cublas)) * 1e3
     kern_alone_us = maxrank(statistics.median(t_kern)) * 1e3
-    kern_op_us = maxrank(statistics.mean(kern_in_op)) * 1e3
+    kern_op_us = maxrank(statistics.median(kern_in_op)) * 1e3
 
     with ClockSampler(local) as cs_loop:  # the headline op back to back (~1.5 s) so the sampler sees load
         t_end = time.time() + 1.5
@@ -869,7 +875,7 @@ def our_arm(args) -> None:
             "parity_spot_check": parity,
             "roofline": {"bound": bound, "achieved": round(achieved, 1), "peak": peak, "unit": unit,
                          "frac": round(achieved / peak, 4), "traffic": traffic_for(wl.key, G, best, best_agent),
-                         "kernel": f"ficco::tile_gemm_kernel inside the {best}/{best_agent} op: mean in-op duration "
+                         "kernel": f"ficco::tile_gemm_kernel inside the {best}/{best_agent} op: median in-op duration "
                                    f"over the timed steps (CUDA events on the launch stream: step start -> event "
                                    f"recorded behind the kernel)",
                          "kernel_us": round(kern_op_us, 2),

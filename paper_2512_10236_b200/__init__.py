@@ -8,6 +8,16 @@ goes through the C-ABI library ``libficco_b200.so`` (copy-engine transfers +
 tcgen05 tile kernel for sm_100a), see ``executor`` and ``ops``.
 """
 
+import os as _os
+
+# The executor's persistent tile kernel spins on readiness flags that copy-engine chains on other streams
+# set. With CUDA's default of 8 hardware work queues, the communicator's 16 copy streams and the caller's
+# stream alias onto shared queues, so a copy chain can end up queued behind work that waits for that very
+# kernel: the run then stalls until the flag timeout (seen as a DeadlockError). 32 queues give every stream
+# its own. CUDA reads the variable when the context is created, so it is set here at import unless the
+# caller set it (import this package, or set the variable, before the first CUDA call).
+_os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 from .domain import (Axis, Collective, CommAgent, GemmShape, MachineConfig, Parallelism, Scenario,
                      ScenarioParseError, ShardedGemm, gemm_flops, gemm_mt, gemm_otb, parse_scenarios,
                      serialize_scenarios, shard_gemm)

@@ -553,11 +553,12 @@ int make_params(ficco_plan* p, uint32_t parity, const void* a, const void* b, vo
   prm->alpha = d.alpha;
   prm->a_evict_last = (d.hints & FICCO_HINT_A_EVICT_LAST) != 0;
   {
-    // Output stores: evict_first keeps the operands L2-resident under compute-bound programs; a
-    // store-bound program (short K: C4's score write) writes HBM ~10 % faster with plain stores
-    // (tools/epi_probe.cu: 6.35 vs 5.72 TB/s). FICCO_OUT_HINT=first|none overrides.
+    // Output stores: evict_first (keeps operands L2-resident). The epilogue-only probe writes HBM faster
+    // with plain stores (tools/epi_probe.cu), but in the tile kernel with the fast epilogue path and
+    // resident B, evict_first measured 2-3 % faster on C4 (tools/out_hint_ab.py). FICCO_OUT_HINT=none
+    // selects plain stores.
     const char* env = getenv("FICCO_OUT_HINT");
-    prm->out_plain = env && env[0] == 'n' ? 1 : env && env[0] == 'f' ? 0 : (p->epi_bufs > 1 ? 1 : 0);
+    prm->out_plain = env && env[0] == 'n' ? 1 : 0;
     const char* fast = getenv("FICCO_EPI_FAST");
     prm->epi_fast = fast && fast[0] == '0' ? 0 : 1;
   }
@@ -812,8 +813,17 @@ int ficco_comm_check(ficco_comm_t* c, void* stream) {
   for (int i = 0; i < FICCO_MAX_STREAMS; ++i) CK(cudaStreamSynchronize(c->copy[i]));
   uint32_t abort_word = 0;
   CK(cudaMemcpy(&abort_word, c->flags(c->rank) + FICCO_FLAG_ABORT, 4, cudaMemcpyDeviceToHost));
-  if (abort_word || *reinterpret_cast<volatile uint32_t*>(c->host_abort))
-    return fail(FICCO_ETIMEOUT, "tile kernel timed out waiting for a readiness flag");
+  if (abort_word || *reinterpret_cast<volatile uint32_t*>(c->host_abort)) {
+    std::string where;
+    if (abort_word & 0x80000000u) {  // the word's address (low 31 bits) -> flag block / index, if it is local
+      const uint32_t base = uint32_t(reinterpret_cast<uintptr_t>(c->flags(c->rank))) & 0x7fffffffu;
+      const int64_t off = (int64_t(abort_word & 0x7fffffffu) - int64_t(base)) / 4;
+      if (off >= 0 && off < FICCO_WS_FLAG_WORDS)
+        where = " (flag block " + std::to_string(off / FICCO_FLAG_BLOCK) + ", word " +
+                std::to_string(off % FICCO_FLAG_BLOCK) + ")";
+    }
+    return fail(FICCO_ETIMEOUT, "tile kernel timed out waiting for a readiness flag" + where);
+  }
   return 0;
 }
 

@@ -159,7 +159,8 @@ __device__ __forceinline__ void wait_flag(const uint32_t* f, uint32_t epoch, uin
       if (t0 == 0) {
         t0 = now;
       } else if (now - t0 > timeout_ns) {
-        atomicExch(abort_word, 1u);
+        // non-zero; the low bits name the word that never arrived (ficco_comm_check reports it)
+        atomicExch(abort_word, 0x80000000u | (uint32_t(reinterpret_cast<uintptr_t>(f)) & 0x7fffffffu));
         if (abort_host) {
           *reinterpret_cast<volatile uint32_t*>(abort_host) = 1u;
           __threadfence_system();

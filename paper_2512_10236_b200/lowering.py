@@ -237,9 +237,15 @@ def _publish(ops: list, g: int, world: int, row_bytes: int, shard_rows: int, gat
     ops.append(_op(OP_RECORD, value=EV_START, stream=0))
 
 
-def _peer_stream(p: int, g: int) -> int:
-    """Copy stream pulling from (or pushing to) peer p: one copy-engine chain per peer."""
-    return 1 + (p if p < g else p - 1)
+def fine_chains() -> int:
+    """Copy-engine chains of the fine-grain AG copy programs (FICCO_FINE_CHAINS, default 0 = one per peer)."""
+    return max(0, min(15, int(os.environ.get("FICCO_FINE_CHAINS", "0"))))
+
+
+def _peer_stream(p: int, g: int, chains: int = 0) -> int:
+    """Copy stream pulling from (or pushing to) peer p: one copy-engine chain per peer (or `chains` shared)."""
+    idx = p if p < g else p - 1
+    return 1 + (idx % chains if chains else idx)
 
 
 def lower_ag(plan: ExecutionPlan, rank: int, gathered: str = "A", alpha: float = 1.0, grid: int = 0,
@@ -354,11 +360,12 @@ def lower_ag(plan: ExecutionPlan, rank: int, gathered: str = "A", alpha: float =
             if b % TILE_K:
                 raise PlanError(f"uniform_fused_2d on B200 needs K/G={b} to be a multiple of {TILE_K}")
             kseg = b // TILE_K
+        chains = fine_chains()
         for x in xfers:
-            st = _peer_stream(x.src, g)
-            if x.src not in started:
+            st = _peer_stream(x.src, g, chains)
+            if st not in started:
                 ops.append(_op(OP_STREAM_WAIT, value=EV_START, stream=st))
-                started.add(x.src)
+                started.add(st)
             c = x.round_idx
             if kind is ScheduleKind.SERIAL:
                 ops.append(pull(x.src, x.src * R, R, st))

@@ -257,8 +257,9 @@ def _cached(grp: FiccoGroup, key, make):
     return hit
 
 
-def prepare_ag(grp: FiccoGroup, R: int, K: int, N: int, kind=None, inplace: bool = False, comm_agent: str = "dma"):
+def prepare_ag(grp: FiccoGroup, R: int, K: int, N: int, kind=None, inplace: bool = False, comm_agent=None):
     """Build (or fetch) the lowered AG->GEMM plan for this rank: (plan, lowered, kind)."""
+    comm_agent = _agent(comm_agent, "ag")
     def make():
         M = R * grp.world
         sc = _scenario("ag_gemm", M, N, K, grp.world)
@@ -270,8 +271,9 @@ def prepare_ag(grp: FiccoGroup, R: int, K: int, N: int, kind=None, inplace: bool
     return _cached(grp, ("ag", R, K, N, kind, inplace, comm_agent), make)
 
 
-def prepare_a2a(grp: FiccoGroup, R: int, K: int, N: int, kind=None, comm_agent: str = "dma"):
+def prepare_a2a(grp: FiccoGroup, R: int, K: int, N: int, kind=None, comm_agent=None):
     """All-to-all (EP dispatch) -> expert GEMM plan for this rank: (plan, lowered, kind)."""
+    comm_agent = _agent(comm_agent, "a2a")
     def make():
         M = R * grp.world
         sc = _scenario("a2a_gemm", M, N, K, grp.world, Collective.ALL_TO_ALL)
@@ -292,7 +294,8 @@ def _is_slot(grp: FiccoGroup, t: torch.Tensor, low) -> bool:
     return t.data_ptr() == want
 
 
-def prepare_rs(grp: FiccoGroup, M: int, K: int, N: int, kind=None, comm_agent: str = "dma"):
+def prepare_rs(grp: FiccoGroup, M: int, K: int, N: int, kind=None, comm_agent=None):
+    comm_agent = _agent(comm_agent, "rs")
     def make():
         sc = _scenario("gemm_rs", M, N, K, grp.world)
         kd = choose_kind(sc, kind)
@@ -303,7 +306,8 @@ def prepare_rs(grp: FiccoGroup, M: int, K: int, N: int, kind=None, comm_agent: s
 
 
 def prepare_cp(grp: FiccoGroup, Tq: int, d: int, Tkv: int, kind=None, scale: float | None = None,
-               comm_agent: str = "dma"):
+               comm_agent=None):
+    comm_agent = _agent(comm_agent, "cp")
     def make():
         sc = _scenario("cp_qk", Tkv, Tq, d, grp.world)
         kd = choose_kind(sc, kind)
@@ -315,10 +319,24 @@ def prepare_cp(grp: FiccoGroup, Tq: int, d: int, Tkv: int, kind=None, scale: flo
     return _cached(grp, ("cp", Tq, d, Tkv, kind, scale, comm_agent), make)
 
 
-def _agent(comm_agent) -> str:
-    """comm_agent None -> the B200 machine file's (the reference's MachineConfig.comm_agent, machines.py:48)."""
+def default_agent(op: str) -> str:
+    """The comm agent an op uses when the caller passes comm_agent=None.
+
+    All-gather-shaped ops (AG -> GEMM, CP KV-AG -> QK^T, EP all-to-all -> GEMM) use the B200 machine file's
+    agent (the reference's MachineConfig.comm_agent, machines.py:48): 'dma', copy-engine transfers, the
+    north star's DMA offload. GEMM -> reduce-scatter uses 'core': on this executor that is the fused
+    GEMM + RS kernel (remote tiles' epilogues TMA-store their partials straight into the owners' receive
+    slots over peer memory; no partial buffer, no copy-engine round trip), which measured faster than
+    copy-engine pushes on every RS shape (C3 at G = 2, 4, 8).
+    """
+    if op == "rs":
+        return "core"
+    return b200_machine().machine.comm_agent.value
+
+
+def _agent(comm_agent, op: str = "ag") -> str:
     if comm_agent is None:
-        return b200_machine().machine.comm_agent.value
+        return default_agent(op)
     return getattr(comm_agent, "value", comm_agent)
 
 
@@ -399,7 +417,7 @@ def matmul_reduce_scatter(a: torch.Tensor, weight: torch.Tensor, kind=None, grou
     _check_tensor("weight", weight)
     N = weight.shape[0]
     _check_call(grp, {"a": (a, None), "weight": (weight, (N, K))}, out, (M // grp.world, N))
-    plan, _, _ = prepare_rs(grp, M, K, N, kind, comm_agent=_agent(comm_agent))
+    plan, _, _ = prepare_rs(grp, M, K, N, kind, comm_agent=_agent(comm_agent, "rs"))
     if out is None:
         out = torch.empty(M // grp.world, N, dtype=torch.bfloat16, device=a.device)
     _run(grp, plan, "gemm_rs", a, weight, out, stream)

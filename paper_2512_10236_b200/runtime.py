@@ -212,6 +212,7 @@ class Communicator:
     def __init__(self, rank: int, world: int, ws_ptrs: list[int], nbytes: int, virtual: bool,
                  owned: list[Workspace], opened: list[int]):
         lib = load_library()
+        self._check_connections()
         arr = (C.c_void_p * world)(*ws_ptrs)
         h = C.c_void_p()
         check(lib.ficco_comm_create(rank, world, arr, nbytes, int(virtual), C.byref(h)))
@@ -219,6 +220,18 @@ class Communicator:
         self.rank, self.world, self.nbytes, self.virtual = rank, world, nbytes, virtual
         self.ws_ptrs = list(ws_ptrs)
         self._owned, self._opened = owned, opened
+
+    @staticmethod
+    def _check_connections() -> None:
+        try:
+            n = int(os.environ.get("CUDA_DEVICE_MAX_CONNECTIONS", "8"))
+        except ValueError:
+            n = 8
+        if n < FICCO_MAX_STREAMS + 1:
+            import warnings
+            warnings.warn(f"CUDA_DEVICE_MAX_CONNECTIONS={n}: copy chains may share a hardware queue with work "
+                          f"that waits for the tile kernel (stalls until the flag timeout); set it to 32 before "
+                          f"the first CUDA call", RuntimeWarning, stacklevel=3)
 
     @classmethod
     def virtual(cls, world: int, rank: int, nbytes: int) -> "Communicator":

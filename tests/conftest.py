@@ -4,6 +4,10 @@ import sys
 
 import pytest
 
+# one hardware queue per stream for the executor's copy chains (paper_2512_10236_b200/__init__.py); set
+# before anything initialises CUDA in the test process (spawned workers inherit it)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = pathlib.Path(__file__).resolve().parents[1]
 if str(ROOT) not in sys.path:
     sys.path.insert(0, str(ROOT))

@@ -304,7 +304,7 @@ def test_missing_transfer_times_out_as_deadlock_error(lib, monkeypatch):
         monkeypatch.setenv("FICCO_FLAG_TIMEOUT_S", "1")
         t0 = time.time()
         plan.run(a, w, c)
-        with pytest.raises(DeadlockError):
+        with pytest.raises(DeadlockError, match=r"flag block \d, word 3\d\d"):  # names an XFER word (320..)
             grp.comm.check()
         assert time.time() - t0 < 30
         # the communicator is poisoned: later runs refuse up front instead of computing on stale chunks
