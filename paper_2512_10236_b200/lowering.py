@@ -202,6 +202,11 @@ def raster(frags: list[tuple[int, int]], N: int, K: int, tn: int) -> list[tuple[
     if N * K * ELT <= W_L2_BYTES:
         return [(m0, n0, rows) for m0, rows in blocks for n0 in range(0, N, tn)]
     per = max(2, (A_GROUP_BYTES // (K * ELT)) // TILE_M // 2 * 2)  # whole CTA pairs per group
+    # balance the groups over this run's blocks: a fragment of 1.25 groups as one group (its A slice a
+    # little over budget) rather than a full group plus a sliver that streams all of W again
+    ngroups = max(1, round(len(blocks) / per))
+    per = -(-len(blocks) // ngroups)
+    per += per % 2
     out = []
     for i in range(0, len(blocks), per):
         out += [(m0, n0, rows) for n0 in range(0, N, tn) for m0, rows in blocks[i:i + per]]

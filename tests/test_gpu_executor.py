@@ -149,3 +149,25 @@ def test_execute_cp_and_a2a_trace(mods, kind):
         _check_trace(res, plan, mods, len(res.timeline))
     finally:
         grp.close()
+
+
+def test_validate_heuristic_with_measured_makespans(mods):
+    """The reference's validate_heuristic (heuristic.py:74-115) with makespan_fn = executor.MeasuredMakespan
+    (real runs on this B200 instead of the simulator) on three small shapes: skinny, square-ish and M <= K."""
+    executor, machines, ops, routing, simulator = mods
+    from paper_2512_10236_b200 import selector
+    scen = [ops._scenario("skinny", 4096, 1024, 512, 8), ops._scenario("square", 2048, 2048, 2048, 8),
+            ops._scenario("m_le_k", 2048, 1024, 4096, 8)]
+    spec = machines.b200_machine()
+    mk = executor.MeasuredMakespan(warmup=2, reps=5)
+    rep = selector.validate_heuristic(scen, spec.machine, spec.topo, machines.b200_calibration(), t_ref=spec.t_ref,
+                                      makespan_fn=mk)
+    assert len(rep.verdicts) == 3
+    for sc, v in zip(scen, rep.verdicts):
+        assert v.chosen is selector.select_schedule(sc, spec.machine, spec.t_ref)
+        fine = {k: s for k, s in v.speedups.items() if k in routing.FINE_GRAIN_KINDS}
+        assert fine and all(0 < s < 10 for s in fine.values()), v.speedups
+        assert v.best is max(routing.FINE_GRAIN_KINDS, key=lambda k: v.speedups.get(k, float("-inf")))
+        assert v.agree == (v.chosen is v.best) and (v.regret == 0.0 if v.agree else 0.0 < v.regret < 1.0)
+    assert v.chosen is routing.ScheduleKind.UNIFORM_FUSED_2D  # M <= K
+    assert {k for (*_, k) in mk.cache} >= set(routing.FINE_GRAIN_KINDS) | {routing.ScheduleKind.SERIAL}

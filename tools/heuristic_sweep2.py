@@ -87,6 +87,9 @@ def main():
     corpus = parse_scenarios(resources.files("paper_2512_10236_b200.data").joinpath("scenarios_corpus.csv")
                              .read_text())
     scen += [s for s in list(corpus) + list(synthetic_grid()) if fits(s)]
+    only = os.environ.get("SWEEP_ONLY")
+    if only:
+        scen = [s for s in scen if s.name in only.split(",")]
     flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     flush = lambda: flush_buf.fill_(1)  # noqa: E731
     cache = {}
