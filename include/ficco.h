@@ -82,6 +82,9 @@ extern "C" {
 #define FICCO_OP_BARRIER 5      /* set byte `rank` of every rank's 8-byte barrier words at flag, wait for all, reset */
 #define FICCO_OP_RECORD 6       /* record event slot `value` on the stream */
 #define FICCO_OP_STREAM_WAIT 7  /* the stream waits for event slot `value` */
+#define FICCO_OP_REDUCE_MC 8    /* comm_agent = nvls: dst (height x width bytes, dst_pitch) := the in-switch sum
+                                   over every rank of the multicast view's rows at src (src_buf = MCV, src_pitch):
+                                   multimem.ld_reduce.add.acc::f32 on bf16x2, one bf16 rounding */
 #define FICCO_MAX_EVENTS 64
 
 /* buffer ids */
@@ -90,6 +93,8 @@ extern "C" {
 #define FICCO_BUF_B 2   /* call argument b */
 #define FICCO_BUF_C 3   /* call argument c */
 #define FICCO_BUF_WS 4  /* symmetric workspace of rank `peer` (local rank for dst) */
+#define FICCO_BUF_MC 5  /* comm_agent = nvls: this rank's memory bound to the multicast object (unicast VA) */
+#define FICCO_BUF_MCV 6 /* comm_agent = nvls: the multicast VA of that object (loads reduce over every rank) */
 
 /* epilogue modes of a tile */
 #define FICCO_EPI_STORE 0        /* out[c] = bf16(alpha * acc) */
@@ -244,6 +249,25 @@ int ficco_plan_info(ficco_plan_t* plan, int* n_tiles, int* grid, int* n_streams)
  * every later ficco_plan_run, so (event before the call -> event) times the in-op kernel alone
  * (bench.py's roofline). NULL detaches. Not available with FICCO_KERNEL_IN_GRAPH=1. */
 int ficco_plan_set_kernel_event(ficco_plan_t* plan, void* event);
+
+/* NVLS (NVLink SHARP) multicast for comm_agent = nvls GEMM -> reduce-scatter: each rank stores its whole
+ * partial into memory bound to one multicast object; an owner reads its rows through the multicast VA with
+ * multimem.ld_reduce, so NVSwitch returns the sum over every rank. Setup (collective, in order):
+ * rank 0 ficco_mc_create -> ficco_mc_export (POSIX fd, passed to the peers) -> peers ficco_mc_import ->
+ * every rank ficco_mc_add_device -> barrier -> every rank ficco_mc_bind -> ficco_comm_set_multicast.
+ * Where the driver cannot create multicast objects (no NVSwitch fabric access) these return FICCO_ENODEV
+ * with the driver's reason. */
+int ficco_mc_supported(int device, int* supported); /* 1 only if a multicast object can really be created */
+int ficco_mc_create(size_t bytes, int n_devices, void** mc, size_t* mapped_bytes);
+int ficco_mc_export(void* mc, int* fd);
+int ficco_mc_import(int fd, size_t mapped_bytes, void** mc);
+int ficco_mc_add_device(void* mc);
+int ficco_mc_bind(void* mc, void** uc_va, void** mc_va); /* back the object with this device's memory, map both */
+int ficco_mc_release(void* mc);                        /* unmap, unbind, free (after every rank stopped using it) */
+int ficco_comm_set_multicast(ficco_comm_t* comm, void* uc_va, void* mc_va, size_t bytes);
+/* dst[rows x cols bf16, ld_dst] := sum over the multicast object's devices of src[.., ld_src] (src = mc VA) */
+int ficco_mc_reduce_bf16(const void* mc_src, void* dst, int64_t rows, int64_t cols, int64_t ld_src, int64_t ld_dst,
+                         void* stream);
 
 /* stand-alone primitives (calibration, benchmarks) */
 int ficco_gemm_bf16(const void* a, const void* b, void* c, int64_t m, int64_t n, int64_t k, float alpha,

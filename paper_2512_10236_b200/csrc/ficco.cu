@@ -24,6 +24,7 @@
 
 #include "../../include/ficco.h"
 #include "copy_kernel.cuh"
+#include "multicast.cuh"
 #include "tile_kernel.cuh"
 
 namespace {
@@ -217,6 +218,11 @@ struct ficco_comm {
   // wait times out, so every later run can refuse a poisoned communicator without a device sync
   uint32_t* host_abort = nullptr;
   uint32_t* dev_host_abort = nullptr;
+  // comm_agent = nvls: this rank's memory bound to the group's multicast object (unicast VA) and the
+  // multicast VA (ficco_comm_set_multicast); null when the group has none
+  uint8_t* mc_uc = nullptr;
+  uint8_t* mc_va = nullptr;
+  size_t mc_bytes = 0;
   Driver* drv = nullptr;
   uint32_t* flags(int r) { return reinterpret_cast<uint32_t*>(ws[r]); }
   uint32_t* block(int r, uint32_t parity) { return flags(r) + parity * FICCO_FLAG_BLOCK; }
@@ -227,6 +233,7 @@ struct GraphInst {
   cudaGraphExec_t exec = nullptr;
   cudaGraphNode_t kernel = nullptr;
   std::vector<std::pair<cudaGraphNode_t, int>> user_copies;
+  std::vector<std::pair<cudaGraphNode_t, int>> user_reduces;  // REDUCE_MC kernel nodes writing a call argument
   const void* a = nullptr;
   const void* b = nullptr;
   void* c = nullptr;
@@ -241,6 +248,7 @@ struct ficco_plan {
   bool user_copies = false;  // some copy touches a call argument (kept out of the graph)
   cudaGraphNode_t captured_kernel = nullptr;
   std::vector<std::pair<cudaGraphNode_t, int>> captured_copies;  // (node, op index) touching call arguments
+  std::vector<std::pair<cudaGraphNode_t, int>> captured_reduces;
   unsigned long long* trace = nullptr;  // optional device timeline buffer
   cudaEvent_t kernel_event = nullptr;   // optional: recorded on the launch stream right after the tile kernel
   bool concurrent = true;               // false: copies complete before the kernel starts (profilers)
@@ -274,6 +282,8 @@ int resolve(ficco_comm* c, uint32_t parity, int buf, int peer, int64_t off, int6
       if (peer >= c->world) return fail(FICCO_EINVAL, "workspace peer out of range");
       base = c->ws[peer];
       break;
+    case FICCO_BUF_MC: base = c->mc_uc; break;
+    case FICCO_BUF_MCV: base = c->mc_va; break;
     default: return fail(FICCO_EINVAL, "bad buffer id " + std::to_string(buf));
   }
   if (!base) return fail(FICCO_EINVAL, "null buffer for id " + std::to_string(buf));
@@ -416,6 +426,30 @@ int enqueue_run(ficco_plan* p, uint32_t parity, const void* a, const void* b, vo
           if (op.value >= FICCO_MAX_EVENTS) return fail(FICCO_EINVAL, "event slot out of range");
           CK(cudaStreamWaitEvent(cs, cm->ev_pool[op.value], 0));
           break;
+        case FICCO_OP_REDUCE_MC: {
+          uint8_t *src, *dst;
+          int r = resolve(cm, parity, op.src_buf, -1, op.src_off, op.src_par, a, b, c, &src);
+          if (r) return r;
+          if ((r = resolve(cm, parity, op.dst_buf, op.dst_peer, op.dst_off, op.dst_par, a, b, c, &dst))) return r;
+          const int64_t rows = op.height <= 1 ? 1 : op.height;
+          const int64_t sp = rows > 1 ? op.src_pitch : op.width, dp = rows > 1 ? op.dst_pitch : op.width;
+          const int64_t vecs = rows * (op.width / 16);
+          const int grid = int(std::min<int64_t>(std::max<int64_t>(1, (vecs + 255) / 256), 4 * cm->sms));
+          ficco::mc_reduce_kernel<<<grid, 256, 0, cs>>>(src, dst, rows, op.width, sp, dp);
+          CK(cudaGetLastError());
+          if (is_user(op.dst_buf)) {  // remember the node: later runs re-point it at the caller's output
+            cudaStreamCaptureStatus st;
+            CK(cudaStreamIsCapturing(cs, &st));
+            if (st == cudaStreamCaptureStatusActive) {
+              const cudaGraphNode_t* deps = nullptr;
+              size_t nd = 0;
+              CK(cudaStreamGetCaptureInfo(cs, &st, nullptr, nullptr, &deps, &nd));
+              if (nd != 1) return fail(FICCO_ECUDA, "graph capture: reduce node not found");
+              p->captured_reduces.push_back({deps[0], int(&op - p->ops.data())});
+            }
+          }
+          break;
+        }
         default: return fail(FICCO_EINVAL, "bad copy opcode " + std::to_string(op.op));
       }
     }
@@ -537,6 +571,7 @@ int make_params(ficco_plan* p, uint32_t parity, const void* a, const void* b, vo
     prm->has_rem_map = 1;
   }
   prm->go_flag = d.go_flag;
+  prm->go_all = d.part.buf == FICCO_BUF_MC ? 1 : 0;  // nvls: the multicast-bound partials are read by peers
   prm->rs_target = d.rs_target > 0 ? uint32_t(d.rs_target) : 1u;
   prm->flags = cm->block(cm->rank, parity);
   prm->counters = cm->block(cm->rank, parity) + FICCO_FLAG_COUNTERS;
@@ -612,6 +647,7 @@ int build_graph(ficco_plan* p, uint32_t parity, const void* a, const void* b, vo
   CK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
   p->captured_kernel = nullptr;
   p->captured_copies.clear();
+  p->captured_reduces.clear();
   int r = enqueue_run(p, parity, a, b, c, cap, true, p->kernel_in_graph, launch_tiles);
   cudaGraph_t graph = nullptr;
   cudaError_t e = cudaStreamEndCapture(cap, &graph);
@@ -623,8 +659,10 @@ int build_graph(ficco_plan* p, uint32_t parity, const void* a, const void* b, vo
   if (e != cudaSuccess) return fail(FICCO_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e));
   gi.kernel = p->captured_kernel;
   gi.user_copies = p->captured_copies;
+  gi.user_reduces = p->captured_reduces;
   p->captured_kernel = nullptr;
   p->captured_copies.clear();
+  p->captured_reduces.clear();
   if (p->kernel_in_graph && p->n_tiles > 0 && !gi.kernel) {
     cudaGraphDestroy(graph);
     return fail(FICCO_ECUDA, "graph capture: kernel node not found");
@@ -667,6 +705,24 @@ int repoint_graph(ficco_plan* p, uint32_t parity, const void* a, const void* b, 
     if (r) return r;
     if ((r = resolve(p->comm, parity, op.dst_buf, op.dst_peer, op.dst_off, op.dst_par, a, b, c, &dst))) return r;
     CK(cudaGraphExecMemcpyNodeSetParams1D(gi.exec, nc.first, dst, src, size_t(op.width), cudaMemcpyDefault));
+  }
+  for (auto& nr : gi.user_reduces) {
+    const ficco_copy_op& op = p->ops[nr.second];
+    uint8_t *src, *dst;
+    int r = resolve(p->comm, parity, op.src_buf, -1, op.src_off, op.src_par, a, b, c, &src);
+    if (r) return r;
+    if ((r = resolve(p->comm, parity, op.dst_buf, op.dst_peer, op.dst_off, op.dst_par, a, b, c, &dst))) return r;
+    cudaKernelNodeParams kp{};
+    CK(cudaGraphKernelNodeGetParams(nr.first, &kp));
+    const int64_t rows = op.height <= 1 ? 1 : op.height;
+    int64_t width = op.width, sp = rows > 1 ? op.src_pitch : op.width, dp = rows > 1 ? op.dst_pitch : op.width;
+    const uint8_t* s8 = src;
+    uint8_t* d8 = dst;
+    int64_t rows_v = rows;
+    void* args[] = {&s8, &d8, &rows_v, &width, &sp, &dp};
+    kp.kernelParams = args;
+    kp.extra = nullptr;
+    CK(cudaGraphExecKernelNodeSetParams(gi.exec, nr.first, &kp));
   }
   gi.a = a;
   gi.b = b;
@@ -880,7 +936,14 @@ int ficco_plan_create(ficco_comm_t* c, const ficco_plan_desc* d, ficco_plan_t** 
   for (int i = 0; i < d->n_ops; ++i) {
     const ficco_copy_op& op = d->ops[i];
     if (op.stream < 0 || op.stream >= FICCO_MAX_STREAMS - 1) return fail(FICCO_EINVAL, "op stream out of range");
-    if (op.op < FICCO_OP_COPY || op.op > FICCO_OP_STREAM_WAIT) return fail(FICCO_EINVAL, "bad copy opcode");
+    if (op.op < FICCO_OP_COPY || op.op > FICCO_OP_REDUCE_MC) return fail(FICCO_EINVAL, "bad copy opcode");
+    if (op.op == FICCO_OP_REDUCE_MC && (op.src_buf != FICCO_BUF_MCV || op.width % 16 ||
+                                        (op.height > 1 && (op.src_pitch % 16 || op.dst_pitch % 16))))
+      return fail(FICCO_EINVAL, "REDUCE_MC reads the multicast view in 16-byte vectors");
+    if ((op.src_buf == FICCO_BUF_MC || op.src_buf == FICCO_BUF_MCV || op.dst_buf == FICCO_BUF_MC ||
+         op.dst_buf == FICCO_BUF_MCV) && !c->mc_va)
+      return fail(FICCO_ENODEV, "the plan uses the multicast (NVLS) workspace but the communicator has none "
+                                "(ficco_comm_set_multicast)");
     if ((op.op == FICCO_OP_SIGNAL || op.op == FICCO_OP_NOTIFY || op.op == FICCO_OP_WAIT ||
          op.op == FICCO_OP_BARRIER) && (op.flag < 0 || op.flag + 4 > FICCO_FLAG_BLOCK))
       return fail(FICCO_EINVAL, "op flag index out of range");
@@ -891,6 +954,10 @@ int ficco_plan_create(ficco_comm_t* c, const ficco_plan_desc* d, ficco_plan_t** 
   }
   if (has_remote && (d->recv.rows <= 0 || d->recv.ld <= 0))
     return fail(FICCO_EINVAL, "STORE_REMOTE tiles need the receive-slot geometry (recv)");
+  if (d->part.buf == FICCO_BUF_MC && (!c->mc_uc || d->part.off + d->part.rows * d->part.ld * 2 >
+                                                       int64_t(c->mc_bytes)))
+    return fail(FICCO_ENODEV, "partials in the multicast (NVLS) workspace need ficco_comm_set_multicast with "
+                              "enough bytes");
   auto* p = new ficco_plan();
   p->comm = c;
   p->desc = *d;
@@ -1165,6 +1232,192 @@ int ficco_gemm_bf16_cfg(const void* a, const void* b, void* c, int64_t m, int64_
 int ficco_gemm_bf16(const void* a, const void* b, void* c, int64_t m, int64_t n, int64_t k, float alpha, int grid,
                     void* stream) {
   return ficco_gemm_bf16_cfg(a, b, c, m, n, k, alpha, grid, 0, 0, stream);
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- NVLS multicast (comm_agent = nvls)
+
+namespace {
+struct McObj {
+  CUmemGenericAllocationHandle handle = 0;  // the multicast object
+  CUmemGenericAllocationHandle mem = 0;     // this device's backing memory
+  size_t bytes = 0, gran = 0;
+  CUdeviceptr uc = 0, va = 0;
+  bool owner_created = false;
+};
+
+int mc_fail(const ficco::McDriver* d, CUresult r, const char* what) {
+  const char* s = nullptr;
+  if (d->error_string) d->error_string(r, &s);
+  return fail(FICCO_ENODEV, std::string(what) + ": " + (s ? s : "CUresult " + std::to_string(int(r))) +
+                                " (NVLS multicast unavailable: the comm_agent='nvls' path needs NVSwitch "
+                                "multicast access on every rank's GPU)");
+}
+
+int mc_prop(const ficco::McDriver* d, size_t bytes, int ndev, CUmulticastObjectProp* prop, size_t* gran) {
+  *prop = CUmulticastObjectProp{};
+  prop->numDevices = unsigned(ndev);
+  prop->handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  prop->size = 2 << 20;
+  CUresult r = d->granularity(gran, prop, CU_MULTICAST_GRANULARITY_RECOMMENDED);
+  if (r != CUDA_SUCCESS || *gran == 0) return mc_fail(d, r, "cuMulticastGetGranularity");
+  prop->size = (bytes + *gran - 1) / *gran * *gran;
+  return 0;
+}
+}  // namespace
+
+extern "C" {
+
+int ficco_mc_supported(int device, int* supported) {
+  if (!supported) return fail(FICCO_EINVAL, "null argument");
+  *supported = 0;
+  const ficco::McDriver* d = ficco::mc_driver();
+  if (!d->ok) return 0;
+  int attr = 0;
+  if (d->dev_attr(&attr, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, device) != CUDA_SUCCESS || !attr) return 0;
+  // the attribute can be set where the fabric still refuses objects (e.g. a container without the
+  // NVSwitch fabric manager): try one
+  CUmulticastObjectProp prop;
+  size_t gran;
+  if (mc_prop(d, 2 << 20, 1, &prop, &gran)) return 0;
+  CUmemGenericAllocationHandle h;
+  if (d->create(&h, &prop) != CUDA_SUCCESS) return 0;
+  d->mem_release(h);
+  *supported = 1;
+  return 0;
+}
+
+int ficco_mc_create(size_t bytes, int n_devices, void** mc, size_t* mapped_bytes) {
+  if (!mc || n_devices < 1 || bytes == 0) return fail(FICCO_EINVAL, "bad multicast arguments");
+  const ficco::McDriver* d = ficco::mc_driver();
+  if (!d->ok) return fail(FICCO_ENODEV, "CUDA driver multicast entry points unavailable");
+  CUmulticastObjectProp prop;
+  auto* o = new McObj();
+  int r = mc_prop(d, bytes, n_devices, &prop, &o->gran);
+  if (!r) {
+    CUresult cr = d->create(&o->handle, &prop);
+    if (cr != CUDA_SUCCESS) r = mc_fail(d, cr, "cuMulticastCreate");
+  }
+  if (r) {
+    delete o;
+    return r;
+  }
+  o->bytes = prop.size;
+  o->owner_created = true;
+  if (mapped_bytes) *mapped_bytes = o->bytes;
+  *mc = o;
+  return 0;
+}
+
+int ficco_mc_export(void* mc, int* fd) {
+  auto* o = static_cast<McObj*>(mc);
+  if (!o || !fd) return fail(FICCO_EINVAL, "null argument");
+  const ficco::McDriver* d = ficco::mc_driver();
+  CUresult r = d->export_handle(fd, o->handle, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0);
+  return r == CUDA_SUCCESS ? 0 : mc_fail(d, r, "cuMemExportToShareableHandle");
+}
+
+int ficco_mc_import(int fd, size_t mapped_bytes, void** mc) {
+  if (!mc || fd < 0 || mapped_bytes == 0) return fail(FICCO_EINVAL, "bad multicast import arguments");
+  const ficco::McDriver* d = ficco::mc_driver();
+  if (!d->ok) return fail(FICCO_ENODEV, "CUDA driver multicast entry points unavailable");
+  auto* o = new McObj();
+  CUresult r = d->import_handle(&o->handle, reinterpret_cast<void*>(uintptr_t(fd)),
+                                CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR);
+  if (r != CUDA_SUCCESS) {
+    delete o;
+    return mc_fail(d, r, "cuMemImportFromShareableHandle");
+  }
+  o->bytes = mapped_bytes;
+  *mc = o;
+  return 0;
+}
+
+int ficco_mc_add_device(void* mc) {
+  auto* o = static_cast<McObj*>(mc);
+  if (!o) return fail(FICCO_EINVAL, "null multicast object");
+  const ficco::McDriver* d = ficco::mc_driver();
+  CUdevice dev;
+  CUresult r = d->ctx_get_device(&dev);
+  if (r == CUDA_SUCCESS) r = d->add_device(o->handle, dev);
+  return r == CUDA_SUCCESS ? 0 : mc_fail(d, r, "cuMulticastAddDevice");
+}
+
+int ficco_mc_bind(void* mc, void** uc_va, void** mc_va) {
+  auto* o = static_cast<McObj*>(mc);
+  if (!o || !uc_va || !mc_va) return fail(FICCO_EINVAL, "null argument");
+  const ficco::McDriver* d = ficco::mc_driver();
+  CUdevice dev;
+  CUresult r = d->ctx_get_device(&dev);
+  if (r != CUDA_SUCCESS) return mc_fail(d, r, "cuCtxGetDevice");
+  if (!o->gran) {
+    CUmulticastObjectProp prop;
+    if (int e = mc_prop(d, o->bytes, 1, &prop, &o->gran)) return e;
+  }
+  CUmemAllocationProp mp{};
+  mp.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  mp.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  mp.location.id = dev;
+  mp.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  if ((r = d->mem_create(&o->mem, o->bytes, &mp, 0)) != CUDA_SUCCESS) return mc_fail(d, r, "cuMemCreate");
+  if ((r = d->bind_mem(o->handle, 0, o->mem, 0, o->bytes, 0)) != CUDA_SUCCESS)
+    return mc_fail(d, r, "cuMulticastBindMem");
+  CUmemAccessDesc acc{};
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = dev;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  if ((r = d->reserve(&o->uc, o->bytes, o->gran, 0, 0)) != CUDA_SUCCESS ||
+      (r = d->map(o->uc, o->bytes, 0, o->mem, 0)) != CUDA_SUCCESS ||
+      (r = d->set_access(o->uc, o->bytes, &acc, 1)) != CUDA_SUCCESS ||
+      (r = d->reserve(&o->va, o->bytes, o->gran, 0, 0)) != CUDA_SUCCESS ||
+      (r = d->map(o->va, o->bytes, 0, o->handle, 0)) != CUDA_SUCCESS ||
+      (r = d->set_access(o->va, o->bytes, &acc, 1)) != CUDA_SUCCESS)
+    return mc_fail(d, r, "mapping the multicast workspace");
+  *uc_va = reinterpret_cast<void*>(o->uc);
+  *mc_va = reinterpret_cast<void*>(o->va);
+  return 0;
+}
+
+int ficco_mc_release(void* mc) {
+  auto* o = static_cast<McObj*>(mc);
+  if (!o) return 0;
+  const ficco::McDriver* d = ficco::mc_driver();
+  if (o->va) {
+    d->unmap(o->va, o->bytes);
+    d->addr_free(o->va, o->bytes);
+  }
+  if (o->uc) {
+    d->unmap(o->uc, o->bytes);
+    d->addr_free(o->uc, o->bytes);
+  }
+  if (o->mem) d->mem_release(o->mem);
+  if (o->handle) d->mem_release(o->handle);
+  delete o;
+  return 0;
+}
+
+int ficco_comm_set_multicast(ficco_comm_t* c, void* uc_va, void* mc_va, size_t bytes) {
+  if (!c) return fail(FICCO_EINVAL, "null comm");
+  c->mc_uc = static_cast<uint8_t*>(uc_va);
+  c->mc_va = static_cast<uint8_t*>(mc_va);
+  c->mc_bytes = uc_va && mc_va ? bytes : 0;
+  return 0;
+}
+
+int ficco_mc_reduce_bf16(const void* mc_src, void* dst, int64_t rows, int64_t cols, int64_t ld_src, int64_t ld_dst,
+                         void* stream) {
+  if (!mc_src || !dst || rows <= 0 || cols <= 0 || cols % 8 || ld_src % 8 || ld_dst % 8)
+    return fail(FICCO_EINVAL, "mc_reduce: 16-byte rows (cols, ld multiples of 8) required");
+  int dev, sms;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int64_t vecs = rows * (cols / 8);
+  const int grid = int(std::min<int64_t>(std::max<int64_t>(1, (vecs + 255) / 256), 4 * sms));
+  ficco::mc_reduce_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint8_t*>(mc_src), static_cast<uint8_t*>(dst), rows, cols * 2, ld_src * 2, ld_dst * 2);
+  CK(cudaGetLastError());
+  return 0;
 }
 
 }  // extern "C"

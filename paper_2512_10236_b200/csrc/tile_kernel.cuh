@@ -100,6 +100,7 @@ struct alignas(64) TileParams {
   int64_t ld_rem;
   int has_rem_map;
   int go_flag;             // STORE_REMOTE stores wait for local flag[go_flag] (<= 0: none)
+  int go_all;              // STORE_SIGNAL stores wait for it too (nvls: peers read the partials in place)
   uint32_t rs_target;      // REDUCE waits its peers' flags >= rs_target
   int has_out_map;
   int has_part_map;
@@ -452,7 +453,7 @@ __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfu
     const bool signal = td.mode == FICCO_EPI_STORE_SIGNAL;
     const bool remote = td.mode == FICCO_EPI_STORE_REMOTE;  // td.chunk = owner rank
     const bool reduce_row = epi_reduce && row_ok;
-    if (remote && !go_seen) {
+    if ((remote || (signal && p.go_all)) && !go_seen) {
       // the owners' receive slots are free once the DONE barrier of this run passed
       if (p.go_flag > 0 && lane == 0)
         wait_flag(p.flags + p.go_flag, p.epoch, p.abort_word, p.timeout_ns, p.abort_host);

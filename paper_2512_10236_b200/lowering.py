@@ -49,11 +49,12 @@ from dataclasses import dataclass, field
 from .domain import Collective, Scenario
 from .routing import (ExecutionPlan, GatherSpec, GemmSpec, PlanError, ScatterSpec, ScheduleKind, TransferSpec,
                       build_plan)
-from .runtime import (BUF_A, BUF_B, BUF_C, BUF_NONE, BUF_WS, EPI_REDUCE, EPI_STORE, EPI_STORE_REMOTE,
+from .runtime import (BUF_A, BUF_B, BUF_C, BUF_MC, BUF_MCV, BUF_NONE, BUF_WS, EPI_REDUCE, EPI_STORE, EPI_STORE_REMOTE,
                       EPI_STORE_SIGNAL, FICCO_HINT_A_EVICT_LAST, FICCO_HINT_B_EVICT_FIRST,
                       FICCO_HINT_CORE_COPIES,
                       FICCO_WS_DATA_OFFSET, MAX_RECV, OP_BARRIER, OP_COPY, OP_NOTIFY, OP_RECORD,
-                      OP_SIGNAL, OP_STREAM_WAIT, OP_WAIT, OP_WAIT_COUNTER, TILE_K, TILE_M, TILE_WIDTHS, CopyOp,
+                      OP_REDUCE_MC, OP_SIGNAL, OP_STREAM_WAIT, OP_WAIT, OP_WAIT_COUNTER, TILE_K, TILE_M,
+                      TILE_WIDTHS, CopyOp,
                       Operand, PlanDesc, Tile)
 
 # Flag words, relative to the run's parity block (one-shot words, include/ficco.h).
@@ -104,6 +105,7 @@ class Lowered:
     recv_off: int = 0
     recv_par: int = 0
     recv_slot: int = 0
+    mc_bytes: int = 0        # comm_agent = nvls: bytes of the multicast-bound partial buffer
     notes: dict = field(default_factory=dict)
 
 
@@ -623,6 +625,8 @@ def lower_rs(scenario: Scenario, kind: ScheduleKind, rank: int, grid: int = 0, v
     once that word reaches the sender's tile count (``rs_target``). Stores wait
     for the DONE barrier (flag F_GO), as the copy-engine pushes do.
     """
+    if getattr(comm_agent, "value", comm_agent) == "nvls":
+        return lower_rs_nvls(scenario, kind, rank, grid=grid, virtual=virtual, cta_group=cta_group)
     order, units = rs_pieces(scenario, kind, rank)
     g, G = rank, scenario.n_gpus
     M, N, K = scenario.gemm.m, scenario.gemm.n, scenario.gemm.k
@@ -727,4 +731,90 @@ def lower_rs(scenario: Scenario, kind: ScheduleKind, rank: int, grid: int = 0, v
         raise PlanError("too many ranks for the RS flag area")
     low.notes = {"kind": kind.value, "rank": g, "world": G, "op": "rs", "units": len(units),
                  "tiles_per_chunk": tiles_per_piece, "comm_agent": comm_agent}
+    return low
+
+
+def lower_rs_nvls(scenario: Scenario, kind: ScheduleKind, rank: int, grid: int = 0, virtual: bool = False,
+                  cta_group: int = DEFAULT_CTA_GROUP) -> Lowered:
+    """GEMM -> reduce-scatter with comm_agent='nvls' (in-switch reduction).
+
+    Every rank stores its WHOLE partial P_g [M, N] (bf16) into the memory it bound to the group's NVLS
+    multicast object (FICCO_BUF_MC); nothing is copied. When a piece's tiles are stored (unit counter) the
+    copy program notifies the piece's owner; once the owner has all G-1 notifications for its piece c and
+    its own tiles of that piece are stored, a REDUCE_MC op reads the rows through the multicast VA
+    (multimem.ld_reduce.add.acc::f32.bf16x2): the NVSwitch returns the sum over every rank's copy, fp32
+    accumulation of the G bf16 partials (the owner's included), one bf16 rounding, written to C. The tile
+    and notification order follow the schedule's adjoint routing (rs_pieces). Partial stores wait for the
+    DONE barrier (go flag), so a rank never overwrites partials an owner is still reducing from the
+    previous call. Needs real ranks on distinct GPUs with multicast access (no virtual peers).
+    """
+    if virtual:
+        raise PlanError("comm_agent='nvls' needs real ranks on distinct GPUs (one multicast object over their "
+                        "memory); virtual peers have none")
+    order, units = rs_pieces(scenario, kind, rank)
+    g, G = rank, scenario.n_gpus
+    M, N, K = scenario.gemm.m, scenario.gemm.n, scenario.gemm.k
+    _check_shape(M, N, K)
+    if N % 8:
+        raise PlanError("nvls reduce reads 16-byte vectors: N must be a multiple of 8")
+    if G - 1 > MAX_RECV or G > MAX_WORLD:
+        raise PlanError(f"at most {MAX_RECV + 1} ranks")
+    R = M // G
+    row_bytes = N * ELT
+    low = Lowered()
+    low.ws_bytes = FICCO_WS_DATA_OFFSET
+    low.mc_bytes = M * row_bytes
+    ops, tiles = low.ops, low.tiles
+
+    def slot_of(src: int, owner: int) -> int:
+        return src if src < owner else src - 1
+
+    def cdiv(a: int, b: int) -> int:
+        return -(-a // b)
+
+    own = [pc for rem, pc in order if not rem]
+    all_units = units + [[pc] for pc in own]  # own pieces are units too: their counter gates the reduce
+    unit_of = {pc: uid for uid, pcs in enumerate(all_units) for pc in pcs}
+    shape0 = order[0][1]
+    tn = choose_tile_n(lambda w: cdiv(len(order) * cdiv(shape0.nrows, TILE_M), cta_group) * cdiv(shape0.ncols, w),
+                       B200_SMS // cta_group)
+    tiles_per_piece = cdiv(shape0.nrows, TILE_M) * cdiv(shape0.ncols, tn)
+    for _, pc in order:
+        for m0 in range(pc.row0, pc.row0 + pc.nrows, TILE_M):
+            rows = min(TILE_M, pc.row0 + pc.nrows - m0)
+            for n0 in range(pc.col0, pc.col0 + pc.ncols, tn):
+                tiles.append(_tile(m0, n0, m0, n0, rows, min(tn, pc.col0 + pc.ncols - n0), mode=EPI_STORE_SIGNAL,
+                                   chunk=unit_of[pc]))
+    if cta_group == 2:
+        tiles[:] = pair_tiles(tiles)
+
+    # stream 0: DONE barrier -> release the partial stores (go) -> notify each owner as its units complete
+    ops.append(_op(OP_BARRIER, flag=F_DONE, stream=0))
+    ops.append(_op(OP_SIGNAL, flag=F_GO, stream=0))
+    for uid, pcs in enumerate(units):
+        ops.append(_op(OP_WAIT_COUNTER, flag=uid, value=tiles_per_piece * len(pcs), stream=0))
+        for pc in pcs:
+            ops.append(_op(OP_NOTIFY, peer=pc.owner, flag=F_RS + pc.idx * (G - 1) + slot_of(g, pc.owner), stream=0))
+    # stream 1: per own piece, wait for it everywhere, then reduce it in the switch into C
+    for pc in own:
+        ops.append(_op(OP_WAIT_COUNTER, flag=unit_of[pc], value=tiles_per_piece, stream=1))
+        for j in range(G - 1):
+            ops.append(_op(OP_WAIT, flag=F_RS + pc.idx * (G - 1) + j, stream=1))
+        ops.append(_op(OP_REDUCE_MC, src_buf=BUF_MCV, dst_buf=BUF_C, src_off=pc.row0 * row_bytes + pc.col0 * ELT,
+                       dst_off=(pc.row0 - g * R) * row_bytes + pc.col0 * ELT, width=pc.ncols * ELT, height=pc.nrows,
+                       src_pitch=row_bytes, dst_pitch=row_bytes, stream=1))
+
+    d = low.desc
+    d.a, d.b = _operand(BUF_A, M, K), _operand(BUF_B, N, K)
+    d.c = _operand(BUF_C, R, N)
+    d.part = _operand(BUF_MC, M, N, 0)
+    d.recv = _operand(BUF_NONE, 0, 0)
+    d.a2, d.b2 = _operand(BUF_NONE, 0, 0), _operand(BUF_NONE, 0, 0)
+    d.n_counters = len(all_units)
+    d.go_flag = F_GO
+    d.k, d.alpha, d.grid, d.tile_n, d.cta_group = K, 1.0, grid, tn, cta_group
+    if len(all_units) >= 4096 - 2048 or F_RS + G * (G - 1) >= 2048:
+        raise PlanError("too many push units / ranks for the flag block")
+    low.notes = {"kind": kind.value, "rank": g, "world": G, "op": "rs", "units": len(all_units),
+                 "tiles_per_chunk": tiles_per_piece, "comm_agent": "nvls"}
     return low

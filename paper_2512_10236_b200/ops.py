@@ -63,6 +63,7 @@ class FiccoGroup:
         self._fast: dict = {}
         self._ws_bytes = 0
         self.device: int | None = None  # CUDA device of the workspaces (set with the first workspace)
+        self._mc = None                  # runtime.Multicast: the NVLS workspace (comm_agent = nvls), lazily
 
     @classmethod
     def virtual_group(cls, world: int, rank: int = 0) -> "FiccoGroup":
@@ -86,6 +87,29 @@ class FiccoGroup:
             self.comm = Communicator.from_process_group(nbytes, self.pg)
         self._ws_bytes = nbytes
         self.device = torch.cuda.current_device()
+        if self._mc is not None:
+            self.comm.set_multicast(self._mc)
+
+    def ensure_multicast(self, nbytes: int) -> None:
+        """The group's NVLS multicast workspace of at least `nbytes` (collective in a distributed group;
+        raises NotImplementedError where the fabric gives no multicast objects)."""
+        if self.virtual:
+            raise PlanError("comm_agent='nvls' needs real ranks on distinct GPUs; virtual peers share one device")
+        if self._mc is not None and self._mc.nbytes >= nbytes:
+            return
+        from .runtime import Multicast
+        torch.cuda.synchronize()
+        self._barrier()
+        if self._mc is not None:
+            for plan, _ in self._plans.values():
+                plan.close()
+            self._plans.clear()
+            self._fast.clear()
+            self._mc.release()
+            self._mc = None
+        self._mc = Multicast(nbytes, self.pg)
+        if self.comm is not None:
+            self.comm.set_multicast(self._mc)
 
     def _barrier(self) -> None:
         if not self.virtual:
@@ -119,6 +143,8 @@ class FiccoGroup:
         if hit is None:
             low = make()
             self.ensure_workspace(low.ws_bytes)
+            if low.mc_bytes:
+                self.ensure_multicast(low.mc_bytes)
             hit = (Plan(self.comm, low.desc, low.ops, low.tiles), low)
             self._plans[key] = hit
         return hit
@@ -148,6 +174,10 @@ class FiccoGroup:
     def close(self) -> None:
         """Release the group (collective for distributed groups: every rank must call it)."""
         self._retire()
+        if self._mc is not None:
+            self._barrier()
+            self._mc.release()
+            self._mc = None
 
     # ---------------------------------------------------------------- virtual-mode data
     def load_peer_shards(self, low: Lowered, shards: list[torch.Tensor]) -> None:

@@ -29,9 +29,9 @@ FICCO_FLAG_ABORT = FICCO_WS_FLAG_WORDS - 1
 FICCO_FLAG_COUNTERS = 2048  # block-relative
 FICCO_MAX_STREAMS = 16
 
-OP_COPY, OP_SIGNAL, OP_NOTIFY, OP_WAIT, OP_WAIT_COUNTER, OP_BARRIER, OP_RECORD, OP_STREAM_WAIT = range(8)
+OP_COPY, OP_SIGNAL, OP_NOTIFY, OP_WAIT, OP_WAIT_COUNTER, OP_BARRIER, OP_RECORD, OP_STREAM_WAIT, OP_REDUCE_MC = range(9)
 FICCO_MAX_EVENTS = 64
-BUF_NONE, BUF_A, BUF_B, BUF_C, BUF_WS = 0, 1, 2, 3, 4
+BUF_NONE, BUF_A, BUF_B, BUF_C, BUF_WS, BUF_MC, BUF_MCV = 0, 1, 2, 3, 4, 5, 6
 FICCO_HINT_A_EVICT_LAST, FICCO_HINT_CORE_COPIES, FICCO_HINT_B_EVICT_FIRST = 1, 2, 4  # ficco_plan_desc.hints
 EPI_STORE, EPI_STORE_SIGNAL, EPI_REDUCE, EPI_STORE_REMOTE = 0, 1, 2, 3
 TILE_M, TILE_N, TILE_K = 128, 256, 64
@@ -45,7 +45,8 @@ EXPORTED = (
     "ficco_plan_create", "ficco_plan_destroy", "ficco_plan_run", "ficco_plan_run_parts",
     "ficco_gemm_bf16", "ficco_copy_batch", "ficco_plan_set_trace", "ficco_plan_info", "ficco_gemm_bf16_cfg", "ficco_occupy_sms",
     "ficco_timestamp", "ficco_ag_gemm", "ficco_a2a_gemm", "ficco_gemm_rs", "ficco_cp_qk",
-    "ficco_plan_set_kernel_event",
+    "ficco_plan_set_kernel_event", "ficco_mc_supported", "ficco_mc_create", "ficco_mc_export", "ficco_mc_import",
+    "ficco_mc_add_device", "ficco_mc_bind", "ficco_mc_release", "ficco_comm_set_multicast", "ficco_mc_reduce_bf16",
 )
 
 
@@ -126,6 +127,15 @@ def load_library(path: os.PathLike | str | None = None) -> C.CDLL:
             "ficco_timestamp": ([vp, vp], i32),
             "ficco_plan_set_trace": ([vp, vp], i32),
             "ficco_plan_set_kernel_event": ([vp, vp], i32),
+            "ficco_mc_supported": ([i32, C.POINTER(i32)], i32),
+            "ficco_mc_create": ([sz, i32, C.POINTER(vp), C.POINTER(sz)], i32),
+            "ficco_mc_export": ([vp, C.POINTER(i32)], i32),
+            "ficco_mc_import": ([i32, sz, C.POINTER(vp)], i32),
+            "ficco_mc_add_device": ([vp], i32),
+            "ficco_mc_bind": ([vp, C.POINTER(vp), C.POINTER(vp)], i32),
+            "ficco_mc_release": ([vp], i32),
+            "ficco_comm_set_multicast": ([vp, vp, vp, sz], i32),
+            "ficco_mc_reduce_bf16": ([vp, vp, i64, i64, i64, i64, vp], i32),
             "ficco_plan_info": ([vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)], i32),
         }
         for name, (args, res) in sig.items():
@@ -146,6 +156,8 @@ def check(rc: int) -> None:
         raise ValueError(msg)
     if rc == -3:
         raise DeadlockError(msg)
+    if rc == -4:
+        raise NotImplementedError(msg)  # FICCO_ENODEV: the device / fabric lacks what the op needs
     raise RuntimeError(f"libficco_b200 error {rc}: {msg}")
 
 
@@ -196,6 +208,70 @@ def exchange_handles(handle: bytes, group=None) -> list[bytes]:
     if any(not isinstance(h, bytes) or len(h) != len(handle) for h in handles):
         raise RuntimeError("workspace handle exchange returned malformed handles")
     return handles
+
+
+def multicast_supported(device: int = 0) -> bool:
+    """Can this process create an NVLS multicast object on `device` (ficco_mc_supported)?"""
+    ok = C.c_int()
+    check(load_library().ficco_mc_supported(device, C.byref(ok)))
+    return bool(ok.value)
+
+
+class Multicast:
+    """One rank's share of a group-wide NVLS multicast workspace (include/ficco.h setup order): rank 0
+    creates the object and exports it as a POSIX fd; the peers duplicate that fd out of rank 0's process
+    (pidfd_getfd; the ranks run as the same user on one node) and import it; every rank adds its device,
+    meets the others, binds `nbytes` of its own HBM and maps the unicast and multicast views."""
+
+    def __init__(self, nbytes: int, group=None):
+        import torch.distributed as dist
+        lib = load_library()
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        h, mapped, fd = C.c_void_p(), C.c_size_t(), C.c_int(-1)
+        err = None
+        if rank == 0:
+            try:
+                check(lib.ficco_mc_create(nbytes, world, C.byref(h), C.byref(mapped)))
+                check(lib.ficco_mc_export(h, C.byref(fd)))
+            except Exception as exc:  # every rank must learn about it, or the peers would wait forever
+                err = str(exc)
+        info = [None] * world
+        dist.all_gather_object(info, (os.getpid(), fd.value, mapped.value, err), group=group)
+        pid0, fd0, mapped0, err0 = info[0]
+        if err0:
+            raise NotImplementedError(err0)
+        if rank != 0:
+            fd_local = _pidfd_getfd(pid0, fd0)
+            check(lib.ficco_mc_import(fd_local, mapped0, C.byref(h)))
+            os.close(fd_local)
+        dist.barrier(group=group)
+        check(lib.ficco_mc_add_device(h))
+        dist.barrier(group=group)  # every device added before anyone binds memory
+        uc, mc = C.c_void_p(), C.c_void_p()
+        check(lib.ficco_mc_bind(h, C.byref(uc), C.byref(mc)))
+        dist.barrier(group=group)
+        if rank == 0:
+            os.close(fd.value)
+        self.handle, self.uc, self.va, self.nbytes = h.value, uc.value, mc.value, mapped0
+
+    def release(self) -> None:
+        if self.handle:
+            check(load_library().ficco_mc_release(C.c_void_p(self.handle)))
+            self.handle = None
+
+
+def _pidfd_getfd(pid: int, fd: int) -> int:
+    """Duplicate file descriptor `fd` of process `pid` into this process (Linux pidfd_open + pidfd_getfd)."""
+    libc = C.CDLL(None, use_errno=True)
+    pidfd = os.pidfd_open(pid)
+    try:
+        new = libc.syscall(438, pidfd, fd, 0)  # SYS_pidfd_getfd
+        if new < 0:
+            raise NotImplementedError(f"pidfd_getfd failed (errno {C.get_errno()}): cannot share the multicast "
+                                      f"handle between ranks")
+        return new
+    finally:
+        os.close(pidfd)
 
 
 class Communicator:
@@ -267,6 +343,14 @@ class Communicator:
     def check(self, stream=None) -> None:
         """Synchronise and raise DeadlockError if a kernel timed out on a flag."""
         check(load_library().ficco_comm_check(C.c_void_p(self.handle), C.c_void_p(_stream_ptr(stream))))
+
+    def set_multicast(self, mc: "Multicast | None") -> None:
+        """Attach (or detach) the group's NVLS multicast workspace (comm_agent = nvls plans)."""
+        if mc is None:
+            check(load_library().ficco_comm_set_multicast(C.c_void_p(self.handle), None, None, 0))
+        else:
+            check(load_library().ficco_comm_set_multicast(C.c_void_p(self.handle), C.c_void_p(mc.uc),
+                                                          C.c_void_p(mc.va), mc.nbytes))
 
     def set_flags(self, first: int, count: int, value: int, stream=None) -> None:
         check(load_library().ficco_comm_set_flags(C.c_void_p(self.handle), first, count, value,

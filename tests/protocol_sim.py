@@ -27,10 +27,12 @@ import random
 
 import numpy as np
 
-from paper_2512_10236_b200.runtime import (BUF_A, BUF_B, BUF_C, BUF_NONE, BUF_WS, EPI_REDUCE, EPI_STORE,
+from paper_2512_10236_b200.runtime import (BUF_A, BUF_B, BUF_C, BUF_MC, BUF_MCV, BUF_NONE, BUF_WS, EPI_REDUCE,
+                                           EPI_STORE,
                                            EPI_STORE_REMOTE, EPI_STORE_SIGNAL, FICCO_FLAG_BLOCK, FICCO_FLAG_COUNTERS,
                                            FICCO_FLAG_RUN_LOCAL, OP_BARRIER, OP_COPY, OP_NOTIFY, OP_RECORD,
-                                           OP_SIGNAL, OP_STREAM_WAIT, OP_WAIT, OP_WAIT_COUNTER, TILE_K)
+                                           OP_REDUCE_MC, OP_SIGNAL, OP_STREAM_WAIT, OP_WAIT, OP_WAIT_COUNTER,
+                                           TILE_K)
 
 
 class Deadlock(AssertionError):
@@ -53,9 +55,10 @@ def round_bf16(x: np.ndarray) -> np.ndarray:
 
 
 class Rank:
-    def __init__(self, g: int, ws_bytes: int):
+    def __init__(self, g: int, ws_bytes: int, mc_bytes: int = 0):
         self.g = g
         self.ws = np.zeros(ws_bytes, dtype=np.uint8)
+        self.mc = np.zeros(mc_bytes, dtype=np.uint8)  # memory bound to the NVLS multicast object
         self.flags = self.ws[: 16384 * 4].view(np.uint32)
 
     def block(self, parity: int) -> np.ndarray:
@@ -68,7 +71,7 @@ class World:
     def __init__(self, lowered: list, args_per_run: list, seed: int = 0):
         self.low = lowered
         self.G = len(lowered)
-        self.ranks = [Rank(g, lowered[g].ws_bytes) for g in range(self.G)]
+        self.ranks = [Rank(g, lowered[g].ws_bytes, getattr(lowered[g], "mc_bytes", 0)) for g in range(self.G)]
         self.args = args_per_run  # args[run][rank] = dict(a=ndarray uint16 2D, b=..., c=...)
         self.rng = random.Random(seed)
         self.steps = 0
@@ -77,6 +80,8 @@ class World:
     def _buf(self, rank: int, run: int, buf: int, peer: int) -> np.ndarray:
         if buf == BUF_WS:
             return self.ranks[rank if peer < 0 else peer].ws
+        if buf == BUF_MC:
+            return self.ranks[rank].mc
         key = {BUF_A: "a", BUF_B: "b", BUF_C: "c"}[buf]
         return self.args[run][rank][key].view(np.uint8).reshape(-1)
 
@@ -91,6 +96,19 @@ class World:
         dp = op.dst_pitch if h > 1 else op.width
         for i in range(h):
             dst[do + i * dp: do + i * dp + op.width] = src[so + i * sp: so + i * sp + op.width]
+
+    def _reduce_mc(self, rank: int, run: int, op) -> None:
+        """NVSwitch in-switch reduction: every rank's multicast-bound copy of the rows, fp32 sum, one bf16
+        rounding (multimem.ld_reduce.add.acc::f32.bf16x2)."""
+        dst = self._buf(rank, run, op.dst_buf, op.dst_peer)
+        h = max(1, op.height)
+        for i in range(h):
+            so = op.src_off + i * op.src_pitch
+            acc = np.zeros(op.width // 2, dtype=np.float32)
+            for rk in self.ranks:
+                acc = acc + bits_f32(rk.mc[so:so + op.width].view(np.uint16))
+            do = op.dst_off + i * op.dst_pitch
+            dst[do:do + op.width] = bf16_bits(round_bf16(acc)).view(np.uint8)
 
     def _operand(self, rank: int, run: int, od) -> np.ndarray | None:
         if od.buf == BUF_NONE:
@@ -252,6 +270,8 @@ class World:
             elif op.op == OP_STREAM_WAIT:
                 if op.value in st["events"]:
                     acts.append(adv)
+            elif op.op == OP_REDUCE_MC:
+                acts.append(lambda op=op, adv=adv: (self._reduce_mc(g, run, op), adv()))
             else:
                 raise AssertionError(f"unknown op {op.op}")
         num_kb = -(-self.low[g].desc.k // TILE_K)
@@ -272,5 +292,8 @@ class World:
                             continue
                     if t.mode == EPI_STORE_REMOTE and d.go_flag > 0 and not rk.block(par)[d.go_flag]:
                         continue  # the epilogue holds its stores until the DONE barrier passed
+                    if (t.mode == EPI_STORE_SIGNAL and d.part.buf == BUF_MC and d.go_flag > 0
+                            and not rk.block(par)[d.go_flag]):
+                        continue  # nvls: peers read the multicast-bound partials in place
                     acts.append(lambda x=x, t=t: (self._run_tile(g, run, t), x.__setitem__("done", True)))
         return acts

@@ -511,3 +511,41 @@ def test_cp_b_stationary_waves(lib, kind, agent):
             np.testing.assert_allclose(_np(out), want, rtol=RTOL, atol=ATOL)
     finally:
         grp.close()
+
+
+def test_nvls_fails_cleanly_or_reduces_in_the_switch(lib):
+    """comm_agent='nvls' (in-switch reduction). Virtual peers share one device, so the
+    op raises PlanError there. The multicast primitives either report the fabric's refusal as
+    FICCO_ENODEV (NotImplementedError) or, where a one-device multicast object can be created, the
+    multimem.ld_reduce kernel returns exactly the bound memory (the sum over one device)."""
+    from paper_2512_10236_b200 import ops
+    from paper_2512_10236_b200.routing import PlanError
+    import ctypes as C
+    grp = ops.FiccoGroup.virtual_group(4, 0)
+    try:
+        with pytest.raises(PlanError, match="real ranks"):
+            ops.prepare_rs(grp, 128 * 16, 256, 512, "hetero_fused_1d", comm_agent="nvls")
+    finally:
+        grp.close()
+    L = lib.load_library()
+    if not lib.multicast_supported(0):
+        h, mapped = C.c_void_p(), C.c_size_t()
+        with pytest.raises(NotImplementedError, match="NVLS multicast unavailable"):
+            lib.check(L.ficco_mc_create(64 << 20, 1, C.byref(h), C.byref(mapped)))
+        return
+    h, mapped = C.c_void_p(), C.c_size_t()
+    lib.check(L.ficco_mc_create(8 << 20, 1, C.byref(h), C.byref(mapped)))
+    try:
+        lib.check(L.ficco_mc_add_device(h))
+        uc, va = C.c_void_p(), C.c_void_p()
+        lib.check(L.ficco_mc_bind(h, C.byref(uc), C.byref(va)))
+        rows, cols = 512, 1024
+        src = ops._wrap_device_ptr(uc.value, (rows, cols), torch.bfloat16)
+        src.copy_(_t(orc.seeded_inputs(18, 0, (rows, cols))))
+        out = torch.empty(rows, cols, dtype=torch.bfloat16, device="cuda")
+        lib.check(L.ficco_mc_reduce_bf16(va, C.c_void_p(out.data_ptr()), rows, cols, cols, cols,
+                                         C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        torch.cuda.synchronize()
+        assert torch.equal(out, src)
+    finally:
+        lib.check(L.ficco_mc_release(h))

@@ -178,3 +178,28 @@ def test_cp_b_stationary_order_keeps_one_kv_block_per_pair():
     real = [t for t in tiles if t.rows]
     cover = {(t.c_row, t.c_col) for t in real}
     assert len(cover) == len(real) == (16384 // 128) * (131072 // 256)
+
+
+@pytest.mark.parametrize("kind", ["serial", "shard_overlap_p2p", "uniform_fused_1d", "hetero_fused_1d",
+                                  "hetero_unfused_1d", "uniform_fused_2d"])
+def test_rs_nvls_lowering(kind):
+    """comm_agent='nvls': every tile stores its partial into the multicast-bound buffer (no copies, no REDUCE
+    tiles); the copy program notifies owners and reduces each own piece once through the multicast view."""
+    from paper_2512_10236_b200.lowering import rs_pieces
+    from paper_2512_10236_b200.runtime import BUF_C, BUF_MC, BUF_MCV, OP_COPY, OP_NOTIFY, OP_REDUCE_MC
+    G, M, N, K = 4, 2048, 512, 256
+    sc = _scenario("x", M, N, K, G)
+    for rank in (0, 3):
+        low = lower_rs(sc, ScheduleKind(kind), rank, comm_agent="nvls")
+        assert low.mc_bytes == M * N * 2 and low.desc.part.buf == BUF_MC and low.desc.go_flag > 0
+        assert all(t.mode == EPI_STORE_SIGNAL for t in low.tiles)
+        assert not any(op.op == OP_COPY for op in low.ops)
+        order, _ = rs_pieces(sc, ScheduleKind(kind), rank)
+        red = [op for op in low.ops if op.op == OP_REDUCE_MC]
+        own = [pc for rem, pc in order if not rem]
+        assert len(red) == len(own) and all(op.src_buf == BUF_MCV and op.dst_buf == BUF_C for op in red)
+        assert sum(op.width * op.height for op in red) == (M // G) * N * 2  # every own element reduced once
+        notified = [op.peer for op in low.ops if op.op == OP_NOTIFY]
+        assert sorted(notified) == sorted(pc.owner for rem, pc in order if rem)
+    with pytest.raises(PlanError, match="virtual"):
+        lower_rs(sc, ScheduleKind(kind), 0, virtual=True, comm_agent="nvls")

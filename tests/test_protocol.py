@@ -108,7 +108,7 @@ def test_a2a_protocol(kind, G, cta_group):
 @pytest.mark.parametrize("kind", AG_KINDS)
 @pytest.mark.parametrize("G", [2, 3, 4])
 @pytest.mark.parametrize("cta_group", [1, 2])
-@pytest.mark.parametrize("agent", ["dma", "core"])
+@pytest.mark.parametrize("agent", ["dma", "core", "nvls"])
 def test_rs_protocol(kind, G, cta_group, agent):
     """comm_agent 'dma': copy-engine pushes of the partial pieces; 'core': the tile epilogues store
     the partials straight into the owners' receive slots and count tiles into their flag words.
@@ -127,7 +127,7 @@ def test_rs_protocol(kind, G, cta_group, agent):
         for run in range(RUNS):
             a = [orc.seeded_inputs(seed * 10 + run, g, (M, Kg)) for g in range(G)]
             w = [orc.seeded_inputs(seed * 10 + run, 50 + g, (N, Kg), "normal") for g in range(G)]
-            expect.append(orc.execute_rs(a, w))
+            expect.append(orc.execute_rs(a, w, own_bf16=agent == "nvls"))
             args.append([{"a": bf16_bits(a[g]), "b": bf16_bits(w[g]), "c": np.zeros((R, N), dtype=np.uint16)}
                          for g in range(G)])
         world = World(lows, args, seed=seed)

@@ -52,21 +52,46 @@ int main() {
   CKD(cuDevicePrimaryCtxRetain(&ctx, dev));
   CKD(cuCtxSetCurrent(ctx));
   CUmulticastObjectProp prop{};
-  prop.numDevices = 1;
-  prop.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
   size_t gran = 0;
-  prop.size = 2 << 20;
-  CKD(cuMulticastGetGranularity(&gran, &prop, CU_MULTICAST_GRANULARITY_RECOMMENDED));
-  const size_t bytes = ((size_t(64) << 20) + gran - 1) / gran * gran;
-  prop.size = bytes;
+  size_t bytes = 0;
   CUmemGenericAllocationHandle mc;
-  CKD(cuMulticastCreate(&mc, &prop));
+  {  // which (handle type, device count) combinations does the driver accept here?
+    const CUmemAllocationHandleType types[] = {CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, CU_MEM_HANDLE_TYPE_NONE,
+                                               CU_MEM_HANDLE_TYPE_FABRIC};
+    const char* tn[] = {"posix_fd", "none", "fabric"};
+    bool made = false;
+    for (int ti = 0; ti < 3 && !made; ++ti)
+      for (int nd : {1, 2}) {
+        CUmulticastObjectProp pr{};
+        pr.numDevices = nd;
+        pr.handleTypes = types[ti];
+        pr.size = 2 << 20;
+        size_t g = 0;
+        CUresult rg = cuMulticastGetGranularity(&g, &pr, CU_MULTICAST_GRANULARITY_RECOMMENDED);
+        if (rg != CUDA_SUCCESS || g == 0) {
+          std::printf("{\"handle\": \"%s\", \"devices\": %d, \"granularity_error\": %d}\n", tn[ti], nd, int(rg));
+          continue;
+        }
+        pr.size = ((size_t(64) << 20) + g - 1) / g * g;
+        CUresult rc = cuMulticastCreate(&mc, &pr);
+        std::printf("{\"handle\": \"%s\", \"devices\": %d, \"granularity\": %zu, \"create\": %d}\n", tn[ti], nd, g,
+                    int(rc));
+        if (rc == CUDA_SUCCESS) {
+          if (nd == 1) {
+            prop = pr, gran = g, bytes = pr.size, made = true;
+            break;
+          }
+          cuMemRelease(mc);
+        }
+      }
+    if (!made) return 0;
+  }
   CKD(cuMulticastAddDevice(mc, dev));
   CUmemAllocationProp mp{};
   mp.type = CU_MEM_ALLOCATION_TYPE_PINNED;
   mp.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
   mp.location.id = 0;
-  mp.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  mp.requestedHandleTypes = CUmemAllocationHandleType(prop.handleTypes);
   CUmemGenericAllocationHandle mem;
   CKD(cuMemCreate(&mem, bytes, &mp, 0));
   CKD(cuMulticastBindMem(mc, 0, mem, 0, bytes, 0));
