@@ -9,8 +9,10 @@
  * real executor that takes that slot: the Python layer lowers an
  * ExecutionPlan (per rank) into
  *   - a COPY PROGRAM run on a dedicated copy stream: copy-engine peer copies
- *     (cudaMemcpyBatchAsync / cudaMemcpy2DAsync, no SMs) interleaved with
- *     stream memory operations that publish per-chunk readiness flags, and
+ *     (cudaMemcpyAsync / cudaMemcpy2DAsync, no SMs; captured once into a CUDA
+ *     graph per workspace parity) each followed by a copy-engine copy of a
+ *     constant word that publishes the chunk's readiness flag (waits are
+ *     cuStreamWaitValue32/64 stream memory operations), and
  *   - a TILE PROGRAM run by one persistent tcgen05/TMEM/TMA kernel on the
  *     compute stream whose producer warp gates each tile's TMA loads on those
  *     flags (no host round trip).
@@ -284,6 +286,10 @@ int ficco_occupy_sms(int64_t ns, void* stream);
 /* Write the %globaltimer (ns, same clock as ficco_plan_set_trace stamps) to device u64 *dst,
  * stream-ordered: marks an op's start/end on the tile kernel's timeline. */
 int ficco_timestamp(void* dst, void* stream);
+/* Diagnostic: one CTA polls device words[0..n) until each is >= want and writes the
+ * %globaltimer of its arrival to u64 out[i] (0 after timeout_ns); out[n] = watcher start.
+ * Gives the copy program's per-flag arrival profile (launch it before the run). */
+int ficco_watch_words(const void* words, int n, uint32_t want, void* out, int64_t timeout_ns, void* stream);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

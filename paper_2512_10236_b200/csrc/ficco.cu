@@ -202,6 +202,24 @@ __global__ void __launch_bounds__(1024, 1) occupy_kernel(int64_t ns) {
 }
 // One %globaltimer stamp, stream-ordered (op-boundary marks for the tile kernel's trace).
 __global__ void stamp_kernel(unsigned long long* dst) { *dst = globaltimer(); }
+// Arrival profile of readiness words (diagnostic): thread i polls words[i] until it is >= want and
+// writes the %globaltimer of that moment to out[i] (0 on timeout); out[n] = the watcher's own start.
+__global__ void watch_kernel(const uint32_t* words, int n, uint32_t want, unsigned long long* out,
+                             int64_t timeout_ns) {
+  const unsigned long long t0 = globaltimer();
+  if (threadIdx.x == 0) out[n] = t0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    unsigned long long t = 0;
+    for (;;) {
+      uint32_t v;
+      asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(words + i) : "memory");
+      const unsigned long long now = globaltimer();
+      if (v >= want) { t = now; break; }
+      if (int64_t(now - t0) > timeout_ns) break;
+    }
+    out[i] = t;
+  }
+}
 }  // namespace ficco
 
 struct ficco_comm {
@@ -1095,6 +1113,14 @@ int ficco_cp_qk(ficco_plan_t* plan, const void* q, const void* k_shard, void* sc
 
 int ficco_timestamp(void* dst, void* stream) {
   ficco::stamp_kernel<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(reinterpret_cast<unsigned long long*>(dst));
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int ficco_watch_words(const void* words, int n, uint32_t want, void* out, int64_t timeout_ns, void* stream) {
+  if (n <= 0 || n > 4096) return fail(FICCO_EINVAL, "watch: 1..4096 words");
+  ficco::watch_kernel<<<1, n < 1024 ? n : 1024, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const uint32_t*>(words), n, want, reinterpret_cast<unsigned long long*>(out), timeout_ns);
   CK(cudaGetLastError());
   return 0;
 }

@@ -197,16 +197,19 @@ __device__ __forceinline__ void producer_loop(const TileParams& p, uint8_t* sA, 
   const uint64_t hint_a = p.a_evict_last ? policy_evict_last() : policy_evict_first();
   const uint64_t hint_b = p.b_evict_first ? policy_evict_first() : policy_evict_last();
   uint32_t stage = 0, phase = 0;
-  int res_b_row = -1, res_b_src = -1;  // B rows resident in smem (b_resident mode)
+  int res_b_row = -1, res_b_src = -1, res_b_cols = -1;  // B rows resident in smem (b_resident mode)
   uint32_t bfree_phase = 0;
   for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
     const ficco_tile td = p.tiles[t];
-    const int b_row = td.b_row + int(rank) * Cfg::B_ROWS;
+    // per-tile MMA width (tile cols, a multiple of 32 <= TN): with CTA pairs each CTA supplies half of
+    // the UMMA N rows, so the second CTA's B rows start cols/2 (not TN/2) past the tile's first row
+    const int b_row = td.b_row + int(rank) * (CG == 2 ? td.cols / 2 : 0);
     const CUtensorMap* map_a = td.a_src ? &p.tmap_a2 : &p.tmap_a;
     const CUtensorMap* map_b = td.b_src ? &p.tmap_b2 : &p.tmap_b;
     // b_resident: (re)load B only when this tile's B rows differ from the resident ones, after the MMAs
     // of every tile that read the old rows completed (b_free, committed by the MMA issuer)
-    const bool load_b = !p.b_resident || td.b_row != res_b_row || int(td.b_src) != res_b_src;
+    const bool load_b =
+        !p.b_resident || td.b_row != res_b_row || int(td.b_src) != res_b_src || int(td.cols) != res_b_cols;
     if (p.b_resident && load_b) {
       if (res_b_row >= 0) {
         mbar_wait(bfree, bfree_phase);
@@ -214,6 +217,7 @@ __device__ __forceinline__ void producer_loop(const TileParams& p, uint8_t* sA, 
       }
       res_b_row = td.b_row;
       res_b_src = td.b_src;
+      res_b_cols = td.cols;
     }
     for (int kb = 0; kb < p.num_kb; ++kb) {
       if (td.flag >= 0) {
@@ -290,10 +294,11 @@ __device__ __forceinline__ void mma_loop(const TileParams& p, uint8_t* sA, uint8
                                          uint64_t* empty, uint64_t* tfull, uint64_t* tempty, uint32_t tmem,
                                          uint64_t* bfree) {
   using Cfg = TileCfg<TN, CG, EB>;
-  constexpr uint32_t idesc = make_idesc_bf16(BM * CG, TN);
   constexpr uint32_t idesc64 = make_idesc_bf16(BM * CG, 64);
   uint32_t stage = 0, phase = 0, it = 0;
   for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
+    // UMMA N = the tile's own width (per-chunk tile shapes; cols % 32 == 0 and <= TN, ficco_plan_create)
+    const uint32_t idesc = make_idesc_bf16(BM * CG, p.tiles[t].cols);
     const uint32_t acc = it & 1u;
     mbar_wait(&tempty[acc], ((it >> 1) & 1u) ^ 1u);
     tc_fence_after();
@@ -352,7 +357,8 @@ __device__ __forceinline__ void mma_loop(const TileParams& p, uint8_t* sA, uint8
     if (p.b_resident) {
       // the resident B rows are free once this tile's MMAs retire, if the CTA's next tile reads other rows
       const int nt = t + int(gridDim.x);
-      if (nt < p.num_tiles && (p.tiles[nt].b_row != p.tiles[t].b_row || p.tiles[nt].b_src != p.tiles[t].b_src)) {
+      if (nt < p.num_tiles && (p.tiles[nt].b_row != p.tiles[t].b_row || p.tiles[nt].b_src != p.tiles[t].b_src ||
+                               p.tiles[nt].cols != p.tiles[t].cols)) {
         if constexpr (CG == 1)
           umma_commit(bfree);
         else

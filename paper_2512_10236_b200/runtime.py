@@ -44,7 +44,7 @@ EXPORTED = (
     "ficco_comm_create", "ficco_comm_destroy", "ficco_comm_epoch", "ficco_comm_check", "ficco_comm_set_flags",
     "ficco_plan_create", "ficco_plan_destroy", "ficco_plan_run", "ficco_plan_run_parts",
     "ficco_gemm_bf16", "ficco_copy_batch", "ficco_plan_set_trace", "ficco_plan_info", "ficco_gemm_bf16_cfg", "ficco_occupy_sms",
-    "ficco_timestamp", "ficco_ag_gemm", "ficco_a2a_gemm", "ficco_gemm_rs", "ficco_cp_qk",
+    "ficco_timestamp", "ficco_watch_words", "ficco_ag_gemm", "ficco_a2a_gemm", "ficco_gemm_rs", "ficco_cp_qk",
     "ficco_plan_set_kernel_event", "ficco_mc_supported", "ficco_mc_create", "ficco_mc_export", "ficco_mc_import",
     "ficco_mc_add_device", "ficco_mc_bind", "ficco_mc_release", "ficco_comm_set_multicast", "ficco_mc_reduce_bf16",
 )
@@ -125,6 +125,7 @@ def load_library(path: os.PathLike | str | None = None) -> C.CDLL:
             "ficco_copy_batch": ([C.POINTER(vp), C.POINTER(vp), C.POINTER(sz), sz, vp], i32),
             "ficco_occupy_sms": ([i64, vp], i32),
             "ficco_timestamp": ([vp, vp], i32),
+            "ficco_watch_words": ([vp, i32, C.c_uint32, vp, i64, vp], i32),
             "ficco_plan_set_trace": ([vp, vp], i32),
             "ficco_plan_set_kernel_event": ([vp, vp], i32),
             "ficco_mc_supported": ([i32, C.POINTER(i32)], i32),
@@ -460,3 +461,12 @@ def timestamp(dst, stream=None) -> None:
     import torch
     s = stream if stream is not None else torch.cuda.current_stream()
     check(load_library().ficco_timestamp(C.c_void_p(dst.data_ptr()), C.c_void_p(s.cuda_stream)))
+
+
+def watch_words(words_ptr: int, n: int, want: int, out, timeout_ns: int = 10**9, stream=None) -> None:
+    """Diagnostic arrival profile: out (int64 CUDA tensor, n + 1) := %globaltimer when each of the n device
+    words at words_ptr first reads >= want (0 on timeout); out[n] = watcher start. Launch before a run."""
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    check(load_library().ficco_watch_words(C.c_void_p(words_ptr), n, want, C.c_void_p(out.data_ptr()), timeout_ns,
+                                           C.c_void_p(s.cuda_stream)))

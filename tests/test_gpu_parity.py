@@ -549,3 +549,49 @@ def test_nvls_fails_cleanly_or_reduces_in_the_switch(lib):
         assert torch.equal(out, src)
     finally:
         lib.check(L.ficco_mc_release(h))
+
+
+@pytest.mark.parametrize("cta_group", [1, 2])
+def test_mixed_tile_widths_in_one_program(lib, cta_group):
+    """Per-tile UMMA widths: every tile of a lowered AG plan re-split into narrower tiles of mixed widths
+    (32 / 64 / 96 / 128 inside a TN = 256 kernel) still matches the oracle (CTA-pair B split at
+    cols/2, per-tile instruction descriptor)."""
+    from paper_2512_10236_b200 import lowering, ops
+    from paper_2512_10236_b200.runtime import Plan
+    G, R, K, N = 4, 256, 512, 768
+    shards = [orc.seeded_inputs(9, p, (R, K)) for p in range(G)]
+    w = orc.seeded_inputs(9, 99, (N, K), "normal")
+    _, outs = orc.execute_ag("hetero_unfused_1d", shards, w)
+    grp = ops.FiccoGroup.virtual_group(G, 2)
+    try:
+        _, low, _ = ops.prepare_ag(grp, R, K, N, "hetero_unfused_1d")
+        grp.load_peer_shards(low, [_t(s) for s in shards])
+        low = lowering.lower_ag(ops.build_plan(ops._scenario("ag", G * R, N, K, G),
+                                               ops.ScheduleKind("hetero_unfused_1d")), 2, "A",
+                                cta_group=cta_group)
+        low.desc.tile_n = 256  # the widest kernel; every tile below is narrower
+        widths = [64, 96, 128]
+        tiles = []
+        for i in range(0, len(low.tiles), cta_group):
+            grp_t = low.tiles[i:i + cta_group]
+            w0 = grp_t[0].cols
+            cut = widths[(i // cta_group) % 3] if w0 > widths[(i // cta_group) % 3] else w0
+            for off, cw in ((0, cut), (cut, w0 - cut)):
+                if cw <= 0:
+                    continue
+                for t in grp_t:
+                    tiles.append(lowering._tile(t.a_row, t.b_row + off, t.c_row, t.c_col + off, t.rows, cw, t.flag,
+                                                t.fmask, t.kseg, t.kstride, t.mode, t.chunk, t.recv_row, t.a_src,
+                                                t.b_src))
+        assert len({t.cols for t in tiles}) >= 3
+        plan = Plan(grp.comm, low.desc, low.ops, tiles)
+        try:
+            out = torch.empty(G * R, N, dtype=torch.bfloat16, device="cuda")
+            for _ in range(2):
+                plan.run(_t(shards[2]), _t(w), out)
+                grp.comm.check()
+                np.testing.assert_allclose(_np(out), outs[2], rtol=RTOL, atol=ATOL)
+        finally:
+            plan.close()
+    finally:
+        grp.close()
