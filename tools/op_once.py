@@ -1,6 +1,6 @@
 """Run one bench workload's overlapped op a few times (ncu target for the in-op tile kernel).
 
-usage: python tools/op_once.py c2|c3|c4 <kind> [dma|core] [calls]
+usage: python tools/op_once.py c2|c3|c4|c3p|ep <kind> [dma|core] [calls] [G]
 Under ncu the copy program runs before the kernel (profilers serialise), so the captured kernel
 is the op's tile program with its flags already satisfied.
 """
@@ -17,10 +17,12 @@ from paper_2512_10236_b200 import ops, runtime  # noqa: E402
 key, kind = sys.argv[1], sys.argv[2]
 agent = sys.argv[3] if len(sys.argv) > 3 else "dma"
 calls = int(sys.argv[4]) if len(sys.argv) > 4 else 4
+G = int(sys.argv[5]) if len(sys.argv) > 5 else bench.G_VIRTUAL
 runtime.load_library()
-wl = bench.WORKLOADS[key](torch, torch.device("cuda", 0), bench.G_VIRTUAL, 0, 1, ops)
+wl = bench.WORKLOADS[key](torch, torch.device("cuda", 0), G, 0, 1, ops)
 wl.agent = agent
-grp = ops.FiccoGroup.virtual_group(bench.G_VIRTUAL, 0)
+wl.inplace = key in ("c2", "c3p")  # as the bench runs them (zero-copy input slot)
+grp = ops.FiccoGroup.virtual_group(G, 0)
 wl.prepare(grp, kind)
 fn = wl.step(grp, kind)
 for _ in range(calls):
