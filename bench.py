@@ -314,7 +314,10 @@ class RSWorkload(AGWorkload):
     key = "c3"
     op = "rs"
     title = "C3 Llama-3-70B TP/SP down-proj GEMM->RS"
-    kinds = ["uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d"]
+    # every executable RS adjoint (lowering.rs_pieces): the fine-grain kinds, the N-block 2D adjoint,
+    # the reversed shard ring and the serial push-after-GEMM
+    kinds = ["uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d", "uniform_fused_2d", "shard_overlap_p2p",
+             "serial"]
 
     def __init__(self, torch, dev, G, rank, world, ops):
         self.t, self.dev, self.G, self.rank, self.world, self.ops = torch, dev, G, rank, world, ops

@@ -7,8 +7,8 @@
 //     written by tiny copy-engine copies of a constant word right behind the data,
 //     waits as stream memory operations (cuStreamWaitValue32/64) — no SMs, no host
 //     round trips; the whole program is captured once per workspace parity into a
-//     CUDA graph and replayed. (ficco_copy_batch exposes cudaMemcpyBatchAsync for
-//     calibration probes; the plans do not use it.)
+//     CUDA graph and replayed. (ficco_copy_batch issues a list of copies, one
+//     cudaMemcpyAsync each, for calibration probes; the plans do not use it.)
 //   * the tile program: TMA descriptors + one persistent tcgen05 kernel launch.
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -1137,13 +1137,10 @@ int ficco_occupy_sms(int64_t ns, void* stream) {
 }
 
 int ficco_copy_batch(void* const* dsts, const void* const* srcs, const size_t* sizes, size_t count, void* stream) {
-  if (count == 0) return 0;
-  cudaMemcpyAttributes attr{};
-  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-  attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-  size_t idx = 0, fail_idx = 0;
-  CK(cudaMemcpyBatchAsync(const_cast<void**>(dsts), const_cast<void**>(srcs), const_cast<size_t*>(sizes), count,
-                          &attr, &idx, 1, &fail_idx, reinterpret_cast<cudaStream_t>(stream)));
+  // one stream-ordered copy per entry (the driver's batched-copy entry point is not used: it faulted
+  // the GPU on this pool)
+  for (size_t i = 0; i < count; ++i)
+    CK(cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], cudaMemcpyDeviceToDevice, reinterpret_cast<cudaStream_t>(stream)));
   return 0;
 }
 

@@ -3,7 +3,7 @@
 Times (CUDA events on a dedicated stream) several ways of moving the 56 MiB a
 C2 rank ingests (56 fine chunks of 1 MiB, or 7 shards of 8 MiB):
   one_big        one 56 MiB cudaMemcpyAsync
-  shards7        7 x 8 MiB in one cudaMemcpyBatchAsync
+  shards7        7 x 8 MiB in one ficco_copy_batch call (one copy per entry)
   chunks56       56 x 1 MiB in one batch
   rounds8x7      8 batches of 7 x 1 MiB (the fine-grain copy program shape)
   torch_copy     torch .copy_ of 8 x 7 MiB slices (reference point)

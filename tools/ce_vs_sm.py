@@ -4,8 +4,7 @@ Every SM is occupied for T ms (ficco_occupy_sms: 1 CTA x 1024 threads with the
 full shared memory per SM, so no other CTA can be resident); a copy is issued
 on another stream right after. If the copy's end event lands before T, a copy
 engine ran it; if it lands after T, it waited for SMs. Variants: cudaMemcpyAsync
-(1D), cudaMemcpy2DAsync, cudaMemcpyBatchAsync with PreferOverlapWithCompute
-(ficco_copy_batch), and the AG copy program of a virtual-peer FiCCO plan.
+(1D), cudaMemcpy2DAsync, a ficco_copy_batch list, and the AG copy program of a virtual-peer FiCCO plan.
 """
 import ctypes as C
 import json
