@@ -145,11 +145,17 @@ int plan_role(const ficco_plan_desc& d) {
 // (M outer) while B [N, K] fits in L2 — every B tile then comes from L2; short-K, store-bound
 // shapes sweep the whole M extent per column block (each B tile read from HBM once, the small A
 // stays in L2); a B too large for L2 goes column-major over row groups whose A slice fits.
+// Rows per raster group of the plain GEMM (lowering.raster mirrors it). A weight up to 32 MiB stays
+// L2-resident under a row-major raster (C2). A larger one would be re-read from HBM by every wave
+// (C3's 59 MiB W: 0.86 GB of DRAM reads for 176 MB of operands), so rows go in groups whose A slice
+// (<= 32 MiB, pinned evict_last) stays in L2 while each group sweeps N: C3 0.40 GB, 2-3 % faster
+// (profiles/r02_experiments/c3_raster_ab.json). ceil(m / budget) groups, balanced.
 int64_t raster_rows(int64_t m, int64_t n, int64_t k, int64_t mstep) {
   if (epi_bufs_for(k) > 1) return m;
-  if (n * k * 2 <= (int64_t(64) << 20)) return mstep;
-  const int64_t rows = (int64_t(32) << 20) / (k * 2);
-  return std::max<int64_t>(mstep, rows / mstep * mstep);
+  if (n * k * 2 <= (int64_t(32) << 20)) return mstep;
+  const int64_t budget = std::max<int64_t>(mstep, (int64_t(32) << 20) / (k * 2) / mstep * mstep);
+  const int64_t groups = (m + budget - 1) / budget;
+  return ((m + groups - 1) / groups + mstep - 1) / mstep * mstep;
 }
 
 // Resolve the (tile width, CTA group, staging buffers) instantiation: entry point, dynamic smem,
@@ -1152,12 +1158,14 @@ int ficco_gemm_bf16_cfg(const void* a, const void* b, void* c, int64_t m, int64_
   if (cta_group != 1 && cta_group != 2) return fail(FICCO_EINVAL, "cta_group must be 1 or 2");
   static std::mutex mu;
   // keyed on the full shape: the tile width, raster grouping and L2 hints all depend on (m, n, k)
-  static std::map<std::tuple<int64_t, int64_t, int64_t, int, int, int, int>, std::pair<ficco_comm*, ficco_plan*>>
+  static std::map<std::tuple<int64_t, int64_t, int64_t, int, int, int, int, int64_t>,
+                  std::pair<ficco_comm*, ficco_plan*>>
       cache;
   std::lock_guard<std::mutex> lock(mu);
   int dev;
   CK(cudaGetDevice(&dev));
-  auto key = std::make_tuple(m, n, k, grid, dev, tile_n, cta_group);
+  const char* genv = getenv("FICCO_GEMM_GROUP_M");  // pair-blocks per raster group (A/B experiments)
+  auto key = std::make_tuple(m, n, k, grid, dev, tile_n, cta_group, genv ? atoll(genv) : int64_t(-1));
   auto it = cache.find(key);
   if (it == cache.end()) {
     static std::map<int, void*> ws_by_dev;
@@ -1205,7 +1213,6 @@ int ficco_gemm_bf16_cfg(const void* a, const void* b, void* c, int64_t m, int64_
         tiles.push_back(t);
       }
     };
-    const char* genv = getenv("FICCO_GEMM_GROUP_M");  // pair-blocks per raster group (A/B experiments)
     const int64_t slots = (grid > 0 ? grid : cm->sms) / cta_group;
     const int64_t ncb = (n + tn - 1) / tn;
     const char* benv = getenv("FICCO_B_RESIDENT");
@@ -1247,7 +1254,9 @@ int ficco_gemm_bf16_cfg(const void* a, const void* b, void* c, int64_t m, int64_
     const bool grouped = raster_rows(m, n, k, int64_t(ficco::BM) * cta_group) > int64_t(ficco::BM) * cta_group &&
                          epi_bufs_for(k) == 1;
     const bool pin = env && env[0] != 'a' ? env[0] == '1' : (m * k * 2 <= (int64_t(32) << 20) || grouped);
-    p->desc.hints = (pin ? FICCO_HINT_A_EVICT_LAST : 0) | (grouped ? FICCO_HINT_B_EVICT_FIRST : 0);
+    // a weight beyond L2 streams (evict_first); one that fits (32-64 MiB) stays evict_last
+    const bool stream_b = grouped && n * k * 2 > (int64_t(64) << 20);
+    p->desc.hints = (pin ? FICCO_HINT_A_EVICT_LAST : 0) | (stream_b ? FICCO_HINT_B_EVICT_FIRST : 0);
   }
   return ficco_plan_run_parts(p, a, b, c, stream, 0, 1);  // no flags: direct launch
 }

@@ -196,6 +196,7 @@ __device__ __forceinline__ void producer_loop(const TileParams& p, uint8_t* sA, 
   using Cfg = TileCfg<TN, CG, EB>;
   const uint64_t hint_a = p.a_evict_last ? policy_evict_last() : policy_evict_first();
   const uint64_t hint_b = p.b_evict_first ? policy_evict_first() : policy_evict_last();
+  const uint64_t hint_recv = policy_evict_first();  // received partials are read once (REDUCE)
   uint32_t stage = 0, phase = 0;
   int res_b_row = -1, res_b_src = -1, res_b_cols = -1;  // B rows resident in smem (b_resident mode)
   uint32_t bfree_phase = 0;
@@ -271,11 +272,11 @@ __device__ __forceinline__ void producer_loop(const TileParams& p, uint8_t* sA, 
           const int rrow = j * p.recv_rows + td.recv_row;
           if constexpr (CG == 1) {
             mbar_arrive_expect_tx(&full[stage], Cfg::RED_STAGE);
-            tma_load_2d(sA + stage * A_STAGE, &p.tmap_recv, &full[stage], td.c_col + kb * 64, rrow, hint_a);
+            tma_load_2d(sA + stage * A_STAGE, &p.tmap_recv, &full[stage], td.c_col + kb * 64, rrow, hint_recv);
             tma_load_2d(sB + stage * Cfg::B_STAGE, &p.tmap_ident, &full[stage], 0, 0, hint_b);
           } else {
             if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::RED_STAGE);
-            tma_load_2d_pair(sA + stage * A_STAGE, &p.tmap_recv, &full[stage], td.c_col + kb * 64, rrow, hint_a);
+            tma_load_2d_pair(sA + stage * A_STAGE, &p.tmap_recv, &full[stage], td.c_col + kb * 64, rrow, hint_recv);
             tma_load_2d_pair(sB + stage * Cfg::B_STAGE, &p.tmap_ident, &full[stage], 0,
                              int(rank) * Cfg::IDENT_ROWS, hint_b);
           }

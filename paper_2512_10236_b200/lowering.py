@@ -187,21 +187,23 @@ def choose_tile_n(tiles_for_width, sms: int = B200_SMS) -> int:
     return best_w
 
 
-W_L2_BYTES = 64 << 20     # a weight up to this size stays L2-resident under a row-major raster
-A_GROUP_BYTES = 32 << 20  # otherwise rows are rastered in groups whose A slice stays in L2
+W_ROW_MAJOR_BYTES = 32 << 20  # a weight up to this size stays L2-resident under a row-major raster
+W_L2_BYTES = 64 << 20         # up to this size it still fits L2 (evict_last) under a grouped raster
+A_GROUP_BYTES = 32 << 20      # otherwise rows are rastered in groups whose A slice stays in L2
 
 
 def raster(frags: list[tuple[int, int]], N: int, K: int, tn: int) -> list[tuple[int, int, int]]:
     """Tiles (m0, n0, rows) covering the row fragments ``frags`` x [0, N).
 
-    Row-major while W [N, K] fits in L2 (each W tile then comes from L2 for every row block:
-    C2/C3). A larger W would be streamed from HBM once per 128-row block (EP g14: 235 MB x 576),
-    so the 128-row blocks go in groups of A_GROUP_BYTES and each group sweeps N column-major:
-    W is read once per group, the group's A rows stay in L2 (pinned evict_last, W evict_first;
-    the plain GEMM uses the same raster, ficco.cu raster_rows).
+    Row-major while W [N, K] stays L2-resident beside the streams (up to 32 MiB: C2; each W tile
+    then comes from L2 for every row block). A larger W is re-read from HBM by every wave (C3's
+    59 MiB: 0.86 GB of DRAM reads; EP g14's 235 MB: 102 GB), so the 128-row blocks go in groups of
+    A_GROUP_BYTES and each group sweeps N column-major: W is read once per group, the group's A rows
+    stay in L2 (pinned evict_last; W evict_first beyond 64 MiB; the plain GEMM uses the same raster,
+    ficco.cu raster_rows).
     """
     blocks = [(m0, min(TILE_M, s + c - m0)) for s, c in frags for m0 in range(s, s + c, TILE_M)]
-    if N * K * ELT <= W_L2_BYTES:
+    if N * K * ELT <= W_ROW_MAJOR_BYTES:
         return [(m0, n0, rows) for m0, rows in blocks for n0 in range(0, N, tn)]
     per = max(2, (A_GROUP_BYTES // (K * ELT)) // TILE_M // 2 * 2)  # whole CTA pairs per group
     # balance the groups over this run's blocks: a fragment of 1.25 groups as one group (its A slice a
@@ -519,11 +521,11 @@ def lower_ag(plan: ExecutionPlan, rank: int, gathered: str = "A", alpha: float =
     # a small A (CP: Q, a few MiB) is re-read by every column tile while the output streams
     # through L2 (4 GiB of scores in C4) — pin it (evict_last) instead of the default evict_first
     a_bytes = (Q if gathered == "B" else M) * K * ELT
-    grouped = gathered == "A" and N * K * ELT > W_L2_BYTES  # column-major raster (see raster)
+    grouped = gathered == "A" and N * K * ELT > W_ROW_MAJOR_BYTES  # column-major raster (see raster)
     if os.environ.get("FICCO_A_EVICT_LAST", "auto") == "1" or (
             os.environ.get("FICCO_A_EVICT_LAST", "auto") == "auto" and (a_bytes <= A_PIN_BYTES or grouped)):
         d.hints |= FICCO_HINT_A_EVICT_LAST
-    if grouped:
+    if grouped and N * K * ELT > W_L2_BYTES:
         d.hints |= FICCO_HINT_B_EVICT_FIRST
     d.hints |= _agent_hint(comm_agent)
     low.notes = {"kind": kind.value, "rank": g, "world": G, "gathered": gathered, "inplace": inplace,
@@ -657,20 +659,50 @@ def lower_rs(scenario: Scenario, kind: ScheduleKind, rank: int, grid: int = 0, v
     tiles_per_piece = cdiv(shape0.nrows, TILE_M) * cdiv(shape0.ncols, tn)
     unit_of = {pc: uid for uid, pcs in enumerate(units) for pc in pcs}
 
-    for is_remote, pc in order:  # piece-major (row-major inside a piece: measured best for W reuse)
-        for m0 in range(pc.row0, pc.row0 + pc.nrows, TILE_M):
-            rows = min(TILE_M, pc.row0 + pc.nrows - m0)
-            for n0 in range(pc.col0, pc.col0 + pc.ncols, tn):
-                cols = min(tn, pc.col0 + pc.ncols - n0)
-                if is_remote and direct:
-                    tiles.append(_tile(m0, n0, m0 - pc.owner * R, n0, rows, cols, mode=EPI_STORE_REMOTE,
-                                       chunk=pc.owner, recv_row=F_RS + pc.idx * (G - 1) + slot_of(g, pc.owner)))
-                elif is_remote:
-                    tiles.append(_tile(m0, n0, m0, n0, rows, cols, mode=EPI_STORE_SIGNAL, chunk=unit_of[pc]))
-                else:
-                    local = m0 - g * R
-                    tiles.append(_tile(m0, n0, local, n0, rows, cols, mode=EPI_REDUCE, chunk=pc.idx,
-                                       recv_row=local))
+    def piece_tiles(pcs):
+        """(piece, m0, rows, n0, cols) of consecutive pieces: row-major inside each piece while W stays
+        L2-resident; otherwise (see raster) the pieces' row blocks sweep N column-major as one group."""
+        if len(pcs) == 1 or N * K * ELT <= W_ROW_MAJOR_BYTES:
+            return [(pc, m0, min(TILE_M, pc.row0 + pc.nrows - m0), n0, min(tn, pc.col0 + pc.ncols - n0))
+                    for pc in pcs for m0 in range(pc.row0, pc.row0 + pc.nrows, TILE_M)
+                    for n0 in range(pc.col0, pc.col0 + pc.ncols, tn)]
+        return [(pc, m0, min(TILE_M, pc.row0 + pc.nrows - m0), n0, min(tn, pc.col0 + pc.ncols - n0))
+                for n0 in range(0, N, tn) for pc in pcs for m0 in range(pc.row0, pc.row0 + pc.nrows, TILE_M)]
+
+    # pieces in schedule order; runs of full-width pieces of the same role (remote / own) go in row
+    # groups of about A_GROUP_BYTES of A (ceil(rows / budget) groups, balanced) when W is large
+    groups: list[tuple[bool, list]] = []
+    budget = max(2 * TILE_M, A_GROUP_BYTES // (K * ELT))
+    i = 0 if os.environ.get("FICCO_RS_GROUP", "1") != "0" else len(order)  # 0: piece by piece (A/B)
+    groups += [(rem, [pc]) for rem, pc in order] if i else []
+    while i < len(order):
+        j = i
+        while (j < len(order) and order[j][0] == order[i][0] and order[j][1].ncols == N and
+               order[i][1].ncols == N):
+            j += 1
+        if j == i:  # a column slab (N-block adjoint): its own group
+            groups.append((order[i][0], [order[i][1]]))
+            i += 1
+            continue
+        run = [pc for _, pc in order[i:j]]
+        rows = sum(pc.nrows for pc in run)
+        ngroups = max(1, -(-rows // budget))
+        per = -(-len(run) // ngroups)
+        groups += [(order[i][0], run[x:x + per]) for x in range(0, len(run), per)]
+        i = j
+    grouped_rs = N * K * ELT > W_ROW_MAJOR_BYTES and any(len(pcs) > 1 for _, pcs in groups)
+
+    for is_remote, pcs in groups:
+        for pc, m0, rows, n0, cols in piece_tiles(pcs):
+            if is_remote and direct:
+                tiles.append(_tile(m0, n0, m0 - pc.owner * R, n0, rows, cols, mode=EPI_STORE_REMOTE,
+                                   chunk=pc.owner, recv_row=F_RS + pc.idx * (G - 1) + slot_of(g, pc.owner)))
+            elif is_remote:
+                tiles.append(_tile(m0, n0, m0, n0, rows, cols, mode=EPI_STORE_SIGNAL, chunk=unit_of[pc]))
+            else:
+                local = m0 - g * R
+                tiles.append(_tile(m0, n0, local, n0, rows, cols, mode=EPI_REDUCE, chunk=pc.idx,
+                                   recv_row=local))
 
     if cta_group == 2:
         tiles[:] = pair_tiles(tiles)
@@ -723,6 +755,8 @@ def lower_rs(scenario: Scenario, kind: ScheduleKind, rank: int, grid: int = 0, v
     d.recv_slot, d.n_recv, d.rs_flag0 = low.recv_slot, G - 1, F_RS
     d.n_counters = len(units)
     d.k, d.alpha, d.grid, d.tile_n, d.cta_group = K, 1.0, grid, tn, cta_group
+    if grouped_rs and os.environ.get("FICCO_A_EVICT_LAST", "auto") != "0":
+        d.hints |= FICCO_HINT_A_EVICT_LAST  # the group's A slice stays in L2 while it sweeps N
     if not direct:
         d.hints |= _agent_hint(comm_agent)
     if len(units) >= 4096 - 1:
