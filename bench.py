@@ -463,7 +463,7 @@ class CPWorkload(AGWorkload):
         return {"Tkv": tkv, "Tq": tq, "d": d, "seq_len": tkv}
 
     def plan_for(self, grp, kind, agent):
-        return self.ops.prepare_cp(grp, self.Tq, self.d, self.Tkv, kind, comm_agent=agent)[0]
+        return self.ops.prepare_cp(grp, self.Tq, self.d, self.Tkv, kind, comm_agent=agent, inplace=self.inplace)[0]
 
     def lowered(self, grp, kind):
         return self.ops.prepare_cp(grp, self.Tq, self.d, self.Tkv, kind, comm_agent=self.agent)[1]
@@ -472,12 +472,21 @@ class CPWorkload(AGWorkload):
         _, low, _ = self.ops.prepare_cp(grp, self.Tq, self.d, self.Tkv, kind, comm_agent=self.agent)
         if grp.virtual:
             grp.load_peer_shards(low, self.shards)
+        if self.inplace:  # the K shard already sits in this rank's workspace slot, both parities
+            for par in (0, 1):
+                off = low.gather_off + par * low.gather_par + grp.rank * self.R * self.d * 2
+                grp.ws_tensor(grp.rank, off, (self.R, self.d)).copy_(self.local)
 
     def run_plan(self, plan):
         plan.run(self.q, self.local, self.out)
 
     def step(self, grp, kind, agent="self"):
         agent = self.agent if agent == "self" else agent
+        if self.inplace:
+            def fn():
+                k = grp.kv_slot(self.Tq, self.d, self.Tkv, kind)
+                self.ops.cp_kv_all_gather_qk(self.q, k, kind=kind, group=grp, out=self.out, comm_agent=agent)
+            return fn
         return lambda: self.ops.cp_kv_all_gather_qk(self.q, self.local, kind=kind, group=grp, out=self.out,
                                                     comm_agent=agent)
 
@@ -667,7 +676,7 @@ def workload_config(args, world: int) -> dict:
     cls = WORKLOADS[args.workload]
     G = args.virtual_ranks if world == 1 else world
     kind, agent = headline_choice(args.workload, G, args)
-    slot = args.input == "slot" and args.workload in ("c2", "c3p")
+    slot = args.input == "slot" and args.workload in ("c2", "c3p", "c4")
     return dict(workload=cls.title, ranks=G, virtual_peers=world == 1, schedule=kind, comm_agent=agent,
                 schedule_source=("--kind/--agent override" if (args.kind or args.agent) else
                                  "public API default: select_schedule on the B200 machine file; "

@@ -622,6 +622,11 @@ int make_params(ficco_plan* p, uint32_t parity, const void* a, const void* b, vo
     prm->epi_fast = fast && fast[0] == '0' ? 0 : 1;
   }
   prm->b_evict_first = (d.hints & FICCO_HINT_B_EVICT_FIRST) != 0;
+  {
+    // FICCO_B_HINT=last|first|normal overrides the plan's B (weight) L2 policy (A/B experiments)
+    const char* env = getenv("FICCO_B_HINT");
+    if (env && env[0]) prm->b_evict_first = env[0] == 'f' ? 1 : env[0] == 'n' ? 2 : 0;
+  }
   prm->trace = p->trace;
   int g = d.grid > 0 ? d.grid : cm->sms;
   if (g > p->n_tiles) g = p->n_tiles;

@@ -122,7 +122,7 @@ struct alignas(64) TileParams {
                            // (b_row, b_src): only A is streamed through the ring (halves the L2->SM bytes
                            // of C4's store-bound tiles). Requires num_kb <= STAGES and no REDUCE tiles.
   int a_evict_last;        // FICCO_HINT_A_EVICT_LAST
-  int b_evict_first;       // FICCO_HINT_B_EVICT_FIRST
+  int b_evict_first;       // FICCO_HINT_B_EVICT_FIRST (1; 2: evict_normal, FICCO_B_HINT experiments)
   int part_hint;           // L2 policy of STORE_SIGNAL (to-be-pushed) stores: 0 evict_first, 1 normal, 2 last
   int epi_fast;            // full 64-column chunks take the straight-line epilogue path (FICCO_EPI_FAST=0: off)
   int out_plain;           // STORE / REDUCE output boxes stored without an L2 policy (store-bound programs:
@@ -195,7 +195,9 @@ __device__ __forceinline__ void producer_loop(const TileParams& p, uint8_t* sA, 
                                               uint64_t* empty, uint32_t rank, uint32_t* seen, uint64_t* bfree) {
   using Cfg = TileCfg<TN, CG, EB>;
   const uint64_t hint_a = p.a_evict_last ? policy_evict_last() : policy_evict_first();
-  const uint64_t hint_b = p.b_evict_first ? policy_evict_first() : policy_evict_last();
+  const uint64_t hint_b = p.b_evict_first == 1   ? policy_evict_first()
+                          : p.b_evict_first == 2 ? policy_evict_normal()
+                                                 : policy_evict_last();
   const uint64_t hint_recv = policy_evict_first();  // received partials are read once (REDUCE)
   uint32_t stage = 0, phase = 0;
   int res_b_row = -1, res_b_src = -1, res_b_cols = -1;  // B rows resident in smem (b_resident mode)

@@ -445,7 +445,21 @@ def lower_ag(plan: ExecutionPlan, rank: int, gathered: str = "A", alpha: float =
         tn = choose_tile_n(lambda w: sum(cdiv(c, w) for _, c in frag_lists) * cdiv(cdiv(Q, TILE_M), cta_group),
                            units)
     tiles = low.tiles
-    if gathered == "A":
+    if gathered == "A" and N * K * ELT > W_ROW_MAJOR_BYTES and os.environ.get("FICCO_AG_GROUP_GATES", "1") != "0":
+        # a W beyond the row-major budget is streamed once per row group, so the groups span fragments
+        # of DIFFERENT gates (each tile keeps its own block's gate): per-gate rasters would sweep all of W
+        # once per fine chunk (hetero_unfused C3': 56 x 117 MB; EP g14: 41 GB per op). The groups follow
+        # plan order, so a group waits at most for the chunks of its own rows.
+        info = {}
+        for start, count in frag_lists:
+            for m0 in range(start, start + count, TILE_M):
+                info[m0] = (gate(start), start // R == g)
+        for m0, n0, rows in raster(frag_lists, N, K, tn):
+            (flag, fmask, ks, kstride), local = info[m0]
+            shift = g * R if local else 0  # own-shard rows come from the call argument (alternate map)
+            tiles.append(_tile(m0 - shift, n0, m0, n0, rows, min(tn, N - n0), flag, fmask, ks, kstride,
+                               a_src=int(local)))
+    elif gathered == "A":
         # consecutive fragments behind the same gate (one fused step, the serial gather) are one
         # raster: a large W is then streamed once per row group, not once per fragment
         runs: list[tuple[tuple, list[tuple[int, int]]]] = []
@@ -659,50 +673,45 @@ def lower_rs(scenario: Scenario, kind: ScheduleKind, rank: int, grid: int = 0, v
     tiles_per_piece = cdiv(shape0.nrows, TILE_M) * cdiv(shape0.ncols, tn)
     unit_of = {pc: uid for uid, pcs in enumerate(units) for pc in pcs}
 
-    def piece_tiles(pcs):
-        """(piece, m0, rows, n0, cols) of consecutive pieces: row-major inside each piece while W stays
-        L2-resident; otherwise (see raster) the pieces' row blocks sweep N column-major as one group."""
-        if len(pcs) == 1 or N * K * ELT <= W_ROW_MAJOR_BYTES:
-            return [(pc, m0, min(TILE_M, pc.row0 + pc.nrows - m0), n0, min(tn, pc.col0 + pc.ncols - n0))
-                    for pc in pcs for m0 in range(pc.row0, pc.row0 + pc.nrows, TILE_M)
-                    for n0 in range(pc.col0, pc.col0 + pc.ncols, tn)]
-        return [(pc, m0, min(TILE_M, pc.row0 + pc.nrows - m0), n0, min(tn, pc.col0 + pc.ncols - n0))
-                for n0 in range(0, N, tn) for pc in pcs for m0 in range(pc.row0, pc.row0 + pc.nrows, TILE_M)]
-
-    # pieces in schedule order; runs of full-width pieces of the same role (remote / own) go in row
-    # groups of about A_GROUP_BYTES of A (ceil(rows / budget) groups, balanced) when W is large
-    groups: list[tuple[bool, list]] = []
-    budget = max(2 * TILE_M, A_GROUP_BYTES // (K * ELT))
-    i = 0 if os.environ.get("FICCO_RS_GROUP", "1") != "0" else len(order)  # 0: piece by piece (A/B)
-    groups += [(rem, [pc]) for rem, pc in order] if i else []
+    # Tile order: the schedule's pieces in order. While W stays L2-resident (<= 32 MiB) each piece is
+    # row-major. A larger W would be re-read from HBM by every wave (C3 at G = 8: 59 MB; at G = 2: 235 MB),
+    # so each run of full-width pieces of the same role (remote / own) is cut into 128-row blocks, the
+    # blocks go in balanced groups of <= A_GROUP_BYTES of A, and each group sweeps N column-major with
+    # its A rows pinned in L2 (as lowering.raster does for the AG side and ficco.cu raster_rows for the
+    # plain GEMM).
+    grouped_rs = N * K * ELT > W_ROW_MAJOR_BYTES and os.environ.get("FICCO_RS_GROUP", "1") != "0"
+    budget = max(2, A_GROUP_BYTES // (K * ELT) // TILE_M // 2 * 2)  # 128-row blocks per group (even)
+    seq: list[tuple[bool, RSPiece, int, int, int, int]] = []  # (remote, piece, m0, rows, n0, cols)
+    i = 0
     while i < len(order):
-        j = i
-        while (j < len(order) and order[j][0] == order[i][0] and order[j][1].ncols == N and
-               order[i][1].ncols == N):
+        j = i + 1
+        full = order[i][1].ncols == N
+        while grouped_rs and full and j < len(order) and order[j][0] == order[i][0] and order[j][1].ncols == N:
             j += 1
-        if j == i:  # a column slab (N-block adjoint): its own group
-            groups.append((order[i][0], [order[i][1]]))
-            i += 1
-            continue
         run = [pc for _, pc in order[i:j]]
-        rows = sum(pc.nrows for pc in run)
-        ngroups = max(1, -(-rows // budget))
-        per = -(-len(run) // ngroups)
-        groups += [(order[i][0], run[x:x + per]) for x in range(0, len(run), per)]
+        blocks = [(pc, m0, min(TILE_M, pc.row0 + pc.nrows - m0)) for pc in run
+                  for m0 in range(pc.row0, pc.row0 + pc.nrows, TILE_M)]
+        if not (grouped_rs and full) or len(blocks) <= 2:
+            seq += [(order[i][0], pc, m0, rows, n0, min(tn, pc.col0 + pc.ncols - n0)) for pc, m0, rows in blocks
+                    for n0 in range(pc.col0, pc.col0 + pc.ncols, tn)]
+        else:
+            per = -(-len(blocks) // -(-len(blocks) // budget))
+            per += per % 2
+            for x in range(0, len(blocks), per):
+                seq += [(order[i][0], pc, m0, rows, n0, min(tn, N - n0)) for n0 in range(0, N, tn)
+                        for pc, m0, rows in blocks[x:x + per]]
         i = j
-    grouped_rs = N * K * ELT > W_ROW_MAJOR_BYTES and any(len(pcs) > 1 for _, pcs in groups)
 
-    for is_remote, pcs in groups:
-        for pc, m0, rows, n0, cols in piece_tiles(pcs):
-            if is_remote and direct:
-                tiles.append(_tile(m0, n0, m0 - pc.owner * R, n0, rows, cols, mode=EPI_STORE_REMOTE,
-                                   chunk=pc.owner, recv_row=F_RS + pc.idx * (G - 1) + slot_of(g, pc.owner)))
-            elif is_remote:
-                tiles.append(_tile(m0, n0, m0, n0, rows, cols, mode=EPI_STORE_SIGNAL, chunk=unit_of[pc]))
-            else:
-                local = m0 - g * R
-                tiles.append(_tile(m0, n0, local, n0, rows, cols, mode=EPI_REDUCE, chunk=pc.idx,
-                                   recv_row=local))
+    for is_remote, pc, m0, rows, n0, cols in seq:
+        if is_remote and direct:
+            tiles.append(_tile(m0, n0, m0 - pc.owner * R, n0, rows, cols, mode=EPI_STORE_REMOTE,
+                               chunk=pc.owner, recv_row=F_RS + pc.idx * (G - 1) + slot_of(g, pc.owner)))
+        elif is_remote:
+            tiles.append(_tile(m0, n0, m0, n0, rows, cols, mode=EPI_STORE_SIGNAL, chunk=unit_of[pc]))
+        else:
+            local = m0 - g * R
+            tiles.append(_tile(m0, n0, local, n0, rows, cols, mode=EPI_REDUCE, chunk=pc.idx,
+                               recv_row=local))
 
     if cta_group == 2:
         tiles[:] = pair_tiles(tiles)
@@ -757,6 +766,8 @@ def lower_rs(scenario: Scenario, kind: ScheduleKind, rank: int, grid: int = 0, v
     d.k, d.alpha, d.grid, d.tile_n, d.cta_group = K, 1.0, grid, tn, cta_group
     if grouped_rs and os.environ.get("FICCO_A_EVICT_LAST", "auto") != "0":
         d.hints |= FICCO_HINT_A_EVICT_LAST  # the group's A slice stays in L2 while it sweeps N
+    if grouped_rs and N * K * ELT > W_L2_BYTES:
+        d.hints |= FICCO_HINT_B_EVICT_FIRST  # a W beyond L2 streams
     if not direct:
         d.hints |= _agent_hint(comm_agent)
     if len(units) >= 4096 - 1:

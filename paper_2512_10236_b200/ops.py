@@ -171,6 +171,15 @@ class FiccoGroup:
         off = low.gather_off + par * low.gather_par + self.rank * rows * cols * 2
         return self.ws_tensor(self.rank, off, (rows, cols))
 
+    def kv_slot(self, tq: int, d: int, tkv: int, kind=None, scale: float | None = None) -> torch.Tensor:
+        """This rank's K-shard slot [tkv / world, d] of the gathered K for the NEXT cp_kv_all_gather_qk call
+        (the context-parallel twin of ``input_slot``: write the shard here and pass the view as ``k_shard``)."""
+        _, low, _ = prepare_cp(self, tq, d, tkv, kind, scale)
+        rows = tkv // self.world
+        par = self.comm.epoch() & 1
+        off = low.gather_off + par * low.gather_par + self.rank * rows * d * 2
+        return self.ws_tensor(self.rank, off, (rows, d))
+
     def close(self) -> None:
         """Release the group (collective for distributed groups: every rank must call it)."""
         self._retire()
@@ -336,17 +345,17 @@ def prepare_rs(grp: FiccoGroup, M: int, K: int, N: int, kind=None, comm_agent=No
 
 
 def prepare_cp(grp: FiccoGroup, Tq: int, d: int, Tkv: int, kind=None, scale: float | None = None,
-               comm_agent=None):
+               comm_agent=None, inplace: bool = False):
     comm_agent = _agent(comm_agent, "cp")
     def make():
         sc = _scenario("cp_qk", Tkv, Tq, d, grp.world)
         kd = choose_kind(sc, kind)
         alpha = (1.0 / math.sqrt(d)) if scale is None else scale
-        plan, low = grp.plan(("cp", Tkv, Tq, d, kd, alpha, comm_agent),
+        plan, low = grp.plan(("cp", Tkv, Tq, d, kd, alpha, inplace, comm_agent),
                              lambda: lower_ag(build_plan(sc, kd), grp.rank, "B", alpha=alpha, other_rows=Tq,
-                                              comm_agent=comm_agent))
+                                              inplace=inplace, comm_agent=comm_agent))
         return plan, low, kd
-    return _cached(grp, ("cp", Tq, d, Tkv, kind, scale, comm_agent), make)
+    return _cached(grp, ("cp", Tq, d, Tkv, kind, scale, inplace, comm_agent), make)
 
 
 def default_agent(op: str) -> str:
@@ -467,7 +476,10 @@ def cp_kv_all_gather_qk(q: torch.Tensor, k_shard: torch.Tensor, kind=None, scale
     _check_tensor("k_shard", k_shard)
     Tkv = k_shard.shape[0] * grp.world
     _check_call(grp, {"q": (q, None), "k_shard": (k_shard, (Tkv // grp.world, d))}, out, (Tq, Tkv))
-    plan, _, _ = prepare_cp(grp, Tq, d, Tkv, kind, scale, comm_agent=_agent(comm_agent))
+    agent = _agent(comm_agent)
+    plan, low, kd = prepare_cp(grp, Tq, d, Tkv, kind, scale, comm_agent=agent)
+    if _is_slot(grp, k_shard, low):  # zero-copy publish: the K shard already sits in its slot
+        plan, _, _ = prepare_cp(grp, Tq, d, Tkv, kd, scale, comm_agent=agent, inplace=True)
     if out is None:
         out = torch.empty(Tq, Tkv, dtype=torch.bfloat16, device=q.device)
     _run(grp, plan, "cp_qk", q, k_shard, out, stream)

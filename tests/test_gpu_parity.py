@@ -168,6 +168,32 @@ def test_ag_input_slot_zero_copy(lib, kind):
         grp.close()
 
 
+@pytest.mark.parametrize("kind", ["shard_overlap_p2p", "hetero_unfused_1d", "serial"])
+def test_cp_kv_slot_zero_copy(lib, kind):
+    """CP: a K shard produced in the group's symmetric slot (kv_slot) skips the publish copy; same scores."""
+    from paper_2512_10236_b200 import ops
+    G, rank, d, Tq, Tkv = 4, 2, 128, 384, 4096
+    q = orc.seeded_inputs(11, 50, (Tq, d), "normal")
+    grp = ops.FiccoGroup.virtual_group(G, rank)
+    try:
+        for call in range(3):
+            ks = [orc.seeded_inputs(20 + call, p, (Tkv // G, d), "normal") for p in range(G)]
+            want, _ = orc.execute_cp_qk(q, ks, 1.0 / math.sqrt(d))
+            _, low, _ = ops.prepare_cp(grp, Tq, d, Tkv, kind)
+            grp.load_peer_shards(low, [_t(x) for x in ks])
+            slot = grp.kv_slot(Tq, d, Tkv, kind)
+            slot.copy_(_t(ks[rank]))
+            out = ops.cp_kv_all_gather_qk(_t(q), slot, kind=kind, group=grp)
+            grp.comm.check()
+            assert any(k[0] == "cp" and k[6] is True for k in grp._plans)  # the in-place plan ran
+            np.testing.assert_allclose(_np(out), want, rtol=RTOL, atol=ATOL)
+            ref = ops.cp_kv_all_gather_qk(_t(q), _t(ks[rank]), kind=kind, group=grp)  # copied-in path
+            grp.comm.check()
+            assert torch.equal(ref, out)
+    finally:
+        grp.close()
+
+
 @pytest.mark.parametrize("kind", AG_KINDS)
 def test_ag_core_agent_matches_oracle(lib, kind):
     """comm_agent='core': the transfers run as SM copy kernels beside the tile kernel; same results."""

@@ -10,7 +10,8 @@ from paper_2512_10236_b200.lowering import (F_RING, F_XFER, W_L2_BYTES, lower_ag
 from paper_2512_10236_b200.ops import _scenario
 from paper_2512_10236_b200 import routing
 from paper_2512_10236_b200.routing import PlanError, ScheduleKind, build_plan
-from paper_2512_10236_b200.runtime import EPI_REDUCE, EPI_STORE_REMOTE, EPI_STORE_SIGNAL
+from paper_2512_10236_b200.runtime import (EPI_REDUCE, EPI_STORE_REMOTE, EPI_STORE_SIGNAL, FICCO_HINT_A_EVICT_LAST,
+                                            FICCO_HINT_B_EVICT_FIRST)
 
 AG_KINDS = ["serial", "shard_overlap_p2p", "uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d",
             "uniform_fused_2d"]
@@ -85,6 +86,35 @@ def test_raster_switches_to_row_groups_above_the_l2_budget():
     big = raster(frags, N, K, 256)  # W 235 MB: column-major over 4096-row groups
     assert [(m, n) for m, n, _ in big[:3]] == [(0, 0), (128, 0), (256, 0)]
     assert len(big) == (4096 // 128) * (N // 256) == len({(m, n) for m, n, _ in big})
+
+
+@pytest.mark.parametrize("kind", [ScheduleKind.HETERO_UNFUSED_1D, ScheduleKind.HETERO_FUSED_1D,
+                                  ScheduleKind.UNIFORM_FUSED_1D])
+def test_large_w_row_groups_span_gates(kind):
+    """W beyond the row-major budget (C3': 117 MB) is swept once per <=32 MiB row group, not once per
+    gated fine chunk; every tile keeps the gate of its own rows; coverage is exact."""
+    M, N, K, G = 16384, 7168, 8192, 8
+    sc = _scenario("c3p", M, N, K, G)
+    low = lower_ag(build_plan(sc, kind), 0, "A")
+    sweeps = 1 + sum(1 for a, b in zip(low.tiles, low.tiles[1:]) if b.c_col < a.c_col)
+    assert sweeps <= 2 * (M * K * 2 // (32 << 20)), sweeps  # ~8 groups of 2048 rows, CTA pairs x2
+    assert (_coverage(low.tiles, M, N) == 1).all()
+    R, r = M // G, M // (G * G)
+    for t in low.tiles:
+        if t.rows and t.c_row // R != 0 and kind is ScheduleKind.HETERO_UNFUSED_1D:
+            c, p = (t.c_row % R) // r, t.c_row // R
+            assert t.flag == F_XFER + c * G + p
+
+
+def test_rs_large_w_row_groups():
+    """GEMM->RS at G = 2 (W 235 MB): the remote and own rows sweep N once per row group of 128-row blocks,
+    with A pinned and W streaming; every (row, col) of the partial is produced once."""
+    M, N, K, G = 16384, 8192, 14336, 2
+    sc = _scenario("c3", M, N, K, G)
+    low = lower_rs(sc, ScheduleKind.HETERO_UNFUSED_1D, 0, virtual=True, comm_agent="core")
+    sweeps = 1 + sum(1 for a, b in zip(low.tiles, low.tiles[1:]) if b.c_col < a.c_col)
+    assert sweeps <= 2 * (M * K * 2 // (32 << 20)) + 2, sweeps
+    assert low.desc.hints & FICCO_HINT_A_EVICT_LAST and low.desc.hints & FICCO_HINT_B_EVICT_FIRST
 
 
 def test_pair_tiles_pads_unmatched_tiles_with_zero_row_partners():

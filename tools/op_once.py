@@ -21,7 +21,7 @@ G = int(sys.argv[5]) if len(sys.argv) > 5 else bench.G_VIRTUAL
 runtime.load_library()
 wl = bench.WORKLOADS[key](torch, torch.device("cuda", 0), G, 0, 1, ops)
 wl.agent = agent
-wl.inplace = key in ("c2", "c3p")  # as the bench runs them (zero-copy input slot)
+wl.inplace = key in ("c2", "c3p", "c4")  # as the bench runs them (zero-copy input slot)
 grp = ops.FiccoGroup.virtual_group(G, 0)
 wl.prepare(grp, kind)
 fn = wl.step(grp, kind)
