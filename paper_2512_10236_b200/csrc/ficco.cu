@@ -180,6 +180,9 @@ int configure_kernels(int dev) {
   static uint64_t configured = 0;  // bit d: device d done
   std::lock_guard<std::mutex> lock(mu);
   if (dev >= 0 && dev < 64 && (configured >> dev) & 1u) return 0;
+  if (const char* env = getenv("FICCO_L2_PERSIST_MB")) {  // L2 set-aside for evict_last lines (experiments)
+    CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, size_t(atoll(env)) << 20));
+  }
 #define FICCO_CFG(T, G, E)                                                                              \
   CK(cudaFuncSetAttribute(ficco::tile_gemm_kernel<T, G, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                           ficco::TileCfg<T, G, E>::SMEM_BYTES));                                        \
@@ -1259,9 +1262,9 @@ int ficco_gemm_bf16_cfg(const void* a, const void* b, void* c, int64_t m, int64_
     const bool grouped = raster_rows(m, n, k, int64_t(ficco::BM) * cta_group) > int64_t(ficco::BM) * cta_group &&
                          epi_bufs_for(k) == 1;
     const bool pin = env && env[0] != 'a' ? env[0] == '1' : (m * k * 2 <= (int64_t(32) << 20) || grouped);
-    // a weight beyond L2 streams (evict_first); one that fits (32-64 MiB) stays evict_last
-    const bool stream_b = grouped && n * k * 2 > (int64_t(64) << 20);
-    p->desc.hints = (pin ? FICCO_HINT_A_EVICT_LAST : 0) | (stream_b ? FICCO_HINT_B_EVICT_FIRST : 0);
+    // W stays evict_last even beyond L2: every column tile is re-read by the group's row blocks, and
+    // evict_first lost those hits (2.3-4.6 % slower on C3 G2/G4, C3', EP; r02_experiments/w_policy_ab.json)
+    p->desc.hints = pin ? FICCO_HINT_A_EVICT_LAST : 0;
   }
   return ficco_plan_run_parts(p, a, b, c, stream, 0, 1);  // no flags: direct launch
 }

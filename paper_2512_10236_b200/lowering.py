@@ -50,7 +50,7 @@ from .domain import Collective, Scenario
 from .routing import (ExecutionPlan, GatherSpec, GemmSpec, PlanError, ScatterSpec, ScheduleKind, TransferSpec,
                       build_plan)
 from .runtime import (BUF_A, BUF_B, BUF_C, BUF_MC, BUF_MCV, BUF_NONE, BUF_WS, EPI_REDUCE, EPI_STORE, EPI_STORE_REMOTE,
-                      EPI_STORE_SIGNAL, FICCO_HINT_A_EVICT_LAST, FICCO_HINT_B_EVICT_FIRST,
+                      EPI_STORE_SIGNAL, FICCO_HINT_A_EVICT_LAST,
                       FICCO_HINT_CORE_COPIES,
                       FICCO_WS_DATA_OFFSET, MAX_RECV, OP_BARRIER, OP_COPY, OP_NOTIFY, OP_RECORD,
                       OP_REDUCE_MC, OP_SIGNAL, OP_STREAM_WAIT, OP_WAIT, OP_WAIT_COUNTER, TILE_K, TILE_M,
@@ -188,7 +188,7 @@ def choose_tile_n(tiles_for_width, sms: int = B200_SMS) -> int:
 
 
 W_ROW_MAJOR_BYTES = 32 << 20  # a weight up to this size stays L2-resident under a row-major raster
-W_L2_BYTES = 64 << 20         # up to this size it still fits L2 (evict_last) under a grouped raster
+W_L2_BYTES = 64 << 20         # about half the L2: a weight this large never stays resident beside the streams
 A_GROUP_BYTES = 32 << 20      # otherwise rows are rastered in groups whose A slice stays in L2
 
 
@@ -199,7 +199,7 @@ def raster(frags: list[tuple[int, int]], N: int, K: int, tn: int) -> list[tuple[
     then comes from L2 for every row block). A larger W is re-read from HBM by every wave (C3's
     59 MiB: 0.86 GB of DRAM reads; EP g14's 235 MB: 102 GB), so the 128-row blocks go in groups of
     A_GROUP_BYTES and each group sweeps N column-major: W is read once per group, the group's A rows
-    stay in L2 (pinned evict_last; W evict_first beyond 64 MiB; the plain GEMM uses the same raster,
+    stay in L2 (pinned evict_last; W evict_last too; the plain GEMM uses the same raster,
     ficco.cu raster_rows).
     """
     blocks = [(m0, min(TILE_M, s + c - m0)) for s, c in frags for m0 in range(s, s + c, TILE_M)]
@@ -539,8 +539,8 @@ def lower_ag(plan: ExecutionPlan, rank: int, gathered: str = "A", alpha: float =
     if os.environ.get("FICCO_A_EVICT_LAST", "auto") == "1" or (
             os.environ.get("FICCO_A_EVICT_LAST", "auto") == "auto" and (a_bytes <= A_PIN_BYTES or grouped)):
         d.hints |= FICCO_HINT_A_EVICT_LAST
-    if grouped and N * K * ELT > W_L2_BYTES:
-        d.hints |= FICCO_HINT_B_EVICT_FIRST
+    # W stays evict_last even when it exceeds L2: the group's row blocks re-read each column tile
+    # (evict_first measured 2.3-4.6 % slower on C3 G2/G4, C3' and EP: r02_experiments/w_policy_ab.json)
     d.hints |= _agent_hint(comm_agent)
     low.notes = {"kind": kind.value, "rank": g, "world": G, "gathered": gathered, "inplace": inplace,
                  "comm_agent": comm_agent, "collective": sc.collective.value}
@@ -766,8 +766,7 @@ def lower_rs(scenario: Scenario, kind: ScheduleKind, rank: int, grid: int = 0, v
     d.k, d.alpha, d.grid, d.tile_n, d.cta_group = K, 1.0, grid, tn, cta_group
     if grouped_rs and os.environ.get("FICCO_A_EVICT_LAST", "auto") != "0":
         d.hints |= FICCO_HINT_A_EVICT_LAST  # the group's A slice stays in L2 while it sweeps N
-    if grouped_rs and N * K * ELT > W_L2_BYTES:
-        d.hints |= FICCO_HINT_B_EVICT_FIRST  # a W beyond L2 streams
+
     if not direct:
         d.hints |= _agent_hint(comm_agent)
     if len(units) >= 4096 - 1:

@@ -108,13 +108,13 @@ def test_large_w_row_groups_span_gates(kind):
 
 def test_rs_large_w_row_groups():
     """GEMM->RS at G = 2 (W 235 MB): the remote and own rows sweep N once per row group of 128-row blocks,
-    with A pinned and W streaming; every (row, col) of the partial is produced once."""
+    with A pinned (W evict_last too); every (row, col) of the partial is produced once."""
     M, N, K, G = 16384, 8192, 14336, 2
     sc = _scenario("c3", M, N, K, G)
     low = lower_rs(sc, ScheduleKind.HETERO_UNFUSED_1D, 0, virtual=True, comm_agent="core")
     sweeps = 1 + sum(1 for a, b in zip(low.tiles, low.tiles[1:]) if b.c_col < a.c_col)
     assert sweeps <= 2 * (M * K * 2 // (32 << 20)) + 2, sweeps
-    assert low.desc.hints & FICCO_HINT_A_EVICT_LAST and low.desc.hints & FICCO_HINT_B_EVICT_FIRST
+    assert low.desc.hints & FICCO_HINT_A_EVICT_LAST and not low.desc.hints & FICCO_HINT_B_EVICT_FIRST
 
 
 def test_pair_tiles_pads_unmatched_tiles_with_zero_row_partners():
