@@ -145,6 +145,12 @@ def time_steps(fn, steps: int, warmup: int, flush, stream, barrier=None) -> list
     return [a.elapsed_time(b) for a, b in evs]
 
 
+def coll_backend() -> str:
+    """The collective library behind torch.distributed here: NCCL, or gloo in the shared-GPU plumbing check."""
+    import torch
+    return "NCCL" if torch.distributed.get_backend() == "nccl" else "gloo (shared-GPU plumbing check)"
+
+
 def time_interleaved(fns, steps: int, warmup: int, flush, stream, barrier=None, starts=None) -> list[list[float]]:
     """time_steps for several step functions ROUND-ROBIN (step i of every fn before step i+1):
     the same clocks, power-cap state and L2 state (flushed before every call) for all of them,
@@ -258,7 +264,7 @@ class AGWorkload:
             def fn():
                 t.distributed.all_gather_into_tensor(self.gathered, self.local)
                 t.matmul(self.gathered, self.w.T, out=self.out)
-            return fn, "NCCL all_gather_into_tensor + cuBLAS"
+            return fn, f"{coll_backend()} all_gather_into_tensor + cuBLAS"
 
         def fn():
             for p in range(self.G):
@@ -377,7 +383,7 @@ class RSWorkload(AGWorkload):
             def fn():
                 t.matmul(self.a, self.w.T, out=self.part)
                 t.distributed.reduce_scatter_tensor(self.out, self.part)
-            return fn, "cuBLAS + NCCL reduce_scatter_tensor"
+            return fn, f"cuBLAS + {coll_backend()} reduce_scatter_tensor"
         R = self.R
 
         peers = t.stack(self.peer_parts)  # the received partials, contiguous like an NCCL receive buffer
@@ -496,7 +502,7 @@ class CPWorkload(AGWorkload):
             def fn():
                 t.distributed.all_gather_into_tensor(self.kall, self.local)
                 t.addmm(self.out, self.q, self.kall.T, beta=0, alpha=self.scale, out=self.out)
-            return fn, "NCCL all_gather_into_tensor + cuBLAS (alpha = 1/sqrt(d))"
+            return fn, f"{coll_backend()} all_gather_into_tensor + cuBLAS (alpha = 1/sqrt(d))"
 
         def fn():
             for p in range(self.G):
@@ -604,7 +610,7 @@ class EPWorkload(AGWorkload):
             def fn():
                 t.distributed.all_to_all_single(self.gathered, self.send)
                 t.matmul(self.gathered, self.w.T, out=self.out)
-            return fn, "NCCL all_to_all_single + cuBLAS"
+            return fn, f"{coll_backend()} all_to_all_single + cuBLAS"
 
         def fn():
             for p in range(self.G):
