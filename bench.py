@@ -662,7 +662,27 @@ class AG70Workload(AGWorkload):
         return 16384, 2 * 28672 // G, 8192
 
 
-WORKLOADS = {"c2": AGWorkload, "c3": RSWorkload, "c4": CPWorkload, "ep": EPWorkload, "c3p": AG70Workload}
+class C1Workload(AGWorkload):
+    """C1 (BASELINE.json configs[0]): the reference's CPU-runnable case, all-gather -> GEMM at
+    M = N = K = 4096 with 4 ranks. The oracle (the CPU baseline here) computes it in fp32, the GPU path in
+    bf16; the selector picks uniform_fused_2d (M <= K, heuristic.py:35)."""
+
+    key = "c1"
+    title = "C1 AG->GEMM 4096^3, 4 ranks (BASELINE configs[0])"
+    default_ranks = 4
+
+    @staticmethod
+    def shape(G):
+        return 4096, 4096, 4096
+
+
+WORKLOADS = {"c1": C1Workload, "c2": AGWorkload, "c3": RSWorkload, "c4": CPWorkload, "ep": EPWorkload,
+             "c3p": AG70Workload}
+
+
+def job_ranks(args) -> int:
+    """G of the N = 1 decomposition-only run: --virtual-ranks, else the workload's own (C1: 4), else 8."""
+    return args.virtual_ranks or getattr(WORKLOADS[args.workload], "default_ranks", G_VIRTUAL)
 
 
 def headline_choice(workload: str, G: int, args) -> tuple[str, str]:
@@ -680,9 +700,9 @@ def headline_choice(workload: str, G: int, args) -> tuple[str, str]:
 def workload_config(args, world: int) -> dict:
     """The JSON line's ``config`` (identical in both arms)."""
     cls = WORKLOADS[args.workload]
-    G = args.virtual_ranks if world == 1 else world
+    G = job_ranks(args) if world == 1 else world
     kind, agent = headline_choice(args.workload, G, args)
-    slot = args.input == "slot" and args.workload in ("c2", "c3p", "c4")
+    slot = args.input == "slot" and args.workload in ("c1", "c2", "c3p", "c4")
     return dict(workload=cls.title, ranks=G, virtual_peers=world == 1, schedule=kind, comm_agent=agent,
                 schedule_source=("--kind/--agent override" if (args.kind or args.agent) else
                                  "public API default: select_schedule on the B200 machine file; "
@@ -743,7 +763,7 @@ def our_arm(args) -> None:
     from paper_2512_10236_b200 import ops, routing, runtime
     runtime.load_library()
 
-    G = args.virtual_ranks if world == 1 else world
+    G = job_ranks(args) if world == 1 else world
     peaks, peaks_src = load_peaks()
     config = workload_config(args, world)
     best, best_agent = config["schedule"], config["comm_agent"]
@@ -1024,8 +1044,9 @@ def main() -> None:
     ap.add_argument("--kind", default="", help="override the headline schedule (default: the selector's choice)")
     ap.add_argument("--agent", default="", help="override the headline comm agent (default: the machine file's)")
     ap.add_argument("--headline-only", action="store_true", help="skip the all-variants table")
-    ap.add_argument("--virtual-ranks", type=int, default=G_VIRTUAL,
-                    help="N=1 only: the job size G this GPU plays rank 0 of (C3 is quoted at G = 2, 4 and 8)")
+    ap.add_argument("--virtual-ranks", type=int, default=0,
+                    help="N=1 only: the job size G this GPU plays rank 0 of (default 8; C1: 4; C3 is quoted at "
+                         "G = 2, 4 and 8)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
     ap.add_argument("--no-core", action="store_true", help="skip the comm_agent=core (SM copies) comparison")
     ap.add_argument("--input", default="slot", choices=["slot", "copy"],

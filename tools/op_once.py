@@ -1,6 +1,6 @@
 """Run one bench workload's overlapped op a few times (ncu target for the in-op tile kernel).
 
-usage: python tools/op_once.py c2|c3|c4|c3p|ep <kind> [dma|core] [calls] [G]
+usage: python tools/op_once.py c1|c2|c3|c4|c3p|ep <kind> [dma|core] [calls] [G]
 Under ncu the copy program runs before the kernel (profilers serialise), so the captured kernel
 is the op's tile program with its flags already satisfied.
 """
@@ -21,7 +21,7 @@ G = int(sys.argv[5]) if len(sys.argv) > 5 else bench.G_VIRTUAL
 runtime.load_library()
 wl = bench.WORKLOADS[key](torch, torch.device("cuda", 0), G, 0, 1, ops)
 wl.agent = agent
-wl.inplace = key in ("c2", "c3p", "c4")  # as the bench runs them (zero-copy input slot)
+wl.inplace = key in ("c1", "c2", "c3p", "c4")  # as the bench runs them (zero-copy input slot)
 grp = ops.FiccoGroup.virtual_group(G, 0)
 wl.prepare(grp, kind)
 fn = wl.step(grp, kind)

@@ -20,10 +20,15 @@ sys.path.insert(0, ROOT)
 import bench  # noqa: E402
 from paper_2512_10236_b200 import ops, runtime  # noqa: E402
 
-CASES = [("c2", k, a) for k in ("shard_overlap_p2p", "uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d",
-                                "uniform_fused_2d", "serial") for a in ("dma", "core")]
-CASES += [("c3", k, a) for k in ("uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d") for a in ("dma", "core")]
-CASES += [("c4", k, "dma") for k in ("shard_overlap_p2p", "hetero_unfused_1d", "uniform_fused_1d")]
+CASES = [("c2", k, a, False) for k in ("shard_overlap_p2p", "uniform_fused_1d", "hetero_fused_1d",
+                                        "hetero_unfused_1d", "uniform_fused_2d", "serial") for a in ("dma", "core")]
+CASES += [("c3", k, a, False) for k in ("uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d", "uniform_fused_2d",
+                                        "shard_overlap_p2p", "serial") for a in ("dma", "core")]
+CASES += [("c4", k, "dma", False) for k in ("shard_overlap_p2p", "hetero_unfused_1d", "uniform_fused_1d")]
+# the bench headlines' own paths: symmetric-slot inputs (zero-copy publish), C1 at 4 ranks, C3'
+CASES += [("c2", "hetero_unfused_1d", "dma", True), ("c4", "hetero_unfused_1d", "dma", True),
+          ("c3p", "hetero_unfused_1d", "dma", True)]
+CASES += [("c1", k, "dma", True) for k in ("uniform_fused_2d", "hetero_unfused_1d", "shard_overlap_p2p")]
 
 
 def main():
@@ -34,13 +39,16 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     res = {}
     wls = {}
-    for key, kind, agent in CASES:
+    for key, kind, agent, inplace in CASES:
+        G = getattr(bench.WORKLOADS[key], "default_ranks", bench.G_VIRTUAL)
         if key not in wls:
-            wls[key] = bench.WORKLOADS[key](torch, dev, bench.G_VIRTUAL, 0, 1, ops)
+            wls[key] = bench.WORKLOADS[key](torch, dev, G, 0, 1, ops)
         wl = wls[key]
-        grp = ops.FiccoGroup.virtual_group(bench.G_VIRTUAL, 0)
+        grp = ops.FiccoGroup.virtual_group(G, 0)
+        name = f"{key}/{kind}/{agent}" + ("/slot" if inplace else "")
         try:
             wl.agent = agent
+            wl.inplace = inplace
             wl.prepare(grp, kind)
             step = wl.step(grp, kind)
             step()
@@ -55,13 +63,13 @@ def main():
                 bad += (wl.out != ref).any().to(torch.int64)
             grp.comm.check()
             nbad = int(bad.item())
-            res[f"{key}/{kind}/{agent}"] = {"first_call_check": ok0, "calls": iters, "mismatching_calls": nbad,
-                                           "seconds": round(time.time() - t0, 2)}
+            res[name] = {"first_call_check": ok0, "calls": iters, "mismatching_calls": nbad,
+                         "seconds": round(time.time() - t0, 2)}
         except Exception as exc:
-            res[f"{key}/{kind}/{agent}"] = {"error": repr(exc)[:300]}
+            res[name] = {"error": repr(exc)[:300]}
         finally:
             grp.close()
-        print(f"{key}/{kind}/{agent}", res[f"{key}/{kind}/{agent}"], flush=True)
+        print(name, res[name], flush=True)
     total_bad = sum(v.get("mismatching_calls", 1) for v in res.values())
     print("TOTAL mismatching calls:", total_bad, flush=True)
     if out_path:
