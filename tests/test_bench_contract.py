@@ -29,7 +29,7 @@ def test_bench_line_has_the_contract_keys(path):
     assert not {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"} & set(d["clocks"]["reasons"])
 
 
-@pytest.mark.parametrize("path", sorted((ROOT / "profiles").glob("r0*_bench_reference_arm.json")),
+@pytest.mark.parametrize("path", sorted((ROOT / "profiles").glob("r0*_bench*reference_arm.json")),
                          ids=lambda p: p.stem)
 def test_reference_arm_line(path):
     d = json.loads(path.read_text().splitlines()[0])
