@@ -1188,7 +1188,8 @@ int ficco_gemm_bf16_cfg(const void* a, const void* b, void* c, int64_t m, int64_
     int r = ficco_comm_create(0, 1, &w, FICCO_WS_DATA_OFFSET, 1, &cm);
     if (r) return r;
     int tn = tile_n;
-    if (tn == 0) {  // tile width minimising (waves x width) over the instantiated widths
+    if (tn == 0) {  // tile width minimising waves x (width + 512) (lowering.choose_tile_n: a tile's A slab
+                    // streams through L2 -> SMEM whatever its width)
       double best = 1e30;
       const int widths[] = {256, 224, 192, 160, 128};
       const int units = cm->sms / cta_group;
@@ -1196,7 +1197,7 @@ int ficco_gemm_bf16_cfg(const void* a, const void* b, void* c, int64_t m, int64_
         const int64_t tiles_n = (n + wdt - 1) / wdt;
         const int64_t tiles_m = ((m + ficco::BM - 1) / ficco::BM + cta_group - 1) / cta_group;
         const int64_t waves = (tiles_n * tiles_m + units - 1) / units;
-        const double cost = double(waves) * wdt * (1.0 + 0.02 * (256.0 / wdt));
+        const double cost = double(waves) * (wdt + 512);
         if (cost < best - 1e-9) {
           best = cost;
           tn = wdt;

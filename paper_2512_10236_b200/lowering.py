@@ -171,17 +171,21 @@ def pair_tiles(tiles: list[Tile]) -> list[Tile]:
 
 
 def choose_tile_n(tiles_for_width, sms: int = B200_SMS) -> int:
-    """Tile width (UMMA N, B box rows) minimising persistent-kernel waves x width.
+    """Tile width (UMMA N, B box rows) minimising persistent-kernel waves x wave time.
 
     ``tiles_for_width(w)`` is the tile count at width w. A wave of the
-    persistent kernel is ``sms`` tiles; its duration scales with w, plus a
-    small per-tile fixed cost (prologue/epilogue). E.g. C2's N = 3584 at 256
-    gives 896 tiles = 6.05 waves (7 issued), at 224 gives 1024 tiles = 6.92.
+    persistent kernel is ``sms`` tiles. A wave does NOT get proportionally
+    shorter with narrower tiles: every tile streams its full 256 x K slab of A
+    through L2 -> SMEM whatever its width, so a tile costs about w + 512
+    (measured, interleaved: 8192^3 takes 720 / 795 / 904 / 1059 / 1266 us at
+    w = 256 / 224 / 192 / 160 / 128; profiles/r02_experiments/tile_width_ab.json).
+    E.g. C2's N = 3584 at 256 gives 896 tiles = 6.05 waves (7 issued), at 224
+    1024 tiles = 6.92 -> 224; 4096^3 at 256 is 3.5 waves -> 256 (not 128).
     """
     best, best_w = None, TILE_WIDTHS[0]
     for w in TILE_WIDTHS:
         n = tiles_for_width(w)
-        cost = -(-n // sms) * w * (1.0 + 0.02 * 256 / w)
+        cost = -(-n // sms) * (w + 512)
         if best is None or cost < best - 1e-9:
             best, best_w = cost, w
     return best_w
