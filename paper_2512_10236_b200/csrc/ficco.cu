@@ -286,6 +286,7 @@ struct ficco_plan {
   // 167.9 -> 165.9 us); every GPU test, multi-process ones included, passes in both modes.
   // FICCO_KERNEL_IN_GRAPH=1 makes the kernel a node of the run's graph instead.
   bool kernel_in_graph = false;
+  bool counter_waits = false;           // the copy program waits on tile counters (RS dma pushes)
   int tile_n = 256;                     // tile width (UMMA N)
   int epi_bufs = 1;                     // epilogue staging buffers per warp (epi_bufs_for)
   bool has_remote = false;              // STORE_REMOTE tiles: peers' receive slots are TMA store targets
@@ -994,6 +995,7 @@ int ficco_plan_create(ficco_comm_t* c, const ficco_plan_desc* d, ficco_plan_t** 
   p->comm = c;
   p->desc = *d;
   p->ops.assign(d->ops, d->ops + d->n_ops);
+  for (const ficco_copy_op& op : p->ops) p->counter_waits |= op.op == FICCO_OP_WAIT_COUNTER;
   p->desc.ops = nullptr;
   p->desc.tiles = nullptr;
   p->n_tiles = d->n_tiles;
@@ -1092,13 +1094,23 @@ int ficco_plan_run(ficco_plan_t* p, const void* a, const void* b, void* c, void*
   }
   // Kernel first, then the copy graph: the kernel is dispatched before any of the graph's
   // stream-wait nodes exists, so a blocked wait can never hold back the kernel that satisfies it.
+  // FICCO_GRAPH_FIRST=1 (A/B knob) launches the graph first when its copy program never waits on
+  // the kernel (no tile-counter waits).
   ficco_comm* cm = p->comm;
   cudaStream_t gs = cm->copy[FICCO_MAX_STREAMS - 1];  // graph launch stream (idle between runs)
+  const char* gf = getenv("FICCO_GRAPH_FIRST");
+  const bool graph_first = gf && gf[0] == '1' && !p->counter_waits;
   CK(cudaEventRecord(cm->ev_fork, s));
+  if (graph_first) {
+    CK(cudaStreamWaitEvent(gs, cm->ev_fork, 0));
+    CK(cudaGraphLaunch(gi.exec, gs));
+  }
   if ((r = launch_tiles(p, parity, a, b, c, s))) return r;
   if (p->kernel_event) CK(cudaEventRecord(p->kernel_event, s));  // completes with the tile kernel
-  CK(cudaStreamWaitEvent(gs, cm->ev_fork, 0));
-  CK(cudaGraphLaunch(gi.exec, gs));
+  if (!graph_first) {
+    CK(cudaStreamWaitEvent(gs, cm->ev_fork, 0));
+    CK(cudaGraphLaunch(gi.exec, gs));
+  }
   CK(cudaEventRecord(cm->ev_join[0], gs));
   CK(cudaStreamWaitEvent(s, cm->ev_join[0], 0));
   return 0;
