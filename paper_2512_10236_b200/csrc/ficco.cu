@@ -1092,14 +1092,16 @@ int ficco_plan_run(ficco_plan_t* p, const void* a, const void* b, void* c, void*
     CK(cudaGraphLaunch(gi.exec, s));
     return 0;
   }
-  // Kernel first, then the copy graph: the kernel is dispatched before any of the graph's
-  // stream-wait nodes exists, so a blocked wait can never hold back the kernel that satisfies it.
-  // FICCO_GRAPH_FIRST=1 (A/B knob) launches the graph first when its copy program never waits on
-  // the kernel (no tile-counter waits).
+  // Launch order. A copy program that waits on tile counters (GEMM -> RS with copy-engine pushes, NVLS)
+  // goes after the kernel: the kernel is then dispatched before any of the graph's stream-wait nodes
+  // exists, so a blocked wait can never hold back the kernel that satisfies it. Every other copy
+  // program waits only on peers' copy programs, so it goes first and its copies start earlier
+  // (C2 hetero_unfused_1d -1.6 / -2.1 %, others unchanged: profiles/r02_experiments/graph_first_ab.json).
+  // FICCO_GRAPH_FIRST=0 restores kernel-first for every plan.
   ficco_comm* cm = p->comm;
   cudaStream_t gs = cm->copy[FICCO_MAX_STREAMS - 1];  // graph launch stream (idle between runs)
   const char* gf = getenv("FICCO_GRAPH_FIRST");
-  const bool graph_first = gf && gf[0] == '1' && !p->counter_waits;
+  const bool graph_first = !(gf && gf[0] == '0') && !p->counter_waits;
   CK(cudaEventRecord(cm->ev_fork, s));
   if (graph_first) {
     CK(cudaStreamWaitEvent(gs, cm->ev_fork, 0));
