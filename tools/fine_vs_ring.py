@@ -23,7 +23,7 @@ def main():
     runtime.load_library()
     dev = torch.device("cuda", 0)
     wl = bench.WORKLOADS[key](torch, dev, 8, 0, 1, ops)
-    wl.inplace = key == "c2"
+    wl.inplace = key in ("c2", "c4")  # as the bench runs them (zero-copy input slot)
     wl.agent = agent
     grp = ops.FiccoGroup.virtual_group(8, 0)
     flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -61,6 +61,10 @@ def main():
             waits.append(wait / grid)
             last_per_cta = [max(done[t] for t in range(c, info["tiles"], grid)) for c in range(grid)]
             tails.append(max(last_per_cta) - min(last_per_cta))
+            first_ready = [ready[c] if c < info["tiles"] else 0.0 for c in range(grid)]
+            late = sorted(range(grid), key=lambda c: -last_per_cta[c])[:8]
+            late_ctas = [(c, round(last_per_cta[c], 1), round(first_ready[c], 1),
+                          len(range(c, info["tiles"], grid))) for c in late]
             gate_open = {}
             for i, tl in enumerate(low.tiles):
                 if tl.flag >= 0 and tl.rows > 0:
@@ -77,7 +81,8 @@ def main():
         res[k] = {"op_us": round(statistics.median(ts) * 1e3, 1), "kernel_span_us": round(statistics.median(spans), 1),
                   "mean_cta_gate_wait_us": round(statistics.median(waits), 2),
                   "cta_finish_spread_us": round(statistics.median(tails), 1), "copy_program_us": copy_us,
-                  "first_gate_opens_us": opens[-1], "tiles": info["tiles"], "copy_ops": len(low.ops)}
+                  "first_gate_opens_us": opens[-1], "tiles": info["tiles"], "copy_ops": len(low.ops),
+                  "latest_ctas (cta, done_us, first_tile_ready_us, tiles)": late_ctas}
         print(k, res[k], flush=True)
     grp.close()
     with open(os.path.join(ROOT, "gpurun_out", f"fine_vs_ring_{key}_{agent}.json"), "w") as f:

@@ -6,7 +6,8 @@ Per schedule kind, with the bench's exact call (L2 flushed before every call):
   post  = op end - last tile stored (copy-stream joins, flag clears)
 op start/end are %globaltimer stamps (runtime.timestamp) on the caller's stream right before and
 after the op; the kernel's stamps come from the plan trace (ficco_plan_set_trace). Medians of reps.
-Usage: python tools/op_timeline.py [c2|c3|c4] [reps] [--copy]
+Usage: python tools/op_timeline.py [c2|c3|c4] [reps] [--copy] [--ahead: a GPU sleep first, so host enqueue
+time is hidden as in the bench loop]
 """
 import json
 import os
@@ -28,8 +29,8 @@ def main():
     runtime.load_library()
     dev = torch.device("cuda", 0)
     wl = bench.WORKLOADS[key](torch, dev, bench.G_VIRTUAL, 0, 1, ops)
-    if key == "c2" and "--copy" not in sys.argv:
-        wl.inplace = True
+    if key in ("c2", "c4") and "--copy" not in sys.argv:
+        wl.inplace = True  # as the bench runs them (zero-copy input slot)
     grp = ops.FiccoGroup.virtual_group(bench.G_VIRTUAL, 0)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stamps = torch.zeros(2, dtype=torch.int64, device=dev)
@@ -45,7 +46,7 @@ def main():
         elif key == "c3":
             plan = ops.prepare_rs(grp, wl.M, wl.K, wl.N, kind)[0]
         else:
-            plan = ops.prepare_cp(grp, wl.Tq, wl.d, wl.Tkv, kind)[0]
+            plan = ops.prepare_cp(grp, wl.Tq, wl.d, wl.Tkv, kind, inplace=wl.inplace)[0]
         info = plan.info()
         g, nt = info["grid"], info["tiles"]
         trace = torch.zeros(g + 2 * nt, dtype=torch.int64, device=dev)
@@ -54,6 +55,8 @@ def main():
         torch.cuda.synchronize()
         rows = []
         for _ in range(reps):
+            if "--ahead" in sys.argv:  # the host runs ahead of the GPU (as in the bench loop)
+                torch.cuda._sleep(1000000)
             flush.fill_(1)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
@@ -71,6 +74,23 @@ def main():
         med = [round(statistics.median(r[i] for r in rows), 1) for i in range(4)]
         out[kind] = {"pre_us": med[0], "span_us": med[1], "post_us": med[2], "event_us": med[3]}
         print(kind, out[kind], flush=True)
+    # the plain tile GEMM of the same shape between the same stamps (no trace: pre + span + post)
+    kfn = wl.kernel(runtime)[0]
+    kfn()
+    torch.cuda.synchronize()
+    rows = []
+    for _ in range(reps):
+        if "--ahead" in sys.argv:
+            torch.cuda._sleep(1000000)
+        flush.fill_(1)
+        runtime.timestamp(stamps[0:1])
+        kfn()
+        runtime.timestamp(stamps[1:2])
+        torch.cuda.synchronize()
+        s0, s1 = stamps.cpu().tolist()
+        rows.append((s1 - s0) / 1e3)
+    out["plain_gemm_stamp_to_stamp_us"] = round(statistics.median(rows), 1)
+    print("plain GEMM stamp to stamp", out["plain_gemm_stamp_to_stamp_us"], flush=True)
     grp.comm.check()
     print(json.dumps(out))
     grp.close()
