@@ -64,6 +64,7 @@ class FiccoGroup:
         self._ws_bytes = 0
         self.device: int | None = None  # CUDA device of the workspaces (set with the first workspace)
         self._mc = None                  # runtime.Multicast: the NVLS workspace (comm_agent = nvls), lazily
+        self._ws_views: dict = {}        # rank -> uint8 view of its whole workspace (this communicator's)
 
     @classmethod
     def virtual_group(cls, world: int, rank: int = 0) -> "FiccoGroup":
@@ -129,6 +130,7 @@ class FiccoGroup:
         """
         if self.comm is None:
             return
+        self._ws_views.clear()
         torch.cuda.synchronize()
         self._barrier()
         for plan, _ in self._plans.values():
@@ -150,13 +152,18 @@ class FiccoGroup:
         return hit
 
     def ws_tensor(self, rank: int, offset: int, shape, dtype=torch.bfloat16) -> torch.Tensor:
-        """A torch view of (part of) a workspace (local, or a virtual peer's)."""
-        numel = math.prod(shape)
-        nbytes = numel * torch.tensor([], dtype=dtype).element_size()
+        """A torch view of (part of) a workspace (local, or a virtual peer's).
+
+        Views are slices of one byte tensor per workspace, wrapped once per communicator: wrapping a raw
+        pointer costs ~40 us of host time, slicing a few (input_slot / kv_slot run before every call)."""
+        nbytes = math.prod(shape) * dtype.itemsize
         if offset + nbytes > self._ws_bytes:
             raise ValueError("view exceeds workspace")
-        ptr = self.comm.ws_ptrs[rank] + offset
-        return _wrap_device_ptr(ptr, shape, dtype)
+        whole = self._ws_views.get(rank)
+        if whole is None:
+            whole = _wrap_device_ptr(self.comm.ws_ptrs[rank], (self._ws_bytes,), torch.uint8)
+            self._ws_views[rank] = whole
+        return whole[offset:offset + nbytes].view(dtype).view(*shape)
 
     def input_slot(self, rows: int, cols: int, n_out: int, kind=None) -> torch.Tensor:
         """This rank's slot of the gathered buffer for the NEXT all_gather_matmul call.
@@ -236,7 +243,7 @@ def _wrap_device_ptr(ptr: int, shape, dtype) -> torch.Tensor:
         pass
 
     h = _Holder()
-    nbytes = math.prod(shape) * torch.tensor([], dtype=dtype).element_size()
+    nbytes = math.prod(shape) * dtype.itemsize
     h.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3,
                                   "strides": None}
     raw = torch.as_tensor(h, device=torch.device("cuda", torch.cuda.current_device()))
