@@ -278,6 +278,20 @@ struct ficco_plan {
   std::vector<std::pair<cudaGraphNode_t, int>> captured_reduces;
   unsigned long long* trace = nullptr;  // optional device timeline buffer
   cudaEvent_t kernel_event = nullptr;   // optional: recorded on the launch stream right after the tile kernel
+  // Kernel parameters of the last direct launch per workspace parity: reused while the call arguments,
+  // the trace buffer and the launch-time knobs are unchanged (encoding the ~10-40 TMA descriptors is
+  // most of an op's host time)
+  struct ParamCache {
+    bool valid = false;
+    const void* a = nullptr;
+    const void* b = nullptr;
+    void* c = nullptr;
+    unsigned long long* trace = nullptr;
+    std::string knobs;
+    int grid = 0;
+    ficco::TileParams prm;
+  };
+  ParamCache pcache[2];
   bool concurrent = true;               // false: copies complete before the kernel starts (profilers)
   // Default: the tile kernel is launched directly on the caller's stream, THEN the copy-only
   // graph on a side stream (kernel first: it is queued before any of the graph's stream-wait
@@ -639,15 +653,35 @@ int make_params(ficco_plan* p, uint32_t parity, const void* a, const void* b, vo
   return 0;
 }
 
+// The launch-time knobs make_params reads (experiments toggle them between calls).
+std::string knob_fingerprint() {
+  static const char* const names[] = {"FICCO_B_RESIDENT", "FICCO_PART_HINT", "FICCO_RS_MMA", "FICCO_RS_ALIAS",
+                                      "FICCO_FLAG_TIMEOUT_S", "FICCO_OUT_HINT", "FICCO_EPI_FAST", "FICCO_B_HINT"};
+  std::string f;
+  for (const char* n : names) {
+    const char* v = getenv(n);
+    f += v ? v : "\x01";
+    f += '\x02';
+  }
+  return f;
+}
+
 int launch_tiles(ficco_plan* p, uint32_t parity, const void* a, const void* b, void* c, cudaStream_t s) {
   if (p->n_tiles == 0) return 0;
   int r = configure_kernels(p->comm->device);
   if (r) return r;
-  ficco::TileParams prm;
   int grid, smem, b_rows;
   const void* fn;
   if ((r = kernel_for(p->tile_n, p->cta_group, p->epi_bufs, &fn, &smem, &b_rows))) return r;
-  if ((r = make_params(p, parity, a, b, c, &prm, &grid))) return r;
+  ficco_plan::ParamCache& pc = p->pcache[parity & 1u];
+  std::string knobs = knob_fingerprint();
+  if (!(pc.valid && pc.a == a && pc.b == b && pc.c == c && pc.trace == p->trace && pc.knobs == knobs)) {
+    pc.valid = false;
+    if ((r = make_params(p, parity, a, b, c, &pc.prm, &pc.grid))) return r;
+    pc.a = a, pc.b = b, pc.c = c, pc.trace = p->trace, pc.knobs = std::move(knobs), pc.valid = true;
+  }
+  ficco::TileParams& prm = pc.prm;
+  grid = pc.grid;
   void* args[] = {&prm};
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
@@ -1270,6 +1304,8 @@ int ficco_gemm_bf16_cfg(const void* a, const void* b, void* c, int64_t m, int64_
   p->desc.c = ficco_operand{FICCO_BUF_C, 0, 0, 0, m, n};
   p->desc.k = k;
   p->epi_bufs = epi_bufs_for(k);
+  const float prev_alpha = p->desc.alpha;
+  const uint32_t prev_hints = p->desc.hints;
   p->desc.alpha = alpha;
   {
     const char* env = getenv("FICCO_A_EVICT_LAST");  // "0" / "1" override the size rule (A/B experiments)
@@ -1281,6 +1317,8 @@ int ficco_gemm_bf16_cfg(const void* a, const void* b, void* c, int64_t m, int64_
     // evict_first lost those hits (2.3-4.6 % slower on C3 G2/G4, C3', EP; r02_experiments/w_policy_ab.json)
     p->desc.hints = pin ? FICCO_HINT_A_EVICT_LAST : 0;
   }
+  if (p->desc.alpha != prev_alpha || p->desc.hints != prev_hints)  // the cached kernel params bake both in
+    p->pcache[0].valid = p->pcache[1].valid = false;
   return ficco_plan_run_parts(p, a, b, c, stream, 0, 1);  // no flags: direct launch
 }
 
