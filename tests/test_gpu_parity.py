@@ -54,6 +54,28 @@ def test_tile_gemm_alpha_and_grid(lib):
     np.testing.assert_allclose(_np(out), 0.125 * (a @ w.T), rtol=RTOL, atol=ATOL)
 
 
+def test_cached_kernel_params_follow_alpha_and_knobs(lib, monkeypatch):
+    """The library reuses a plan's kernel parameters while the call is unchanged: a new alpha on the same
+    buffers, or a launch-time knob toggled between calls, must still take effect (bit-exact per setting)."""
+    a = orc.seeded_inputs(4, 0, (512, 256))
+    w = orc.seeded_inputs(4, 1, (512, 256), "normal")
+    ta, tw = _t(a), _t(w)
+    out = torch.empty(512, 512, dtype=torch.bfloat16, device="cuda")
+    outs = {}
+    for alpha in (1.0, 0.5, 1.0, 0.25):
+        lib.gemm_bf16(ta, tw, out, alpha=alpha)
+        torch.cuda.synchronize()
+        np.testing.assert_allclose(_np(out), alpha * (a @ w.T), rtol=RTOL, atol=ATOL)
+        if alpha in outs:
+            assert torch.equal(outs[alpha], out)
+        outs[alpha] = out.clone()
+    for knob in ("0", "1", "0"):  # straight-line vs generic epilogue: same bits
+        monkeypatch.setenv("FICCO_EPI_FAST", knob)
+        lib.gemm_bf16(ta, tw, out)
+        torch.cuda.synchronize()
+        assert torch.equal(out, outs[1.0])
+
+
 AG_KINDS = ["serial", "shard_overlap_p2p", "uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d",
             "uniform_fused_2d"]
 
