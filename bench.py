@@ -644,10 +644,14 @@ class EPWorkload(AGWorkload):
         return fn, self.M * self.K * 2, self.M * self.N * 2
 
     def cpu_op(self, orc, kind):
-        a = self.t.cat(self.blocks)[:self.M // 16].float().cpu().numpy()
+        import numpy as np
+        blocks = [b.float().cpu().numpy() for b in self.blocks]
         w = self.w.float().cpu().numpy()
-        return (lambda: a @ w.T, f"numpy fp32 expert GEMM of 1/16 of the {self.M} dispatched rows (the whole op is "
-                                 f"~35 TFLOP, ~45 s on the host); value scaled x16", 1 / 16)
+        sink = np.empty((self.R, self.N), dtype=np.float32)
+        return (lambda: orc.execute_a2a_rank(kind, blocks, w, self.rank, sink),
+                f"oracle execute_a2a_rank({kind}), rank {self.rank}'s whole op: the {self.G} dispatched blocks "
+                f"routed by the plan, every GemmSpec fragment (~35 TFLOP, fp32 numpy BLAS) into a [{self.R}, "
+                f"{self.N}] staging block (the 17 GB fp32 output is not kept)", 1.0)
 
 
 class AG70Workload(AGWorkload):

@@ -52,4 +52,4 @@ def test_round2_line_reports_the_in_op_kernel_and_the_api_default(path):
     assert abs(r["work_per_launch"] / (r["kernel_us"] * 1e-6) / (1e12 if r["unit"] == "TFLOP/s" else 1e9)
                - r["achieved"]) / r["achieved"] < 1e-3
     if d["cpu_baseline"] is not None:
-        assert "scaled" not in d["cpu_baseline"]["sample"] or "x16" in d["cpu_baseline"]["sample"]
+        assert "scaled" not in d["cpu_baseline"]["sample"] or d["config"]["workload"].startswith("EP")

@@ -101,6 +101,28 @@ def test_a2a_dispatch_routes_each_block_to_its_rank(kind):
         np.testing.assert_allclose(outs[g], want @ ws[g].T, rtol=1e-5, atol=1e-4)
 
 
+@pytest.mark.parametrize("kind", ["serial", "hetero_unfused_1d", "uniform_fused_2d"])
+def test_a2a_rank_sample_computes_the_last_fragment(kind):
+    """execute_a2a_rank (the EP CPU baseline) routes and computes every fragment into an R-row sink:
+    after the call the sink holds the plan's last computed piece, equal to the same rows of execute_a2a."""
+    G, R, K, N, g = 4, 64, 128, 32, 2
+    sends = [orc.seeded_inputs(5, p, (G * R, K)) for p in range(G)]
+    ws = [orc.seeded_inputs(6, p, (N, K), "normal") for p in range(G)]
+    disp, _ = orc.execute_a2a(kind, sends, ws)
+    blocks = [sends[p][g * R:(g + 1) * R] for p in range(G)]
+    sink = orc.execute_a2a_rank(kind, blocks, ws[g], g)
+    rows, col_block = orc.gemm_fragments(kind, G * R, K, G, g)[-1]
+    if col_block is not None:  # the last K block's product for the last R rows
+        k0, kb = col_block
+        want = disp[g][-R:, k0:k0 + kb] @ ws[g][:, k0:k0 + kb].T
+        np.testing.assert_allclose(sink, want, rtol=1e-5, atol=1e-4)
+    else:
+        start, count = rows[-1]
+        last = list(range(start, start + count, R))[-1]
+        n = min(R, start + count - last)
+        np.testing.assert_allclose(sink[:n], disp[g][last:last + n] @ ws[g].T, rtol=1e-5, atol=1e-4)
+
+
 def test_a2a_plans_equal_all_gather_plans():
     """The reference's planner never reads the collective: the product planner
     gives an EP all_to_all scenario the same task list as the all_gather scenario."""
