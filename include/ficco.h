@@ -202,7 +202,8 @@ int ficco_ipc_get_handle(void* ptr, void* out_handle);
 int ficco_ipc_open(const void* handle, void** out);
 int ficco_ipc_close(void* ptr);
 
-/* communicator: ws[r] = rank r's workspace as mapped in this process.
+/* communicator (replaces the interconnect model topology.Topology, overlap_sim/topology.py:20-47):
+ * ws[r] = rank r's workspace as mapped in this process.
  * virtual_peers=1: a single process plays rank `rank` of `world`; peers'
  * workspaces are local allocations and cross-rank waits/notifies are
  * satisfied locally (decomposition-only mode). */
@@ -210,21 +211,25 @@ int ficco_comm_create(int rank, int world, void* const* ws, size_t ws_bytes, int
                       ficco_comm_t** out);
 int ficco_comm_destroy(ficco_comm_t* comm);
 int ficco_comm_epoch(ficco_comm_t* comm, uint32_t* runs); /* runs started so far */
-/* blocks until all work of the communicator finished; FICCO_ETIMEOUT if a kernel hit its flag timeout */
+/* blocks until all work of the communicator finished; FICCO_ETIMEOUT if a kernel hit its flag timeout
+ * (raised as the reference's engine.DeadlockError, overlap_sim/engine.py:35-36, 231-236) */
 int ficco_comm_check(ficco_comm_t* comm, void* stream);
 /* set local flag words [first, first+count) (absolute word index) to value, stream-ordered on `stream` */
 int ficco_comm_set_flags(ficco_comm_t* comm, int first, int count, uint32_t value, void* stream);
 
-/* plans */
+/* plans: one rank's share of planner.build_plan's ExecutionPlan (overlap_sim/planner.py:409, DAG payloads
+ * planner.py:58-113), lowered to a copy program + tile list by paper_2512_10236_b200/lowering.py */
 int ficco_plan_create(ficco_comm_t* comm, const ficco_plan_desc* desc, ficco_plan_t** out);
 int ficco_plan_destroy(ficco_plan_t* plan);
-/* One execution, replayed from a CUDA graph (one per flag/workspace parity,
+/* One execution (executes what engine.simulate prices, overlap_sim/engine.py:117-297), replayed from a
+ * CUDA graph (one per flag/workspace parity,
  * instantiated on first use, kernel/copy nodes re-pointed when a/b/c change):
  * run-local flag reset, copy program on the copy streams and the tile kernel,
  * all joined into `stream`. Advances the comm's run counter. Non-blocking. */
 int ficco_plan_run(ficco_plan_t* plan, const void* a, const void* b, void* c, void* stream);
 /* Same semantics enqueued directly on streams (no graph); run_copies / run_tiles
- * select the halves (calibration of DIL/CIL; a tile half alone only terminates if
+ * select the halves (calibration of the loss model's DIL/CIL tables, overlap_sim/lossmodel.py:85-108,
+ * engine.base_duration engine.py:76-103; a tile half alone only terminates if
  * its flags are satisfied). run_tiles = 2: serialised — the kernel launches after
  * the whole copy program (for kernel profilers that serialise work). */
 int ficco_plan_run_parts(ficco_plan_t* plan, const void* a, const void* b, void* c, void* stream,
@@ -274,7 +279,8 @@ int ficco_mc_reduce_bf16(const void* mc_src, void* dst, int64_t rows, int64_t co
 /* stand-alone primitives (calibration, benchmarks) */
 int ficco_gemm_bf16(const void* a, const void* b, void* c, int64_t m, int64_t n, int64_t k, float alpha,
                     int grid, void* stream);
-/* tile_n 0 / cta_group 0: automatic (waves x width model, CTA pairs) */
+/* tile_n 0 / cta_group 0: automatic (waves x (width + 512) model, CTA pairs); the GEMM task price
+ * flops / effective_flops of engine.py:86-93 measured instead of modelled */
 int ficco_gemm_bf16_cfg(const void* a, const void* b, void* c, int64_t m, int64_t n, int64_t k, float alpha,
                         int grid, int tile_n, int cta_group, void* stream);
 int ficco_copy_batch(void* const* dsts, const void* const* srcs, const size_t* sizes, size_t count,
