@@ -250,6 +250,17 @@ def _publish(ops: list, g: int, world: int, row_bytes: int, shard_rows: int, gat
     ops.append(_op(OP_RECORD, value=EV_START, stream=0))
 
 
+def slab_split(G: int) -> int:
+    """Copy-engine chains per uniform_fused_2d slab (FICCO_2D_SPLIT, default 1): each R x b slab pull is
+    cut into that many row blocks on parallel copy streams, joined before the slab's XFER flag
+    (strided 2D copies run at about half the 1D rate on one engine)."""
+    want = int(os.environ.get("FICCO_2D_SPLIT", "1"))
+    return max(1, min(want, (MAX_WORLD - 2) // max(1, G - 1)))
+
+
+EV_SLAB = 40     # + peer chain * (split - 1) + part - 1: uniform_fused_2d slab-part landed (slab_split > 1)
+
+
 def fine_chains() -> int:
     """Copy-engine chains of the fine-grain AG copy programs (FICCO_FINE_CHAINS, default 0 = one per peer)."""
     return max(0, min(15, int(os.environ.get("FICCO_FINE_CHAINS", "0"))))
@@ -387,9 +398,23 @@ def lower_ag(plan: ExecutionPlan, rank: int, gathered: str = "A", alpha: float =
                 off = low.gather_off + x.src * R * row_bytes + c * b * ELT
                 src, spar = (low.send_off + g * R * row_bytes + c * b * ELT, low.send_par) if a2a else \
                     (off, low.gather_par)
-                ops.append(_op(OP_COPY, peer=x.src, src_buf=BUF_WS, dst_buf=BUF_WS, src_off=src, dst_off=off,
-                               src_par=spar, dst_par=low.gather_par, width=b * ELT, height=R,
-                               src_pitch=row_bytes, dst_pitch=row_bytes, stream=st))
+                split = slab_split(G)
+                bounds = [R * j // split for j in range(split + 1)]
+                chain = st - 1
+                for j in range(split - 1, -1, -1):  # helper parts first, the chain's own part last
+                    sj = st + j * (G - 1)
+                    if j and sj not in started:
+                        ops.append(_op(OP_STREAM_WAIT, value=EV_START, stream=sj))
+                        started.add(sj)
+                    h = bounds[j + 1] - bounds[j]
+                    ops.append(_op(OP_COPY, peer=x.src, src_buf=BUF_WS, dst_buf=BUF_WS,
+                                   src_off=src + bounds[j] * row_bytes, dst_off=off + bounds[j] * row_bytes,
+                                   src_par=spar, dst_par=low.gather_par, width=b * ELT, height=h,
+                                   src_pitch=row_bytes, dst_pitch=row_bytes, stream=sj))
+                    if j:
+                        ops.append(_op(OP_RECORD, value=EV_SLAB + chain * (split - 1) + j - 1, stream=sj))
+                for j in range(1, split):
+                    ops.append(_op(OP_STREAM_WAIT, value=EV_SLAB + chain * (split - 1) + j - 1, stream=st))
             else:
                 r = M // (G * G)
                 ops.append(pull(x.src, x.src * R + c * r, r, st))

@@ -201,8 +201,18 @@ class World:
             self.on_run_start(g, st["run"])
         low = self.low[g]
         streams: dict[int, list] = {}
-        for op in low.ops:
+        # event semantics of stream capture: a STREAM_WAIT binds to the latest RECORD of its slot that
+        # precedes it in enqueue (list) order, so event slots may be reused
+        last_rec: dict[int, int] = {}
+        bind: dict[int, int | None] = {}
+        for i, op in enumerate(low.ops):
             streams.setdefault(op.stream, []).append(op)
+            if op.op == OP_RECORD:
+                last_rec[op.value] = i
+            elif op.op == OP_STREAM_WAIT:
+                bind[i] = last_rec.get(op.value)
+        st["op_index"] = {id(op): i for i, op in enumerate(low.ops)}
+        st["bind"] = bind
         st["streams"] = streams
         st["pos"] = {s: 0 for s in streams}
         st["bar_set"] = {s: False for s in streams}
@@ -266,9 +276,11 @@ class World:
                             adv()
                         acts.append(done)
             elif op.op == OP_RECORD:
-                acts.append(lambda op=op, st=st, adv=adv: (st["events"].add(op.value), adv()))
+                idx = st["op_index"][id(op)]
+                acts.append(lambda idx=idx, st=st, adv=adv: (st["events"].add(idx), adv()))
             elif op.op == OP_STREAM_WAIT:
-                if op.value in st["events"]:
+                rec = st["bind"][st["op_index"][id(op)]]
+                if rec is None or rec in st["events"]:
                     acts.append(adv)
             elif op.op == OP_REDUCE_MC:
                 acts.append(lambda op=op, adv=adv: (self._reduce_mc(g, run, op), adv()))

@@ -406,6 +406,30 @@ def test_cp_ragged(lib, kind):
         grp.close()
 
 
+@pytest.mark.parametrize("split", [2, 3])
+def test_ag_2d_slab_split_matches_oracle(lib, split, monkeypatch):
+    """uniform_fused_2d with each R x b slab pulled as `split` row blocks on parallel copy streams."""
+    from paper_2512_10236_b200 import ops
+    monkeypatch.setenv("FICCO_2D_SPLIT", str(split))
+    G, rank, R, K, N = 4, 1, 384, 512, 512
+    shards = [orc.seeded_inputs(17, p, (R, K)) for p in range(G)]
+    w = orc.seeded_inputs(17, 99, (N, K), "normal")
+    gathered_ref, outs = orc.execute_ag("uniform_fused_2d", shards, w)
+    grp = ops.FiccoGroup.virtual_group(G, rank)
+    try:
+        _, low, _ = ops.prepare_ag(grp, R, K, N, "uniform_fused_2d")
+        assert sum(op.op == 0 for op in low.ops) == 1 + split * G * (G - 1)  # publish + split parts per slab
+        grp.load_peer_shards(low, [_t(s) for s in shards])
+        for _ in range(3):
+            out, gathered = ops.all_gather_matmul(_t(shards[rank]), _t(w), kind="uniform_fused_2d", group=grp,
+                                                  return_gathered=True)
+            grp.comm.check()
+            assert np.array_equal(_np(gathered), gathered_ref[rank])
+            np.testing.assert_allclose(_np(out), outs[rank], rtol=RTOL, atol=ATOL)
+    finally:
+        grp.close()
+
+
 @pytest.mark.parametrize("split", [2, 4])
 def test_ag_ring_split_matches_oracle(lib, split, monkeypatch):
     """shard_overlap_p2p with each ring step pulled as `split` row blocks on parallel copy streams."""

@@ -260,3 +260,12 @@ def test_ag_ring_split_protocol(split, G, monkeypatch):
     every part lands before RING[i] and before the right neighbour is notified."""
     monkeypatch.setenv("FICCO_RING_SPLIT", str(split))
     test_ag_protocol("shard_overlap_p2p", G, 2)
+
+
+@pytest.mark.parametrize("split", [2, 3])
+@pytest.mark.parametrize("G", [2, 4])
+def test_ag_2d_slab_split_protocol(split, G, monkeypatch):
+    """uniform_fused_2d with each R x b slab pulled as `split` row blocks on parallel copy streams
+    (FICCO_2D_SPLIT): every part lands before the slab's XFER flag."""
+    monkeypatch.setenv("FICCO_2D_SPLIT", str(split))
+    test_ag_protocol("uniform_fused_2d", G, 2)
