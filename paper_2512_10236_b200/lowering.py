@@ -261,6 +261,24 @@ def slab_split(G: int) -> int:
 EV_SLAB = 40     # + peer chain * (split - 1) + part - 1: uniform_fused_2d slab-part landed (slab_split > 1)
 
 
+def coalesce_groups(G: int) -> list[list[int]]:
+    """Rounds whose chunks of one peer are pulled by ONE copy (FICCO_COALESCE=1): {0}, {1}, {2, 3},
+    {4..7}, ... The plan's routing and every tile's gate are unchanged (each round's flag is still set,
+    right behind the copy that carries it); only consecutive chunks of the same peer, adjacent in memory,
+    share a copy-engine copy. Early rounds stay single so the first remote tiles start as soon as
+    possible; later ones land long before the GEMM reaches them (profiles/r02_experiments/)."""
+    if os.environ.get("FICCO_COALESCE", "0") != "1":
+        return [[c] for c in range(G)]
+    groups, c, size = [], 0, 1
+    while c < G:
+        n = min(size, G - c)
+        groups.append(list(range(c, c + n)))
+        c += n
+        if len(groups) >= 2:
+            size *= 2
+    return groups
+
+
 def fine_chains() -> int:
     """Copy-engine chains of the fine-grain AG copy programs (FICCO_FINE_CHAINS, default 0 = one per peer)."""
     return max(0, min(15, int(os.environ.get("FICCO_FINE_CHAINS", "0"))))
@@ -385,12 +403,34 @@ def lower_ag(plan: ExecutionPlan, rank: int, gathered: str = "A", alpha: float =
                 raise PlanError(f"uniform_fused_2d on B200 needs K/G={b} to be a multiple of {TILE_K}")
             kseg = b // TILE_K
         chains = fine_chains()
+        group_of = {c: grp for grp in coalesce_groups(G) for c in grp}
+        if kind is ScheduleKind.SERIAL or slab_split(G) > 1:
+            group_of = {c: [c] for c in range(G)}
         for x in xfers:
             st = _peer_stream(x.src, g, chains)
             if st not in started:
                 ops.append(_op(OP_STREAM_WAIT, value=EV_START, stream=st))
                 started.add(st)
             c = x.round_idx
+            rounds = group_of.get(c, [c])
+            if kind is not ScheduleKind.SERIAL and len(rounds) > 1:
+                if c != rounds[0]:
+                    continue  # pulled with its group's first round
+                n = len(rounds)
+                if kind is ScheduleKind.UNIFORM_FUSED_2D:
+                    b = K // G
+                    off = low.gather_off + x.src * R * row_bytes + c * b * ELT
+                    src, spar = (low.send_off + g * R * row_bytes + c * b * ELT, low.send_par) if a2a else \
+                        (off, low.gather_par)
+                    ops.append(_op(OP_COPY, peer=x.src, src_buf=BUF_WS, dst_buf=BUF_WS, src_off=src, dst_off=off,
+                                   src_par=spar, dst_par=low.gather_par, width=n * b * ELT, height=R,
+                                   src_pitch=row_bytes, dst_pitch=row_bytes, stream=st))
+                else:
+                    r = M // (G * G)
+                    ops.append(pull(x.src, x.src * R + c * r, n * r, st))
+                for cc in rounds:
+                    ops.append(_op(OP_SIGNAL, flag=F_XFER + cc * G + x.src, stream=st))
+                continue
             if kind is ScheduleKind.SERIAL:
                 ops.append(pull(x.src, x.src * R, R, st))
             elif kind is ScheduleKind.UNIFORM_FUSED_2D:

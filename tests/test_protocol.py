@@ -269,3 +269,21 @@ def test_ag_2d_slab_split_protocol(split, G, monkeypatch):
     (FICCO_2D_SPLIT): every part lands before the slab's XFER flag."""
     monkeypatch.setenv("FICCO_2D_SPLIT", str(split))
     test_ag_protocol("uniform_fused_2d", G, 2)
+
+
+@pytest.mark.parametrize("kind", ["uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d", "uniform_fused_2d"])
+@pytest.mark.parametrize("G", [4, 8])
+def test_ag_coalesced_rounds_protocol(kind, G, monkeypatch):
+    """FICCO_COALESCE=1: consecutive rounds of one peer pulled by one copy ({0}, {1}, {2, 3}, {4..7}),
+    every round's flag set right behind it; AG and all-to-all stay correct under random interleavings."""
+    if kind == "uniform_fused_2d" and G == 8:
+        pytest.skip("the interpreter's K = 256 gives K/G = 32, below the 64-column k-block")
+    monkeypatch.setenv("FICCO_COALESCE", "1")
+    test_ag_protocol(kind, G, 2)
+    test_a2a_protocol(kind, G, 2)
+
+
+@pytest.mark.parametrize("kind", ["uniform_fused_1d", "hetero_unfused_1d"])
+def test_cp_coalesced_rounds_protocol(kind, monkeypatch):
+    monkeypatch.setenv("FICCO_COALESCE", "1")
+    test_cp_protocol(kind, 2)
