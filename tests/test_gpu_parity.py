@@ -406,6 +406,31 @@ def test_cp_ragged(lib, kind):
         grp.close()
 
 
+@pytest.mark.parametrize("kind,G", [("hetero_unfused_1d", 8), ("uniform_fused_1d", 8), ("uniform_fused_2d", 4)])
+def test_ag_coalesced_rounds_match_oracle(lib, kind, G, monkeypatch):
+    """FICCO_COALESCE=1: consecutive rounds of a peer share one copy; gathered bits and C unchanged."""
+    from paper_2512_10236_b200 import ops
+    monkeypatch.setenv("FICCO_COALESCE", "1")
+    rank, R, K, N = 1, 512, 512, 384
+    shards = [orc.seeded_inputs(19, p, (R, K)) for p in range(G)]
+    w = orc.seeded_inputs(19, 99, (N, K), "normal")
+    gathered_ref, outs = orc.execute_ag(kind, shards, w)
+    grp = ops.FiccoGroup.virtual_group(G, rank)
+    try:
+        _, low, _ = ops.prepare_ag(grp, R, K, N, kind)
+        n_groups = {8: 4, 4: 3}[G]
+        assert sum(op.op == 0 for op in low.ops) == 1 + n_groups * (G - 1)  # publish + one copy per group
+        grp.load_peer_shards(low, [_t(s) for s in shards])
+        for _ in range(3):
+            out, gathered = ops.all_gather_matmul(_t(shards[rank]), _t(w), kind=kind, group=grp,
+                                                  return_gathered=True)
+            grp.comm.check()
+            assert np.array_equal(_np(gathered), gathered_ref[rank])
+            np.testing.assert_allclose(_np(out), outs[rank], rtol=RTOL, atol=ATOL)
+    finally:
+        grp.close()
+
+
 @pytest.mark.parametrize("split", [2, 3])
 def test_ag_2d_slab_split_matches_oracle(lib, split, monkeypatch):
     """uniform_fused_2d with each R x b slab pulled as `split` row blocks on parallel copy streams."""
