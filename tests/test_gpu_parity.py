@@ -387,6 +387,57 @@ def test_rs_ragged_chunks(lib, kind, agent):
         grp.close()
 
 
+@pytest.mark.parametrize("kind", ["hetero_unfused_1d", "uniform_fused_1d", "serial", "shard_overlap_p2p"])
+@pytest.mark.parametrize("agent", ["dma", "core"])
+def test_rs_ragged_large_w_row_groups(lib, kind, agent):
+    """W of 33.7 MB (> 32 MiB: the RS tile program goes in row groups of 128-row blocks sweeping N) with
+    96-row chunks, so groups and CTA pairs mix blocks of different pieces, and a K tail of 8."""
+    from paper_2512_10236_b200 import ops
+    from paper_2512_10236_b200.lowering import W_ROW_MAJOR_BYTES
+    G, rank = 4, 1
+    M, Kg, N = 96 * G * G, 2056, 8192
+    assert N * Kg * 2 > W_ROW_MAJOR_BYTES
+    a = [orc.seeded_inputs(21, p, (M, Kg)) for p in range(G)]
+    w = [orc.seeded_inputs(21, 100 + p, (N, Kg), "normal") for p in range(G)]
+    want = orc.execute_rs(a, w)[rank]
+    R = M // G
+    peers = [orc.bf16_round(a[p] @ w[p].T)[rank * R:(rank + 1) * R] for p in range(G) if p != rank]
+    grp = ops.FiccoGroup.virtual_group(G, rank)
+    try:
+        _, low, _ = ops.prepare_rs(grp, M, Kg, N, kind, comm_agent=agent)
+        assert low.desc.hints & 1  # FICCO_HINT_A_EVICT_LAST: the grouped raster pins A
+        grp.load_peer_partials(low, [_t(x) for x in peers])
+        for _ in range(2):
+            out = ops.matmul_reduce_scatter(_t(a[rank]), _t(w[rank]), kind=kind, group=grp, comm_agent=agent)
+            grp.comm.check()
+            np.testing.assert_allclose(_np(out), want, rtol=RTOL, atol=ATOL * math.sqrt(G))
+    finally:
+        grp.close()
+
+
+@pytest.mark.parametrize("kind", ["hetero_unfused_1d", "hetero_fused_1d", "uniform_fused_1d", "shard_overlap_p2p"])
+def test_ag_ragged_large_w_groups_span_gates(lib, kind):
+    """AG->GEMM with W of 33.7 MB: row groups span fragments of different gates (96-row chunks, so CTA
+    pairs and groups mix chunks of different peers); gathered bits and C vs the oracle."""
+    from paper_2512_10236_b200 import ops
+    G, rank, R, K, N = 4, 3, 96 * 4, 2056, 8192
+    shards = [orc.seeded_inputs(23, p, (R, K)) for p in range(G)]
+    w = orc.seeded_inputs(23, 99, (N, K), "normal")
+    gathered_ref, outs = orc.execute_ag(kind, shards, w)
+    grp = ops.FiccoGroup.virtual_group(G, rank)
+    try:
+        _, low, _ = ops.prepare_ag(grp, R, K, N, kind)
+        grp.load_peer_shards(low, [_t(s) for s in shards])
+        for _ in range(2):
+            out, gathered = ops.all_gather_matmul(_t(shards[rank]), _t(w), kind=kind, group=grp,
+                                                  return_gathered=True)
+            grp.comm.check()
+            assert np.array_equal(_np(gathered), gathered_ref[rank])
+            np.testing.assert_allclose(_np(out), outs[rank], rtol=RTOL, atol=ATOL)
+    finally:
+        grp.close()
+
+
 @pytest.mark.parametrize("kind", ["shard_overlap_p2p", "hetero_unfused_1d"])
 def test_cp_ragged(lib, kind):
     """CP QK^T with 96-row kv chunks and a query count that is not a multiple of the tile width."""
