@@ -638,6 +638,8 @@ int make_params(ficco_plan* p, uint32_t parity, const void* a, const void* b, vo
     prm->out_plain = env && env[0] == 'n' ? 1 : 0;
     const char* fast = getenv("FICCO_EPI_FAST");
     prm->epi_fast = fast && fast[0] == '0' ? 0 : 1;
+    const char* x64 = getenv("FICCO_EPI_X64");
+    prm->epi_x64 = x64 && x64[0] == '1' ? 1 : 0;
   }
   prm->b_evict_first = (d.hints & FICCO_HINT_B_EVICT_FIRST) != 0;
   {
@@ -656,7 +658,8 @@ int make_params(ficco_plan* p, uint32_t parity, const void* a, const void* b, vo
 // The launch-time knobs make_params reads (experiments toggle them between calls).
 std::string knob_fingerprint() {
   static const char* const names[] = {"FICCO_B_RESIDENT", "FICCO_PART_HINT", "FICCO_RS_MMA", "FICCO_RS_ALIAS",
-                                      "FICCO_FLAG_TIMEOUT_S", "FICCO_OUT_HINT", "FICCO_EPI_FAST", "FICCO_B_HINT"};
+                                      "FICCO_FLAG_TIMEOUT_S", "FICCO_OUT_HINT", "FICCO_EPI_FAST", "FICCO_B_HINT",
+                                      "FICCO_EPI_X64"};
   std::string f;
   for (const char* n : names) {
     const char* v = getenv(n);

@@ -125,6 +125,7 @@ struct alignas(64) TileParams {
   int b_evict_first;       // FICCO_HINT_B_EVICT_FIRST (1; 2: evict_normal, FICCO_B_HINT experiments)
   int part_hint;           // L2 policy of STORE_SIGNAL (to-be-pushed) stores: 0 evict_first, 1 normal, 2 last
   int epi_fast;            // full 64-column chunks take the straight-line epilogue path (FICCO_EPI_FAST=0: off)
+  int epi_x64;             // the fast path reads its 64 columns with one tcgen05.ld .x64 (FICCO_EPI_X64=1)
   int out_plain;           // STORE / REDUCE output boxes stored without an L2 policy (store-bound programs:
                            // +10 % HBM write rate over evict_first, tools/epi_probe.cu)
   uint32_t* flags;         // local flag block of this run's parity
@@ -491,9 +492,15 @@ __device__ __forceinline__ void epilogue_loop(const TileParams& p, uint64_t* tfu
       if (p.epi_fast && tma && !reduce_row && col + 64 <= td.cols) {
         // fast path (every full 64-column chunk without epilogue reduction): both 32-column TMEM loads
         // in flight before one wait, scale, pack, eight 16-byte swizzled st.shared, one TMA store
-        uint32_t v0[32], v1[32];
-        tmem_ld_32x32b_x32(taddr + col, v0);
-        tmem_ld_32x32b_x32(taddr + col + 32, v1);
+        uint32_t v[64];
+        uint32_t* v0 = v;
+        uint32_t* v1 = v + 32;
+        if (p.epi_x64) {
+          tmem_ld_32x32b_x64(taddr + col, v);
+        } else {
+          tmem_ld_32x32b_x32(taddr + col, *reinterpret_cast<uint32_t(*)[32]>(v0));
+          tmem_ld_32x32b_x32(taddr + col + 32, *reinterpret_cast<uint32_t(*)[32]>(v1));
+        }
         tmem_ld_wait();
         const uint32_t srow = smem_addr(buf + bi * EPI_BUF_BYTES) + uint32_t(lane) * 128u;
         const uint32_t l7 = uint32_t(lane) & 7u;

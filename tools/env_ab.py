@@ -52,7 +52,8 @@ def main():
         res[name] = {f"{var}={v}": round(statistics.median(x), 1) for v, x in t.items()}
         print(name, res[name], flush=True)
     for wl, grp in wls.values():
-        grp.comm.check()
+        if grp.comm is not None:  # plain-GEMM-only workloads never built a communicator
+            grp.comm.check()
         grp.close()
     with open(os.path.join(ROOT, "gpurun_out", f"env_ab_{var}.json"), "w") as f:
         json.dump(res, f, indent=1)
