@@ -82,7 +82,7 @@ AG_KINDS = ["serial", "shard_overlap_p2p", "uniform_fused_1d", "hetero_fused_1d"
 
 @pytest.mark.parametrize("kind", AG_KINDS)
 @pytest.mark.parametrize("G,rank,R,K,N", [(4, 0, 512, 1024, 768), (4, 3, 512, 1024, 768), (2, 1, 256, 512, 256),
-                                          (8, 5, 128, 512, 512)])
+                                          (8, 5, 128, 512, 512), (3, 2, 384, 768, 384), (6, 5, 384, 768, 256)])
 def test_ag_virtual_matches_oracle(lib, kind, G, rank, R, K, N):
     from paper_2512_10236_b200 import ops
     shards = [orc.seeded_inputs(0, p, (R, K)) for p in range(G)]
@@ -141,6 +141,30 @@ def test_rs_virtual_matches_oracle(lib, kind, G, rank):
         grp.load_peer_partials(low, [_t(x) for x in peers])
         for _ in range(2):
             out = ops.matmul_reduce_scatter(_t(a[rank]), _t(w[rank]), kind=kind, group=grp)
+            grp.comm.check()
+            np.testing.assert_allclose(_np(out), want, rtol=RTOL, atol=ATOL * math.sqrt(G))
+    finally:
+        grp.close()
+
+
+@pytest.mark.parametrize("kind", RS_KINDS)
+@pytest.mark.parametrize("agent", ["dma", "core"])
+@pytest.mark.parametrize("G,rank", [(3, 1), (6, 4)])
+def test_rs_odd_world_sizes_match_oracle(lib, kind, agent, G, rank):
+    """GEMM -> RS with G = 3 and 6 ranks (flag blocks, receive slots and pair tiles at non-power-of-2 G)."""
+    from paper_2512_10236_b200 import ops
+    M, Kg, N = 128 * G * G, 256, 768
+    a = [orc.seeded_inputs(25, p, (M, Kg)) for p in range(G)]
+    w = [orc.seeded_inputs(25, 100 + p, (N, Kg), "normal") for p in range(G)]
+    want = orc.execute_rs(a, w)[rank]
+    R = M // G
+    peers = [orc.bf16_round(a[p] @ w[p].T)[rank * R:(rank + 1) * R] for p in range(G) if p != rank]
+    grp = ops.FiccoGroup.virtual_group(G, rank)
+    try:
+        _, low, _ = ops.prepare_rs(grp, M, Kg, N, kind, comm_agent=agent)
+        grp.load_peer_partials(low, [_t(x) for x in peers])
+        for _ in range(2):
+            out = ops.matmul_reduce_scatter(_t(a[rank]), _t(w[rank]), kind=kind, group=grp, comm_agent=agent)
             grp.comm.check()
             np.testing.assert_allclose(_np(out), want, rtol=RTOL, atol=ATOL * math.sqrt(G))
     finally:
