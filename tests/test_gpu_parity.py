@@ -171,6 +171,27 @@ def test_rs_odd_world_sizes_match_oracle(lib, kind, agent, G, rank):
         grp.close()
 
 
+@pytest.mark.parametrize("kind", ["uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d", "shard_overlap_p2p",
+                                  "serial"])
+def test_cp_qk_three_ranks_matches_oracle(lib, kind):
+    """CP QK^T at G = 3 (kv chunks of 512 rows, non-power-of-2 world)."""
+    from paper_2512_10236_b200 import ops
+    G, rank, d, Tq, Tkv = 3, 2, 128, 384, 4608
+    q = orc.seeded_inputs(27, 50, (Tq, d), "normal")
+    ks = [orc.seeded_inputs(27, p, (Tkv // G, d), "normal") for p in range(G)]
+    want, _ = orc.execute_cp_qk(q, ks, 1.0 / math.sqrt(d))
+    grp = ops.FiccoGroup.virtual_group(G, rank)
+    try:
+        _, low, _ = ops.prepare_cp(grp, Tq, d, Tkv, kind)
+        grp.load_peer_shards(low, [_t(x) for x in ks])
+        for _ in range(2):
+            out = ops.cp_kv_all_gather_qk(_t(q), _t(ks[rank]), kind=kind, group=grp)
+            grp.comm.check()
+            np.testing.assert_allclose(_np(out), want, rtol=RTOL, atol=ATOL)
+    finally:
+        grp.close()
+
+
 @pytest.mark.parametrize("kind", ["uniform_fused_1d", "hetero_fused_1d", "hetero_unfused_1d", "serial"])
 def test_cp_qk_virtual_matches_oracle(lib, kind):
     from paper_2512_10236_b200 import ops
@@ -312,7 +333,7 @@ def test_cp_core_agent_matches_oracle(lib):
 
 
 @pytest.mark.parametrize("kind", AG_KINDS)
-@pytest.mark.parametrize("G,rank,R,K,N", [(4, 2, 256, 512, 384), (8, 0, 128, 512, 256)])
+@pytest.mark.parametrize("G,rank,R,K,N", [(4, 2, 256, 512, 384), (8, 0, 128, 512, 256), (3, 1, 384, 768, 256)])
 @pytest.mark.parametrize("agent", ["dma", "core"])
 def test_a2a_virtual_matches_oracle(lib, kind, G, rank, R, K, N, agent):
     """EP all-to-all -> expert GEMM: dispatched tokens bit-exact, expert GEMM within tolerance."""
